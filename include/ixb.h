@@ -1,0 +1,208 @@
+/*
+ * ixb.h — C-ABI of the B200-native executor for Insum's indirect Einsums.
+ *
+ * Drop-in boundary for the hot path of the reference toolkit `ixsum`
+ * (/root/reference/proj/include/ixsum): the format builders and the four
+ * indirect-Einsum evaluators. Plain pointers and sizes only — no C++ or torch
+ * types. All device pointers are CUDA device memory on the current device;
+ * every call is stream-ordered on `stream` (NULL = legacy default stream).
+ *
+ * Index arrays are int32 on the device (the reference stores int64,
+ * formats.hpp:43-45); values are fp32 or bf16 with fp32 accumulation (the
+ * reference is fp64/int64, tensor.hpp:11). See DESIGN.md for layouts.
+ *
+ * Return codes map 1:1 onto the reference's exception classes and CLI exit
+ * codes (driver.hpp:19-27, report_error driver.cpp:571-580):
+ *   IXB_OK 0, IXB_FAILURE 1 (std::runtime_error / std::invalid_argument),
+ *   IXB_PARSE 2 (ParseError), IXB_BIND 3 (BindError), IXB_SHAPE 4
+ *   (ShapeError / InferenceError), IXB_INDEX_RANGE 6 (IndexRangeError),
+ *   IXB_CUDA 7 (device failure — no reference equivalent).
+ * The message of the last failure on the calling thread is ixb_last_error().
+ */
+#ifndef IXB_H
+#define IXB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ixb_stream; /* == cudaStream_t */
+
+enum ixb_status {
+  IXB_OK = 0,
+  IXB_FAILURE = 1,
+  IXB_PARSE = 2,
+  IXB_BIND = 3,
+  IXB_SHAPE = 4,
+  IXB_INDEX_RANGE = 6,
+  IXB_CUDA = 7
+};
+
+enum ixb_dtype { IXB_F32 = 0, IXB_BF16 = 1 };
+
+/* Evaluator flags. */
+enum ixb_flags {
+  /* Evaluator returns without synchronising; index-range errors found by the
+   * kernel are reported by the next ixb_check_errors() call. */
+  IXB_ASYNC = 1,
+  /* Caller asserts the group-coordinate array (AM / MAPX-groups / CGL ...)
+   * is non-decreasing, as every ixb builder produces it. Without the flag
+   * the evaluator verifies it (one extra pass + sync) and falls back to a
+   * stable permutation when it is not sorted. */
+  IXB_GROUPS_SORTED = 2,
+  /* Skip the in-kernel index range checks (inputs already validated). */
+  IXB_UNCHECKED = 4
+};
+
+const char* ixb_last_error(void);
+int ixb_version(void);
+/* Details of the last IXB_INDEX_RANGE failure on this thread: which operand
+ * (evaluator-specific order, gathers before scatters), flat position, value
+ * and the extent it violated. */
+int ixb_last_index_error(int* operand, int64_t* position, int64_t* value, int64_t* extent);
+/* Reports (and clears) index-range errors recorded by IXB_ASYNC calls on this
+ * device; synchronises `stream`. */
+int ixb_check_errors(ixb_stream stream);
+/* Number of SMs of the current device (148 on B200). */
+int ixb_sm_count(void);
+/* Number of ixb kernels launched by this process (for launch accounting). */
+int64_t ixb_launch_count(void);
+
+/* ======================================================================
+ * Builders (K1/K2 + rank-n grouping). Two phases: *_plan computes sizes
+ * (one device->host sync) and keeps device temporaries in the opaque
+ * ixb_pack; *_pack writes caller-allocated outputs and may be called with
+ * several value arrays; ixb_pack_free releases it.
+ * Outputs reproduce the reference bit-for-bit (after int32->int64 widening).
+ * ==================================================================== */
+typedef struct ixb_pack ixb_pack;
+void ixb_pack_free(ixb_pack* plan);
+
+/* dense_to_coo (formats.hpp:26, formats.cpp:24-46): row-major scan of a
+ * dense [rows, cols] matrix, entries != 0 kept. */
+int ixb_dense_to_coo_plan(const void* dense, int dtype, int64_t rows, int64_t cols,
+                          ixb_stream stream, ixb_pack** plan, int64_t* nnz);
+int ixb_dense_to_coo_pack(ixb_pack* plan, int32_t* row_coord, int32_t* col_coord, void* values,
+                          ixb_stream stream);
+
+/* coo_to_groupcoo (formats.hpp:53, formats.cpp:115-174): stable sort by
+ * (group coordinate, member coordinate), runs split into ceil(occ/g) groups,
+ * tail padded with the last real member and value 0. `canonical` != 0 asserts
+ * the input is already sorted by (row, col) (CooMatrix::canonical).
+ * g == 0 selects g with the reference tuner (tuner.cpp:100-118; the
+ * `format: auto` path of driver.cpp:106-113); *g_out returns the g used. */
+int ixb_groupcoo_plan(const int32_t* row_coord, const int32_t* col_coord, int64_t nnz,
+                      int64_t rows, int64_t cols, int canonical, int group_dim, int64_t g,
+                      ixb_stream stream, ixb_pack** plan, int64_t* num_groups, int64_t* g_out);
+/* AV: [G, g] of `dtype`; mask: [G, g] u8 (1 = real) or NULL. `values` may be
+ * NULL when only the index arrays are wanted. */
+int ixb_groupcoo_pack(ixb_pack* plan, const void* values, int dtype, int32_t* AM, int32_t* AK,
+                      void* AV, uint8_t* mask, ixb_stream stream);
+
+/* dense_to_coo + coo_to_groupcoo fused for a dense [rows, cols] source
+ * (group_dim 0 or 1; g == 0 -> tuner). */
+int ixb_dense_groupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t cols,
+                            int group_dim, int64_t g, ixb_stream stream, ixb_pack** plan,
+                            int64_t* num_groups, int64_t* g_out, int64_t* nnz);
+int ixb_dense_groupcoo_pack(ixb_pack* plan, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask,
+                            ixb_stream stream);
+
+/* dense_to_blockgroupcoo (formats.hpp:81-83, formats.cpp:224-292): a bM x bK
+ * block is stored iff any element != 0 (in the device dtype); block COO is
+ * grouped like coo_to_groupcoo; ragged edges and pad slots are zero.
+ * g == 0 -> tuner on block occupancy. AV: [G, g, bM, bK] of `dtype`. */
+int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t bm,
+                           int64_t bk, int64_t g, int group_dim, ixb_stream stream,
+                           ixb_pack** plan, int64_t* num_groups, int64_t* g_out,
+                           int64_t* num_blocks);
+int ixb_blockgroupcoo_pack(ixb_pack* plan, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask,
+                           ixb_stream stream);
+
+/* group_coo_tensor (formats.hpp:141, formats.cpp:417-479): rank-n COO
+ * (coords: `rank` device arrays of nnz int32) grouped along group_dim; sort
+ * key (group coord, then the other dims in order), stable. */
+int ixb_group_coo_tensor_plan(int rank, const int64_t* shape, const int32_t* const* coords,
+                              int64_t nnz, int group_dim, int64_t g, ixb_stream stream,
+                              ixb_pack** plan, int64_t* num_groups);
+/* member_coords: rank-1 device arrays [G, g] (dims in order, group_dim skipped). */
+int ixb_group_coo_tensor_pack(ixb_pack* plan, const void* values, int dtype,
+                              int32_t* group_coord, int32_t* const* member_coords, void* out_values,
+                              uint8_t* mask, ixb_stream stream);
+
+/* Reference tuner over a device occupancy source (tuner.cpp:31-118):
+ * coord: nnz int32 coordinates in [0, extent). */
+int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
+                        ixb_stream stream, int64_t* g_out, double* gstar_out);
+
+/* ======================================================================
+ * Evaluators. Each validates indices in-kernel (unless IXB_UNCHECKED);
+ * `accumulate` != 0 is `+=` (the output's contents prime the sum),
+ * accumulate == 0 is `=` (plan.cpp:540). Results are run-to-run
+ * deterministic: no floating-point atomics; each output row has one owner
+ * that sums its groups in group order.
+ * ==================================================================== */
+
+/* K3 — GroupCOO SpMM, `C[AM[p],n] += AV[p,q] * B[AK[p,q],n]`
+ * (corpus/unstructured_spmm.json:2). AV [G,g], B [K,N], C [M,N], fp32.
+ * g == 1 is the COO SpMM `C[AM[p],n] += AV[p] * B[AK[p],n]`.
+ * Operands for ixb_last_index_error: 0 = AK, 1 = AM. */
+int ixb_spmm_groupcoo(const int32_t* AM, const int32_t* AK, const float* AV, int64_t G, int64_t g,
+                      const float* B, int64_t K, int64_t N, float* C, int64_t M, int accumulate,
+                      int flags, ixb_stream stream);
+
+/* K4 — BlockGroupCOO SpMM on tcgen05/TMEM,
+ * `C[AM[p],bm,n] += AV[p,q,bm,bk] * B[AK[p,q],bk,n]` (corpus/structured_spmm.json:2).
+ * AV [G,g,16,16] bf16, B [KB,16,N] bf16, C [MB,16,N] fp32. bm = bk = 16,
+ * N % 128 == 0. Operands: 0 = AK, 1 = AM. */
+int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, int64_t G,
+                           int64_t g, int64_t bm, int64_t bk, const void* B, int64_t KB,
+                           int64_t N, float* C, int64_t MB, int accumulate, int flags,
+                           ixb_stream stream);
+
+/* K5 — submanifold 3x3x3 kernel map over n voxels (coords [n,3] int32,
+ * unique). Pairs (out i, in j, offset z) with coord[j] == coord[i] + delta(z),
+ * z = (dx+1)*9 + (dy+1)*3 + (dz+1), ordered by (z, i) — the canonical order
+ * of group_coo_tensor(map, 2, g) input. */
+int ixb_kernel_map_plan(const int32_t* coords, int64_t n, ixb_stream stream, ixb_pack** plan,
+                        int64_t* num_pairs);
+int ixb_kernel_map_pack(ixb_pack* plan, int32_t* map_out, int32_t* map_in, int32_t* map_off,
+                        ixb_stream stream);
+
+/* K6 — grouped sparse convolution,
+ * `Out[MAPX[p,q],m] += MAPV[p,q] * In[MAPY[p,q],c] * Weight[MAPZ[p],c,m]`
+ * (corpus/grouped_sparse_conv.json:2). In [n_in, Cin] bf16, Weight
+ * [n_off, Cin, Cout] bf16, MAPV [G,g] fp32 (NULL = all ones), Out
+ * [n_out, Cout] fp32. Operands: 0 = MAPY, 1 = MAPZ, 2 = MAPX. */
+int ixb_conv_grouped(const int32_t* MAPZ, const int32_t* MAPX, const int32_t* MAPY,
+                     const float* MAPV, int64_t G, int64_t g, const void* In, int64_t n_in,
+                     int64_t Cin, const void* Weight, int64_t n_off, int64_t Cout, float* Out,
+                     int64_t n_out, int accumulate, int flags, ixb_stream stream);
+
+/* K7 — grouped Clebsch–Gordan tensor product,
+ * `Z[b,CGI[p,q],w] += CGV[p,q] * X[b,CGJ[p,q],u] * Y[b,CGK[p,q]] * W[CGL[p],u,w]`
+ * (corpus/grouped_tensor_product.json:2 with `w_per_batch` = 1; the
+ * shared-weight form `W[CGL[p],u,w]` with w_per_batch = 0). X [B,nj,U] bf16,
+ * Y [B,nk] bf16, W [(B,)nl,U,Wd] bf16, CGV [G,g] fp32, Z [B,ni,Wd] fp32.
+ * Operands: 0 = CGJ, 1 = CGK, 2 = CGL, 3 = CGI. */
+int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ, const int32_t* CGK,
+                   const float* CGV, int64_t G, int64_t g, const void* X, const void* Y,
+                   const void* W, int w_per_batch, int64_t batch, int64_t ni, int64_t nj,
+                   int64_t nk, int64_t nl, int64_t U, int64_t Wd, float* Z, int accumulate,
+                   int flags, ixb_stream stream);
+
+/* ======================================================================
+ * Multi-GPU sharding (host-side planning). Cuts G sorted
+ * groups into `parts` contiguous ranges of ~equal slot count, cutting only
+ * where the group coordinate changes, so no output row spans two ranks and
+ * per-row summation order (hence every bit of the result) is independent
+ * of `parts`. group_coord is a HOST array here. bounds: parts+1 entries.
+ * ==================================================================== */
+int ixb_shard_groups(const int32_t* group_coord_host, int64_t G, int parts, int64_t* bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IXB_H */

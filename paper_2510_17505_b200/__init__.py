@@ -1,0 +1,31 @@
+"""ixsum-b200 — B200-native executor for Insum's indirect Einsums.
+
+Python mirror of the reference's hot-path API (/root/reference/proj/include/
+ixsum/{formats,plan,driver}.hpp) over the C-ABI in include/ixb.h
+(libixb.so, hand-written sm_100a kernels). torch is used only for device
+memory and streams. There is no CPU fallback: if libixb.so is missing, or
+no CUDA device is present, every call raises.
+
+Names and argument meaning follow the reference:
+  dense_to_coo, coo_to_groupcoo, dense_to_blockgroupcoo, group_coo_tensor,
+  emit_operands, execute_mode("b200", ...)
+Errors raise the reference's exception classes (ParseError, BindError,
+ShapeError, IndexRangeError) with the reference's message content.
+"""
+from .abi import (BindError, IxbError, IndexRangeError, ParseError, ShapeError, lib,
+                  lib_path)
+from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupcoo,
+                  dense_to_coo, dense_to_groupcoo, coo_to_groupcoo, emit_operands,
+                  group_coo_tensor, kernel_map, tune_group_size, spmm_groupcoo,
+                  spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups,
+                  count_accesses_model)
+from .executor import execute_mode, match_workload, WORKLOADS
+
+__all__ = [
+    "lib", "lib_path", "IxbError", "ParseError", "BindError", "ShapeError", "IndexRangeError",
+    "GroupCoo", "BlockGroupCoo", "GroupCooTensor", "dense_to_coo", "coo_to_groupcoo",
+    "dense_to_groupcoo", "dense_to_blockgroupcoo", "group_coo_tensor", "emit_operands",
+    "kernel_map", "tune_group_size", "spmm_groupcoo", "spmm_blockgroupcoo", "conv_grouped",
+    "tp_grouped", "shard_groups", "count_accesses_model", "execute_mode", "match_workload",
+    "WORKLOADS",
+]

@@ -1,0 +1,102 @@
+// Internal host/device definitions shared by the ixb translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ixb.h"
+
+namespace ixb {
+
+// Device-side record of the first index-range offender (see common.cuh).
+struct ErrorRecord {
+  unsigned long long key;  // (operand << 56) | flat position; ~0 = none
+  long long value[8];
+};
+
+constexpr unsigned long long kNoError = ~0ull;
+
+// Host exception carrying an ixb_status; converted at the C-ABI boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define IXB_CUDA_CHECK(x) ::ixb::cuda_check((x), #x)
+#define IXB_LAUNCH_CHECK(name) \
+  do {                         \
+    ::ixb::note_launch();      \
+    ::ixb::cuda_check(cudaGetLastError(), name); \
+  } while (0)
+
+void note_launch(int n = 1);
+int sm_count();
+
+// Per-device error record (lazily allocated, reset after each check).
+ErrorRecord* device_error_record();
+// Resets the record on `stream` before a checked launch.
+void reset_error_record(cudaStream_t stream);
+// Syncs `stream`, reads the record; on an offender throws IXB_INDEX_RANGE with
+// the reference message (plan.cpp:253-256). names/index arrays/extents are
+// per operand; idx_arrays are the device index arrays the operand id refers to.
+struct OperandInfo {
+  const char* index_name;   // e.g. "AK"
+  const char* target_name;  // e.g. "B"
+  int target_dim;           // dim of the target indexed
+  int64_t extent;           // its extent
+  const int32_t* device_array;
+  int64_t numel;
+};
+void check_error_record(cudaStream_t stream, const OperandInfo* ops, int nops);
+
+// Stream-ordered scratch allocation (cudaMallocAsync pool).
+void* scratch_alloc(size_t bytes, cudaStream_t stream);
+void scratch_free(void* p, cudaStream_t stream);
+
+template <typename T>
+struct Scratch {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch() = default;
+  Scratch(size_t n, cudaStream_t st) : s(st) {
+    p = static_cast<T*>(scratch_alloc(n * sizeof(T) + 16, st));
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  Scratch(Scratch&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+  Scratch& operator=(Scratch&& o) noexcept {
+    reset();
+    p = o.p;
+    s = o.s;
+    o.p = nullptr;
+    return *this;
+  }
+  void reset() {
+    if (p) scratch_free(p, s);
+    p = nullptr;
+  }
+  ~Scratch() { reset(); }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace ixb
+
+// ABI guard: converts exceptions into status codes + thread-local message.
+int ixb_guard_set(int code, const char* msg);
+template <typename F>
+int ixb_guard(F&& f) {
+  try {
+    f();
+    return ixb_guard_set(IXB_OK, "");
+  } catch (const ixb::Error& e) {
+    return ixb_guard_set(e.code, e.what());
+  } catch (const std::exception& e) {
+    return ixb_guard_set(IXB_FAILURE, e.what());
+  }
+}

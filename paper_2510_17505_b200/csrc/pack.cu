@@ -1,0 +1,887 @@
+// Device-side format builders (K1 GroupCOO, K2 BlockGroupCOO, rank-n
+// grouping) and the group-size tuner. Outputs reproduce the reference
+// builders bit-for-bit (formats.cpp:24-46, 115-174, 224-292, 417-479;
+// tuner.cpp:31-118).
+//
+// Two grouping engines, both HBM-bound integer work:
+//  * dense-row engine (dense source, group_dim 0): one warp per row counts
+//    the row's nonzeros with 16-byte loads (occ), two scans give row and
+//    group offsets, and a second warp-per-row pass compacts the nonzeros in
+//    column order straight into their (group, slot) — the sort of
+//    formats.cpp:124-129 is the identity for a row-major scan.
+//  * sorted-run engine (COO / rank-n sources): stable LSD radix sort of a
+//    permutation over the key dims (CUB, stable per pass ⇒ lexicographic and
+//    stable like std::stable_sort), head flags + scans for the runs of equal
+//    group coordinate, then element-parallel slot writes.
+// Padding repeats the last real member and stores value 0 / mask 0
+// (formats.cpp:155-160, 454-468).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ixb {
+
+// ------------------------------------------------------------------ tuner
+struct OccStats {
+  unsigned long long S = 0, nonzero = 0, maxocc = 0;
+  unsigned long long groups_pow2[32] = {};  // sum_r ceil(occ_r / 2^i)
+};
+
+namespace {
+
+constexpr int kTB = 256;
+
+__global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
+  __shared__ unsigned long long sh[35];
+  for (int i = threadIdx.x; i < 35; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  unsigned long long S = 0, nz = 0, mx = 0, grp[32] = {};
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long o = static_cast<unsigned long long>(occ[r]);
+    S += o;
+    nz += o > 0;
+    mx = o > mx ? o : mx;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) grp[i] += (o + (1ull << i) - 1) >> i;
+  }
+  atomicAdd(&sh[0], S);
+  atomicAdd(&sh[1], nz);
+  atomicMax(&sh[2], mx);
+  for (int i = 0; i < 32; ++i) {
+    if (grp[i]) atomicAdd(&sh[3 + i], grp[i]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&out->S, sh[0]);
+    atomicAdd(&out->nonzero, sh[1]);
+    atomicMax(&out->maxocc, sh[2]);
+  }
+  if (threadIdx.x < 32 && sh[3 + threadIdx.x]) atomicAdd(&out->groups_pow2[threadIdx.x], sh[3 + threadIdx.x]);
+}
+
+}  // namespace
+
+// select() of tuner.cpp:100-118 over device occupancy counts.
+int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_empty_rows,
+                      cudaStream_t s, double* gstar_out) {
+  Scratch<OccStats> d(1, s);
+  IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
+  if (n > 0) {
+    int64_t grid = ceil_div(n, kTB);
+    if (grid > 4 * sm_count()) grid = 4 * sm_count();
+    occ_stats_kernel<<<grid, kTB, 0, s>>>(occ, n, d.p);
+    IXB_LAUNCH_CHECK("occ_stats_kernel");
+  }
+  OccStats h;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  // g_star (tuner.cpp:60-65)
+  double gs = 1.0;
+  if (h.S > 0) {
+    double nn = count_empty_rows ? static_cast<double>(extent) : static_cast<double>(h.nonzero);
+    gs = nn <= 0 ? 1.0 : std::sqrt(static_cast<double>(h.S) / nn);
+  }
+  if (gstar_out) *gstar_out = gs;
+  if (h.S == 0) return 1;  // candidate_group_sizes: {1}
+  // candidate_group_sizes (tuner.cpp:67-84)
+  int64_t lo = 1;
+  while (lo * 2 <= static_cast<int64_t>(gs)) lo *= 2;
+  int64_t hi = lo;
+  while (static_cast<double>(hi) < gs) hi *= 2;
+  int64_t cap = 1;
+  while (cap * 2 <= static_cast<int64_t>(h.maxocc)) cap *= 2;
+  lo = lo < 1 ? 1 : (lo > cap ? cap : lo);
+  hi = hi < 1 ? 1 : (hi > cap ? cap : hi);
+  auto cost = [&](int64_t g) {  // cost_exact (tuner.cpp:31-36), g a power of two
+    int sh = 0;
+    while ((1ll << sh) < g) ++sh;
+    return static_cast<double>((g + 1) * static_cast<int64_t>(h.groups_pow2[sh]));
+  };
+  int64_t chosen = lo;
+  double best = cost(lo);
+  if (hi != lo && cost(hi) < best) chosen = hi;
+  return chosen;
+}
+
+namespace {
+
+// ------------------------------------------------------------ elem helpers
+template <typename T>
+__device__ __forceinline__ bool nz(T v);
+template <>
+__device__ __forceinline__ bool nz<float>(float v) { return v != 0.0f; }
+template <>
+__device__ __forceinline__ bool nz<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v) != 0.0f;
+}
+template <>
+__device__ __forceinline__ bool nz<uint8_t>(uint8_t v) { return v != 0; }
+
+template <typename T>
+struct Vec16 {
+  static constexpr int V = 16 / sizeof(T);
+  T x[V];
+};
+
+// occ[row] = number of nonzeros of row `row` (formats.cpp:33-41 scan order).
+template <typename T, int V>
+__global__ void row_count_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
+                                 int32_t* occ) {
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (row >= rows) return;
+  const int lane = lane_id();
+  const T* p = dense + row * cols;
+  int cnt = 0;
+  for (int64_t c = static_cast<int64_t>(lane) * V; c < cols; c += 32 * V) {
+    if (V > 1) {
+      Vec16<T> v = *reinterpret_cast<const Vec16<T>*>(p + c);
+#pragma unroll
+      for (int j = 0; j < (V > 1 ? V : 1); ++j) cnt += nz<T>(v.x[j]);
+    } else {
+      cnt += nz<T>(p[c]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) occ[row] = cnt;
+}
+
+// Dense-row pack. mode 0: GroupCOO slots (gofs, g); mode 1: plain COO at rowptr.
+template <typename T, int V>
+__global__ void row_pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
+                                const int32_t* __restrict__ occ,
+                                const int32_t* __restrict__ offs,  // gofs (mode 0) / rowptr (1)
+                                int64_t g, int mode, int32_t* AM, int32_t* AK, T* AV,
+                                uint8_t* mask) {
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (row >= rows) return;
+  const int lane = lane_id();
+  const int n = occ[row];
+  if (n == 0) return;
+  const T* p = dense + row * cols;
+  const int64_t base = offs[row];
+  int64_t k0 = 0;
+  int last_col = 0;
+  for (int64_t c = static_cast<int64_t>(lane) * V; c - lane * V < cols; c += 32 * V) {
+    T vals[V];
+    if (V > 1) {
+      if (c < cols) {
+        Vec16<T> v = *reinterpret_cast<const Vec16<T>*>(p + c);
+#pragma unroll
+        for (int j = 0; j < V; ++j) vals[j] = v.x[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) vals[j] = T(0);
+      }
+    } else {
+      vals[0] = c < cols ? p[c] : T(0);
+    }
+    int mine = 0;
+#pragma unroll
+    for (int j = 0; j < V; ++j) mine += nz<T>(vals[j]);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int64_t k = k0 + incl - mine;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (!nz<T>(vals[j])) continue;
+      const int col = static_cast<int>(c + j);
+      if (mode == 0) {
+        const int64_t slot = (base + k / g) * g + k % g;
+        AK[slot] = col;
+        if (AV) AV[slot] = vals[j];
+        if (mask) mask[slot] = 1;
+      } else {
+        AM[base + k] = static_cast<int32_t>(row);
+        AK[base + k] = col;
+        if (AV) AV[base + k] = vals[j];
+      }
+      last_col = col;
+      ++k;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    // the lane holding the row's last nonzero so far
+    const unsigned has = __ballot_sync(0xffffffffu, mine > 0);
+    if (has) last_col = __shfl_sync(0xffffffffu, last_col, 31 - __clz(has));
+    k0 += total;
+  }
+  if (mode == 0) {
+    const int64_t ng = (n + g - 1) / g;
+    for (int64_t j = lane; j < ng; j += 32) AM[base + j] = static_cast<int32_t>(row);
+    const int64_t real_last = n - (ng - 1) * g;  // real entries in the last group
+    const int64_t lastg = base + ng - 1;
+    for (int64_t q = real_last + lane; q < g; q += 32) {
+      const int64_t slot = lastg * g + q;
+      AK[slot] = last_col;
+      if (AV) AV[slot] = T(0);
+      if (mask) mask[slot] = 0;
+    }
+  }
+}
+
+__global__ void occupancy_kernel(const int32_t* c, int64_t n, int64_t ext, int32_t* o) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && c[i] >= 0 && c[i] < ext) atomicAdd(o + c[i], 1);
+}
+
+__global__ void groups_per_run_kernel(const int32_t* occ, int64_t n, int64_t g, int32_t* ng) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) ng[i] = static_cast<int32_t>((static_cast<int64_t>(occ[i]) + g - 1) / g);
+}
+
+// ---------------------------------------------------------- sorted runs
+__global__ void iota32(int32_t* x, int64_t n) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = static_cast<int32_t>(i);
+}
+
+__global__ void gather_key(const int32_t* coord, const int32_t* perm, int64_t n, int32_t* key) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) key[i] = coord[perm[i]];
+}
+
+__global__ void head_flags(const int32_t* gcoord, const int32_t* perm, int64_t n, int32_t* flag) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t a = gcoord[perm ? perm[i] : i];
+  flag[i] = (i == 0 || a != gcoord[perm ? perm[i - 1] : i - 1]) ? 1 : 0;
+}
+
+__global__ void run_starts(const int32_t* flag, const int32_t* run_incl, int64_t n,
+                           int32_t* start) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) start[run_incl[i] - 1] = static_cast<int32_t>(i);
+}
+
+__global__ void run_lengths(const int32_t* start, int64_t R, int64_t n, int32_t* len) {
+  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < R) len[r] = (r + 1 < R ? start[r + 1] : static_cast<int32_t>(n)) - start[r];
+}
+
+struct RunPackArgs {
+  const int32_t* perm;      // sorted pos -> source (null = identity)
+  const int32_t* run_incl;  // inclusive run count per sorted pos (run id + 1)
+  const int32_t* start;     // [R]
+  const int32_t* len;       // [R]
+  const int32_t* gofs;      // [R] exclusive group offsets
+  const int32_t* gcoord;    // source group coordinates
+  const int32_t* mcoord[8]; // source member coordinates
+  int32_t* mout[8];         // member outputs [G, g]
+  int nm;
+  int64_t n, R, g;
+  const void* vals;
+  void* vout;
+  int vbytes;  // 0 (no values), 2 (bf16) or 4 (f32)
+  uint8_t* mask;
+  int32_t* gout;  // group coordinate output [G]
+};
+
+__global__ void run_pack_elems(RunPackArgs a) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const int64_t r = a.run_incl[i] - 1;
+  const int64_t k = i - a.start[r];
+  const int64_t slot = (a.gofs[r] + k / a.g) * a.g + k % a.g;
+  const int64_t src = a.perm ? a.perm[i] : i;
+  for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][src];
+  if (a.vbytes == 4) {
+    static_cast<float*>(a.vout)[slot] = static_cast<const float*>(a.vals)[src];
+  } else if (a.vbytes == 2) {
+    static_cast<__nv_bfloat16*>(a.vout)[slot] = static_cast<const __nv_bfloat16*>(a.vals)[src];
+  }
+  if (a.mask) a.mask[slot] = 1;
+}
+
+__global__ void run_pack_runs(RunPackArgs a) {
+  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= a.R) return;
+  const int64_t len = a.len[r];
+  const int64_t ng = (len + a.g - 1) / a.g;
+  const int64_t g0 = a.gofs[r];
+  const int64_t first = a.start[r], last = first + len - 1;
+  const int64_t src0 = a.perm ? a.perm[first] : first;
+  const int64_t srcl = a.perm ? a.perm[last] : last;
+  const int32_t gc = a.gcoord[src0];
+  for (int64_t j = 0; j < ng; ++j) a.gout[g0 + j] = gc;
+  const int64_t real_last = len - (ng - 1) * a.g;
+  for (int64_t q = real_last; q < a.g; ++q) {
+    const int64_t slot = (g0 + ng - 1) * a.g + q;
+    for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][srcl];
+    if (a.vbytes == 4) static_cast<float*>(a.vout)[slot] = 0.f;
+    else if (a.vbytes == 2)
+      static_cast<__nv_bfloat16*>(a.vout)[slot] = __float2bfloat16(0.f);
+    if (a.mask) a.mask[slot] = 0;
+  }
+}
+
+// ------------------------------------------------------------- blocks (K2)
+template <typename T>
+__global__ void block_flags_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
+                                   int64_t bm, int64_t bk, int64_t gr, int64_t gcn,
+                                   uint8_t* flags) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= gr * gcn) return;
+  const int64_t br = b / gcn, bc = b % gcn;
+  const int64_t ie = (br + 1) * bm < rows ? (br + 1) * bm : rows;
+  const int64_t je = (bc + 1) * bk < cols ? (bc + 1) * bk : cols;
+  bool any = false;
+  for (int64_t i = br * bm; i < ie && !any; ++i) {
+    const T* p = dense + i * cols;
+    for (int64_t j = bc * bk; j < je; ++j) any |= nz<T>(p[j]);
+  }
+  flags[b] = any ? 1 : 0;
+}
+
+// 16x16 bf16/f32 fast path: one warp per block row-stripe element group.
+template <typename T>
+__global__ void block_copy_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
+                                  int64_t bm, int64_t bk, int group_dim, const int32_t* AM,
+                                  const int32_t* AK, const uint8_t* mask, int64_t slots, int64_t g,
+                                  T* AV) {
+  // one warp per slot; lanes stride the bm*bk elements
+  const int64_t slot = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (slot >= slots) return;
+  const int lane = lane_id();
+  T* dst = AV + slot * bm * bk;
+  const bool real = mask[slot] != 0;
+  const int64_t p = slot / g;
+  const int64_t rb = group_dim == 0 ? AM[p] : AK[slot];
+  const int64_t cb = group_dim == 0 ? AK[slot] : AM[p];
+  for (int64_t e = lane; e < bm * bk; e += 32) {
+    const int64_t i = e / bk, j = e % bk;
+    const int64_t si = rb * bm + i, sj = cb * bk + j;
+    T v = T(0);
+    if (real && si < rows && sj < cols) v = dense[si * cols + sj];
+    dst[e] = v;
+  }
+}
+
+}  // namespace
+}  // namespace ixb
+
+// =========================================================== the plan object
+struct ixb_pack {
+  int type = 0;  // 1 dense-row grouping, 2 dense_to_coo, 3 sorted-run grouping, 4 blocks, 5 kmap
+  cudaStream_t s = nullptr;
+  int64_t nnz = 0, G = 0, g = 1, R = 0;
+  int group_dim = 0, rank = 2, dtype = IXB_F32;
+  // dense sources
+  const void* dense = nullptr;
+  int64_t rows = 0, cols = 0;
+  ixb::Scratch<int32_t> occ, offs;  // per row: occupancy, group/row offsets
+  // sorted-run engine
+  std::vector<const int32_t*> coords;  // rank source coordinate arrays
+  ixb::Scratch<int32_t> perm, run_incl, start, len, gofs;
+  // blocks
+  int64_t bm = 1, bk = 1, gr = 0, gcn = 0, nblocks = 0;
+  ixb::Scratch<uint8_t> flags;
+  std::unique_ptr<ixb_pack> inner;
+  ixb::Scratch<int32_t> coo_r, coo_c;  // block COO when grouping by columns
+  // kernel map
+  ixb::Scratch<int32_t> kmap_out, kmap_in, kmap_off;
+};
+
+namespace ixb {
+namespace {
+
+template <typename T>
+void launch_row_count(const T* d, int64_t rows, int64_t cols, int32_t* occ, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t grid = ceil_div(rows * 32, kTB);
+  if (rows == 0) return;
+  if (cols % V == 0 && reinterpret_cast<uintptr_t>(d) % 16 == 0) {
+    row_count_kernel<T, V><<<grid, kTB, 0, s>>>(d, rows, cols, occ);
+  } else {
+    row_count_kernel<T, 1><<<grid, kTB, 0, s>>>(d, rows, cols, occ);
+  }
+  IXB_LAUNCH_CHECK("row_count_kernel");
+}
+
+template <typename T>
+void launch_row_pack(const T* d, int64_t rows, int64_t cols, const int32_t* occ,
+                     const int32_t* offs, int64_t g, int mode, int32_t* AM, int32_t* AK, T* AV,
+                     uint8_t* mask, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t grid = ceil_div(rows * 32, kTB);
+  if (rows == 0) return;
+  if (cols % V == 0 && reinterpret_cast<uintptr_t>(d) % 16 == 0) {
+    row_pack_kernel<T, V><<<grid, kTB, 0, s>>>(d, rows, cols, occ, offs, g, mode, AM, AK, AV, mask);
+  } else {
+    row_pack_kernel<T, 1><<<grid, kTB, 0, s>>>(d, rows, cols, occ, offs, g, mode, AM, AK, AV, mask);
+  }
+  IXB_LAUNCH_CHECK("row_pack_kernel");
+}
+
+// Exclusive scan of n int32 into out[0..n] (out[n] = total); returns total (sync).
+int64_t exclusive_scan_total(const int32_t* in, int64_t n, int32_t* out, cudaStream_t s) {
+  if (n == 0) return 0;
+  size_t tb = 0;
+  IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int>(n), s));
+  Scratch<char> tmp(tb, s);
+  IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, static_cast<int>(n), s));
+  note_launch();
+  int32_t last_in = 0, last_out = 0;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&last_out, out + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  const int64_t total = static_cast<int64_t>(last_in) + last_out;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(out + n, &total, 4, cudaMemcpyHostToDevice, s));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (total > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 entries");
+  return total;
+}
+
+void count_rows(ixb_pack* P) {
+  P->occ = Scratch<int32_t>(P->rows + 1, P->s);
+  if (P->dtype == IXB_F32) {
+    launch_row_count(static_cast<const float*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
+  } else if (P->dtype == IXB_BF16) {
+    launch_row_count(static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
+  } else {
+    launch_row_count(static_cast<const uint8_t*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
+  }
+}
+
+// Dense-row grouping plan (group_dim 0): occ -> tuner -> groups per row -> gofs.
+void plan_dense_rows(ixb_pack* P, int64_t g_req, int64_t* g_out) {
+  count_rows(P);
+  Scratch<int32_t> tmp(P->rows + 1, P->s);
+  P->nnz = exclusive_scan_total(P->occ.p, P->rows, tmp.p, P->s);
+  int64_t g = g_req;
+  if (g == 0) g = tune_from_occ(P->occ.p, P->rows, P->rows, 0, P->s, nullptr);
+  P->g = g;
+  if (g_out) *g_out = g;
+  Scratch<int32_t> ng(P->rows + 1, P->s);
+  if (P->rows) {
+    groups_per_run_kernel<<<ceil_div(P->rows, kTB), kTB, 0, P->s>>>(P->occ.p, P->rows, g, ng.p);
+    IXB_LAUNCH_CHECK("groups_per_run_kernel");
+  }
+  P->offs = Scratch<int32_t>(P->rows + 1, P->s);
+  P->G = exclusive_scan_total(ng.p, P->rows, P->offs.p, P->s);
+}
+
+template <typename T>
+void pack_dense_rows_t(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask) {
+  launch_row_pack(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p, P->g, 0,
+                  AM, AK, static_cast<T*>(AV), mask, P->s);
+}
+
+void pack_dense_rows(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask) {
+  if (P->dtype == IXB_F32) pack_dense_rows_t<float>(P, AM, AK, AV, mask);
+  else if (P->dtype == IXB_BF16) pack_dense_rows_t<__nv_bfloat16>(P, AM, AK, AV, mask);
+  else pack_dense_rows_t<uint8_t>(P, AM, AK, AV, mask);
+}
+
+// Sorted-run plan over rank coordinate arrays; key order: group_dim, then
+// the other dims ascending (formats.cpp:124-129, 423-434).
+void plan_sorted_runs(ixb_pack* P, bool identity_order, int64_t g_req, int64_t extent,
+                      int count_empty_rows, int64_t* g_out) {
+  const int64_t n = P->nnz;
+  cudaStream_t s = P->s;
+  if (n > INT32_MAX) fail(IXB_SHAPE, "more than 2^31 nonzeros");
+  if (!identity_order && n > 0) {
+    P->perm = Scratch<int32_t>(n, s);
+    iota32<<<ceil_div(n, kTB), kTB, 0, s>>>(P->perm.p, n);
+    IXB_LAUNCH_CHECK("iota32");
+    std::vector<int> order;  // most significant first
+    order.push_back(P->group_dim);
+    for (int d = 0; d < P->rank; ++d) {
+      if (d != P->group_dim) order.push_back(d);
+    }
+    Scratch<int32_t> key(n, s), key_out(n, s), perm_out(n, s);
+    size_t tb = 0;
+    IXB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_out.p, P->perm.p,
+                                                   perm_out.p, static_cast<int>(n), 0, 32, s));
+    Scratch<char> tmp(tb, s);
+    for (int i = static_cast<int>(order.size()) - 1; i >= 0; --i) {  // LSD over keys
+      gather_key<<<ceil_div(n, kTB), kTB, 0, s>>>(P->coords[order[i]], P->perm.p, n, key.p);
+      IXB_LAUNCH_CHECK("gather_key");
+      IXB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_out.p, P->perm.p,
+                                                     perm_out.p, static_cast<int>(n), 0, 32, s));
+      note_launch(4);
+      std::swap(P->perm.p, perm_out.p);
+    }
+  }
+  const int32_t* gcoord = P->coords[P->group_dim];
+  Scratch<int32_t> flag(n + 1, s);
+  P->run_incl = Scratch<int32_t>(n + 1, s);
+  if (n > 0) {
+    head_flags<<<ceil_div(n, kTB), kTB, 0, s>>>(gcoord, P->perm.p, n, flag.p);
+    IXB_LAUNCH_CHECK("head_flags");
+    size_t tb = 0;
+    IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.p, P->run_incl.p,
+                                                 static_cast<int>(n), s));
+    Scratch<char> tmp(tb, s);
+    IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.p, tb, flag.p, P->run_incl.p,
+                                                 static_cast<int>(n), s));
+    note_launch();
+    int32_t R = 0;
+    IXB_CUDA_CHECK(cudaMemcpyAsync(&R, P->run_incl.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    P->R = R;
+  }
+  const int64_t R = P->R;
+  P->start = Scratch<int32_t>(R + 1, s);
+  P->len = Scratch<int32_t>(R + 1, s);
+  if (n > 0) {
+    run_starts<<<ceil_div(n, kTB), kTB, 0, s>>>(flag.p, P->run_incl.p, n, P->start.p);
+    IXB_LAUNCH_CHECK("run_starts");
+    run_lengths<<<ceil_div(R, kTB), kTB, 0, s>>>(P->start.p, R, n, P->len.p);
+    IXB_LAUNCH_CHECK("run_lengths");
+  }
+  int64_t g = g_req;
+  if (g == 0) g = tune_from_occ(P->len.p, R, extent, count_empty_rows, s, nullptr);
+  P->g = g;
+  if (g_out) *g_out = g;
+  Scratch<int32_t> ng(R + 1, s);
+  if (R) {
+    groups_per_run_kernel<<<ceil_div(R, kTB), kTB, 0, s>>>(P->len.p, R, g, ng.p);
+    IXB_LAUNCH_CHECK("groups_per_run_kernel");
+  }
+  P->gofs = Scratch<int32_t>(R + 1, s);
+  P->G = exclusive_scan_total(ng.p, R, P->gofs.p, s);
+}
+
+void pack_sorted_runs(ixb_pack* P, const void* vals, int dtype, int32_t* gout,
+                      int32_t* const* mout, void* vout, uint8_t* mask) {
+  RunPackArgs a{};
+  a.perm = P->perm.p;
+  a.run_incl = P->run_incl.p;
+  a.start = P->start.p;
+  a.len = P->len.p;
+  a.gofs = P->gofs.p;
+  a.gcoord = P->coords[P->group_dim];
+  int m = 0;
+  for (int d = 0; d < P->rank; ++d) {
+    if (d == P->group_dim) continue;
+    a.mcoord[m] = P->coords[d];
+    a.mout[m] = mout[m];
+    ++m;
+  }
+  a.nm = m;
+  a.n = P->nnz;
+  a.R = P->R;
+  a.g = P->g;
+  a.vals = vals;
+  a.vout = vout;
+  a.vbytes = (vals && vout) ? (dtype == IXB_BF16 ? 2 : 4) : 0;
+  a.mask = mask;
+  a.gout = gout;
+  if (a.n > 0) {
+    run_pack_elems<<<ceil_div(a.n, kTB), kTB, 0, P->s>>>(a);
+    IXB_LAUNCH_CHECK("run_pack_elems");
+    run_pack_runs<<<ceil_div(a.R, kTB), kTB, 0, P->s>>>(a);
+    IXB_LAUNCH_CHECK("run_pack_runs");
+  }
+}
+
+void check_dtype(int dtype) {
+  if (dtype != IXB_F32 && dtype != IXB_BF16) fail(IXB_FAILURE, "unsupported dtype");
+}
+
+}  // namespace
+}  // namespace ixb
+
+using namespace ixb;
+
+extern "C" {
+
+void ixb_pack_free(ixb_pack* plan) { delete plan; }
+
+int ixb_dense_to_coo_plan(const void* dense, int dtype, int64_t rows, int64_t cols,
+                          ixb_stream stream, ixb_pack** plan, int64_t* nnz) {
+  return ixb_guard([&] {
+    check_dtype(dtype);
+    if (rows < 0 || cols < 0) fail(IXB_SHAPE, "dense_to_coo expects a rank-2 tensor");
+    auto P = std::make_unique<ixb_pack>();
+    P->type = 2;
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    P->dense = dense;
+    P->dtype = dtype;
+    P->rows = rows;
+    P->cols = cols;
+    count_rows(P.get());
+    P->offs = Scratch<int32_t>(rows + 1, P->s);
+    P->nnz = exclusive_scan_total(P->occ.p, rows, P->offs.p, P->s);
+    *nnz = P->nnz;
+    *plan = P.release();
+  });
+}
+
+int ixb_dense_to_coo_pack(ixb_pack* P, int32_t* row_coord, int32_t* col_coord, void* values,
+                          ixb_stream stream) {
+  return ixb_guard([&] {
+    if (!P || P->type != 2) fail(IXB_FAILURE, "not a dense_to_coo plan");
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    if (P->dtype == IXB_F32) {
+      launch_row_pack(static_cast<const float*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p, 1,
+                      1, row_coord, col_coord, static_cast<float*>(values), nullptr, P->s);
+    } else {
+      launch_row_pack(static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->occ.p,
+                      P->offs.p, 1, 1, row_coord, col_coord, static_cast<__nv_bfloat16*>(values),
+                      nullptr, P->s);
+    }
+  });
+}
+
+int ixb_groupcoo_plan(const int32_t* row_coord, const int32_t* col_coord, int64_t nnz,
+                      int64_t rows, int64_t cols, int canonical, int group_dim, int64_t g,
+                      ixb_stream stream, ixb_pack** plan, int64_t* num_groups, int64_t* g_out) {
+  return ixb_guard([&] {
+    if (g < 0) fail(IXB_SHAPE, "group size must be >= 1, got " + std::to_string(g));
+    if (group_dim != 0 && group_dim != 1) fail(IXB_SHAPE, "group_dim must be 0 or 1");
+    auto P = std::make_unique<ixb_pack>();
+    P->type = 3;
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    P->nnz = nnz;
+    P->rank = 2;
+    P->group_dim = group_dim;
+    P->coords = {row_coord, col_coord};
+    plan_sorted_runs(P.get(), canonical && group_dim == 0, g, group_dim == 0 ? rows : cols, 0,
+                     g_out);
+    *num_groups = P->G;
+    *plan = P.release();
+  });
+}
+
+int ixb_groupcoo_pack(ixb_pack* P, const void* values, int dtype, int32_t* AM, int32_t* AK,
+                      void* AV, uint8_t* mask, ixb_stream stream) {
+  return ixb_guard([&] {
+    if (!P || P->type != 3 || P->rank != 2) fail(IXB_FAILURE, "not a groupcoo plan");
+    if (values) check_dtype(dtype);
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    int32_t* mo[1] = {AK};
+    pack_sorted_runs(P, values, dtype, AM, mo, AV, mask);
+  });
+}
+
+int ixb_dense_groupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t cols,
+                            int group_dim, int64_t g, ixb_stream stream, ixb_pack** plan,
+                            int64_t* num_groups, int64_t* g_out, int64_t* nnz) {
+  return ixb_guard([&] {
+    check_dtype(dtype);
+    if (g < 0) fail(IXB_SHAPE, "group size must be >= 1, got " + std::to_string(g));
+    if (group_dim != 0 && group_dim != 1) fail(IXB_SHAPE, "group_dim must be 0 or 1");
+    auto P = std::make_unique<ixb_pack>();
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    P->dense = dense;
+    P->dtype = dtype;
+    P->rows = rows;
+    P->cols = cols;
+    P->group_dim = group_dim;
+    if (group_dim == 0) {
+      P->type = 1;
+      plan_dense_rows(P.get(), g, g_out);
+    } else {
+      // columns: dense_to_coo, then the sorted-run engine keyed (col, row)
+      count_rows(P.get());
+      P->offs = Scratch<int32_t>(rows + 1, P->s);
+      P->nnz = exclusive_scan_total(P->occ.p, rows, P->offs.p, P->s);
+      P->coo_r = Scratch<int32_t>(P->nnz, P->s);
+      P->coo_c = Scratch<int32_t>(P->nnz, P->s);
+      if (dtype == IXB_F32) {
+        launch_row_pack(static_cast<const float*>(dense), rows, cols, P->occ.p, P->offs.p, 1, 1,
+                        P->coo_r.p, P->coo_c.p, static_cast<float*>(nullptr), nullptr, P->s);
+      } else {
+        launch_row_pack(static_cast<const __nv_bfloat16*>(dense), rows, cols, P->occ.p, P->offs.p,
+                        1, 1, P->coo_r.p, P->coo_c.p, static_cast<__nv_bfloat16*>(nullptr),
+                        nullptr, P->s);
+      }
+      P->type = 3;
+      P->rank = 2;
+      P->coords = {P->coo_r.p, P->coo_c.p};
+      plan_sorted_runs(P.get(), false, g, cols, 0, g_out);
+    }
+    *num_groups = P->G;
+    if (nnz) *nnz = P->nnz;
+    *plan = P.release();
+  });
+}
+
+int ixb_dense_groupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask,
+                            ixb_stream stream) {
+  return ixb_guard([&] {
+    if (!P || (P->type != 1 && P->type != 3) || !P->dense) fail(IXB_FAILURE, "not a dense groupcoo plan");
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    if (P->type == 1) {
+      pack_dense_rows(P, AM, AK, AV, mask);
+    } else {
+      // values in dense_to_coo order = row-major positions; gather by (r, c)
+      Scratch<char> vals(P->nnz * (P->dtype == IXB_BF16 ? 2 : 4), P->s);
+      if (P->dtype == IXB_F32) {
+        launch_row_pack(static_cast<const float*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p,
+                        1, 1, P->coo_r.p, P->coo_c.p, reinterpret_cast<float*>(vals.p), nullptr,
+                        P->s);
+      } else {
+        launch_row_pack(static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->occ.p,
+                        P->offs.p, 1, 1, P->coo_r.p, P->coo_c.p,
+                        reinterpret_cast<__nv_bfloat16*>(vals.p), nullptr, P->s);
+      }
+      int32_t* mo[1] = {AK};
+      pack_sorted_runs(P, vals.p, P->dtype, AM, mo, AV, mask);
+    }
+  });
+}
+
+int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t cols, int64_t bm,
+                           int64_t bk, int64_t g, int group_dim, ixb_stream stream,
+                           ixb_pack** plan, int64_t* num_groups, int64_t* g_out,
+                           int64_t* num_blocks) {
+  return ixb_guard([&] {
+    check_dtype(dtype);
+    if (bm < 1 || bk < 1) fail(IXB_SHAPE, "block dims must be >= 1");
+    if (g < 0) fail(IXB_SHAPE, "group size must be >= 1");
+    if (group_dim != 0 && group_dim != 1) fail(IXB_SHAPE, "group_dim must be 0 or 1");
+    auto P = std::make_unique<ixb_pack>();
+    P->type = 4;
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    P->dense = dense;
+    P->dtype = dtype;
+    P->rows = rows;
+    P->cols = cols;
+    P->bm = bm;
+    P->bk = bk;
+    P->group_dim = group_dim;
+    P->gr = ceil_div(rows, bm);
+    P->gcn = ceil_div(cols, bk);
+    const int64_t nb = P->gr * P->gcn;
+    P->flags = Scratch<uint8_t>(nb + 16, P->s);
+    if (nb) {
+      if (dtype == IXB_F32) {
+        block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
+            static_cast<const float*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
+      } else {
+        block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
+            static_cast<const __nv_bfloat16*>(dense), rows, cols, bm, bk, P->gr, P->gcn,
+            P->flags.p);
+      }
+      IXB_LAUNCH_CHECK("block_flags_kernel");
+    }
+    // group the block-level COO like coo_to_groupcoo (formats.cpp:265)
+    auto I = std::make_unique<ixb_pack>();
+    I->s = P->s;
+    I->dense = P->flags.p;
+    I->dtype = 2;  // u8 flags
+    I->rows = P->gr;
+    I->cols = P->gcn;
+    I->group_dim = group_dim;
+    if (group_dim == 0) {
+      I->type = 1;
+      plan_dense_rows(I.get(), g, g_out);
+    } else {
+      count_rows(I.get());
+      I->offs = Scratch<int32_t>(I->rows + 1, I->s);
+      I->nnz = exclusive_scan_total(I->occ.p, I->rows, I->offs.p, I->s);
+      I->coo_r = Scratch<int32_t>(I->nnz, I->s);
+      I->coo_c = Scratch<int32_t>(I->nnz, I->s);
+      launch_row_pack(static_cast<const uint8_t*>(I->dense), I->rows, I->cols, I->occ.p,
+                      I->offs.p, 1, 1, I->coo_r.p, I->coo_c.p, static_cast<uint8_t*>(nullptr),
+                      nullptr, I->s);
+      I->type = 3;
+      I->rank = 2;
+      I->coords = {I->coo_r.p, I->coo_c.p};
+      plan_sorted_runs(I.get(), false, g, I->cols, 0, g_out);
+    }
+    P->G = I->G;
+    P->g = I->g;
+    P->nblocks = I->nnz;
+    *num_groups = P->G;
+    if (num_blocks) *num_blocks = P->nblocks;
+    P->inner = std::move(I);
+    *plan = P.release();
+  });
+}
+
+int ixb_blockgroupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask,
+                           ixb_stream stream) {
+  return ixb_guard([&] {
+    if (!P || P->type != 4) fail(IXB_FAILURE, "not a blockgroupcoo plan");
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    ixb_pack* I = P->inner.get();
+    I->s = P->s;
+    const int64_t slots = P->G * P->g;
+    Scratch<uint8_t> own_mask;
+    uint8_t* m = mask;
+    if (!m) {
+      own_mask = Scratch<uint8_t>(slots + 16, P->s);
+      m = own_mask.p;
+    }
+    if (I->type == 1) {
+      pack_dense_rows(I, AM, AK, nullptr, m);
+    } else {
+      int32_t* mo[1] = {AK};
+      pack_sorted_runs(I, nullptr, IXB_F32, AM, mo, nullptr, m);
+    }
+    if (AV && slots) {
+      const int64_t grid = ceil_div(slots * 32, kTB);
+      if (P->dtype == IXB_F32) {
+        block_copy_kernel<<<grid, kTB, 0, P->s>>>(static_cast<const float*>(P->dense), P->rows,
+                                                 P->cols, P->bm, P->bk, P->group_dim, AM, AK, m,
+                                                 slots, P->g, static_cast<float*>(AV));
+      } else {
+        block_copy_kernel<<<grid, kTB, 0, P->s>>>(
+            static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->bm, P->bk,
+            P->group_dim, AM, AK, m, slots, P->g, static_cast<__nv_bfloat16*>(AV));
+      }
+      IXB_LAUNCH_CHECK("block_copy_kernel");
+    }
+  });
+}
+
+int ixb_group_coo_tensor_plan(int rank, const int64_t* shape, const int32_t* const* coords,
+                              int64_t nnz, int group_dim, int64_t g, ixb_stream stream,
+                              ixb_pack** plan, int64_t* num_groups) {
+  return ixb_guard([&] {
+    if (g < 1) fail(IXB_SHAPE, "group size must be >= 1");
+    if (group_dim < 0 || group_dim >= rank) fail(IXB_SHAPE, "group_dim out of range");
+    if (rank > 9) fail(IXB_SHAPE, "rank > 9 not supported");
+    auto P = std::make_unique<ixb_pack>();
+    P->type = 3;
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    P->nnz = nnz;
+    P->rank = rank;
+    P->group_dim = group_dim;
+    P->coords.assign(coords, coords + rank);
+    plan_sorted_runs(P.get(), false, g, shape ? shape[group_dim] : 0, 0, nullptr);
+    *num_groups = P->G;
+    *plan = P.release();
+  });
+}
+
+int ixb_group_coo_tensor_pack(ixb_pack* P, const void* values, int dtype, int32_t* group_coord,
+                              int32_t* const* member_coords, void* out_values, uint8_t* mask,
+                              ixb_stream stream) {
+  return ixb_guard([&] {
+    if (!P || P->type != 3) fail(IXB_FAILURE, "not a group_coo_tensor plan");
+    if (values) check_dtype(dtype);
+    P->s = reinterpret_cast<cudaStream_t>(stream);
+    pack_sorted_runs(P, values, dtype, group_coord, member_coords, out_values, mask);
+  });
+}
+
+int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
+                        ixb_stream stream, int64_t* g_out, double* gstar_out) {
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    // occupancy histogram (occupancy(), formats.cpp:96-103): integer atomics
+    Scratch<int32_t> occ(extent + 1, s);
+    IXB_CUDA_CHECK(cudaMemsetAsync(occ.p, 0, (extent + 1) * 4, s));
+    if (nnz) {
+      occupancy_kernel<<<ceil_div(nnz, kTB), kTB, 0, s>>>(coord, nnz, extent, occ.p);
+      IXB_LAUNCH_CHECK("occupancy_kernel");
+    }
+    *g_out = tune_from_occ(occ.p, extent, extent, count_empty_rows, s, gstar_out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+// Host runtime of the C-ABI: error state, per-device error records, scratch
+// pool, launch accounting and the multi-GPU shard planner.
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ixb_internal.h"
+
+namespace {
+
+thread_local std::string t_msg;
+thread_local int t_idx_operand = -1;
+thread_local int64_t t_idx_pos = 0, t_idx_value = 0, t_idx_extent = 0;
+std::atomic<int64_t> g_launches{0};
+
+struct DeviceCtx {
+  ixb::ErrorRecord* rec = nullptr;
+  int sms = 0;
+};
+std::mutex g_mu;
+std::vector<DeviceCtx> g_dev;
+
+DeviceCtx& ctx() {
+  int d = 0;
+  ixb::cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (static_cast<int>(g_dev.size()) <= d) g_dev.resize(static_cast<size_t>(d) + 1);
+  DeviceCtx& c = g_dev[static_cast<size_t>(d)];
+  if (!c.rec) {
+    ixb::cuda_check(cudaMalloc(&c.rec, sizeof(ixb::ErrorRecord)), "cudaMalloc(error record)");
+    ixb::cuda_check(cudaMemset(c.rec, 0xff, sizeof(ixb::ErrorRecord)), "cudaMemset");
+    ixb::cuda_check(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, d),
+                    "cudaDeviceGetAttribute");
+  }
+  return c;
+}
+
+}  // namespace
+
+namespace ixb {
+
+void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(IXB_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void note_launch(int n) { g_launches += n; }
+
+int sm_count() { return ctx().sms; }
+
+ErrorRecord* device_error_record() { return ctx().rec; }
+
+void reset_error_record(cudaStream_t stream) {
+  IXB_CUDA_CHECK(cudaMemsetAsync(&ctx().rec->key, 0xff, sizeof(unsigned long long), stream));
+}
+
+void check_error_record(cudaStream_t stream, const OperandInfo* ops, int nops) {
+  unsigned long long key = kNoError;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&key, &ctx().rec->key, sizeof key, cudaMemcpyDeviceToHost,
+                                 stream));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(stream));
+  if (key == kNoError) return;
+  int op = static_cast<int>(key >> 56);
+  int64_t pos = static_cast<int64_t>(key & ((1ull << 56) - 1));
+  reset_error_record(stream);
+  if (op >= nops || !ops) fail(IXB_INDEX_RANGE, "index out of range");
+  const OperandInfo& o = ops[op];
+  int32_t v = 0;
+  if (o.device_array && pos < o.numel) {
+    IXB_CUDA_CHECK(cudaMemcpy(&v, o.device_array + pos, sizeof v, cudaMemcpyDeviceToHost));
+  }
+  t_idx_operand = op;
+  t_idx_pos = pos;
+  t_idx_value = v;
+  t_idx_extent = o.extent;
+  // Message content of checked_index (plan.cpp:253-256).
+  fail(IXB_INDEX_RANGE, "index tensor " + std::string(o.index_name) + " value " +
+                            std::to_string(v) + " at position [" + std::to_string(pos) +
+                            "] out of range for dim " + std::to_string(o.target_dim) + " of " +
+                            o.target_name + " (extent " + std::to_string(o.extent) + ")");
+}
+
+void* scratch_alloc(size_t bytes, cudaStream_t stream) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  IXB_CUDA_CHECK(cudaMallocAsync(&p, bytes, stream));
+  return p;
+}
+
+void scratch_free(void* p, cudaStream_t stream) {
+  if (p) cudaFreeAsync(p, stream);
+}
+
+}  // namespace ixb
+
+int ixb_guard_set(int code, const char* msg) {
+  if (code != IXB_OK) {
+    t_msg = msg;
+  }
+  return code;
+}
+
+extern "C" {
+
+const char* ixb_last_error(void) { return t_msg.c_str(); }
+
+int ixb_version(void) { return 1; }
+
+int ixb_last_index_error(int* operand, int64_t* position, int64_t* value, int64_t* extent) {
+  if (operand) *operand = t_idx_operand;
+  if (position) *position = t_idx_pos;
+  if (value) *value = t_idx_value;
+  if (extent) *extent = t_idx_extent;
+  return t_idx_operand >= 0 ? IXB_INDEX_RANGE : IXB_OK;
+}
+
+int ixb_check_errors(ixb_stream stream) {
+  return ixb_guard([&] { ixb::check_error_record(stream, nullptr, 0); });
+}
+
+int ixb_sm_count(void) {
+  int n = 0;
+  ixb_guard([&] { n = ixb::sm_count(); });
+  return n;
+}
+
+int64_t ixb_launch_count(void) { return g_launches.load(); }
+
+// Shard planner: contiguous group ranges with ~equal slots,
+// cut only at group-coordinate changes so no output row spans two ranks.
+int ixb_shard_groups(const int32_t* gc, int64_t G, int parts, int64_t* bounds) {
+  return ixb_guard([&] {
+    if (parts < 1) ixb::fail(IXB_FAILURE, "ixb_shard_groups: parts must be >= 1");
+    bounds[0] = 0;
+    for (int r = 1; r < parts; ++r) {
+      int64_t target = (G * r) / parts;
+      int64_t cut = target;
+      if (cut < bounds[r - 1]) cut = bounds[r - 1];
+      // advance to the next row boundary (never split a row's groups)
+      while (cut > 0 && cut < G && gc[cut] == gc[cut - 1]) ++cut;
+      bounds[r] = cut;
+    }
+    bounds[parts] = G;
+  });
+}
+
+}  // extern "C"

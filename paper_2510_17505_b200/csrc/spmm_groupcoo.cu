@@ -1,0 +1,343 @@
+// K3 — GroupCOO SpMM on sm_100a:  C[AM[p],n] += AV[p,q] * B[AK[p,q],n]
+// (corpus/unstructured_spmm.json:2; reference evaluators plan.cpp:383-534,
+// oracle plan.cpp:579-594, fused kernel kernel.cpp:461-473).
+//
+// HBM/L2-gather bound. Design:
+//  * Row-segment ownership instead of atomics: groups are sorted by AM (the
+//    builders guarantee it), so the groups of one output row are contiguous.
+//    Each warp scans a chunk of CH group positions for segment starts
+//    (AM[p] != AM[p-1]) and owns every segment that starts there, summing
+//    its groups in group order and writing the C row once. The result is
+//    run-to-run deterministic and independent of CH / grid / sharding.
+//  * The dense operand row B[k, :] is gathered with 128-bit
+//    ld.global.nc.L1::no_allocate loads under an L2 evict_last policy (B is
+//    re-read by every group that names k), the format (AK/AV) is streamed
+//    under evict_first. Group metadata is loaded coalesced (one slot per
+//    lane) and broadcast by shuffles; the q loop is unrolled by 8 so every
+//    lane keeps 8×T independent 16-byte gathers in flight.
+//  * `=` writes every row of C exactly once: the owner of a segment also
+//    zero-fills the empty rows between the previous segment's row and its
+//    own (and the tail after the last segment), so no memset pass is needed.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace ixb {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+  using T = float4;
+};
+template <>
+struct VecT<1> {
+  using T = float;
+};
+
+__device__ __forceinline__ void vzero(float4& a) { a = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void vzero(float& a) { a = 0.f; }
+__device__ __forceinline__ void vfma(float4& a, float s, const float4& b) {
+  a.x = fmaf(s, b.x, a.x);
+  a.y = fmaf(s, b.y, a.y);
+  a.z = fmaf(s, b.z, a.z);
+  a.w = fmaf(s, b.w, a.w);
+}
+__device__ __forceinline__ void vfma(float& a, float s, const float& b) { a = fmaf(s, b, a); }
+__device__ __forceinline__ void vadd(float4& a, const float4& b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+__device__ __forceinline__ void vadd(float& a, const float& b) { a += b; }
+
+template <int VEC>
+__device__ __forceinline__ typename VecT<VEC>::T ld_b(const float* p, uint64_t pol);
+template <>
+__device__ __forceinline__ float4 ld_b<4>(const float* p, uint64_t pol) {
+  return ldg_f4_keep(p, pol);
+}
+template <>
+__device__ __forceinline__ float ld_b<1>(const float* p, uint64_t pol) {
+  return ldg_f_keep(p, pol);
+}
+
+struct SpmmArgs {
+  const int32_t* AM;    // [G] (sorted copy when perm != null)
+  const int32_t* perm;  // [G] original group index per sorted position, or null
+  const int32_t* AK;    // [G, g]
+  const float* AV;      // [G, g]
+  const float* B;       // [K, N]
+  float* C;             // [M, N]
+  int64_t G, g, K, N, M;
+  int chunk;            // CH: group positions scanned per warp (<= 32)
+  int accumulate;
+  int check;
+  ErrorRecord* err;
+};
+
+// Zero rows [r0, r1) of C, cooperatively by one warp.
+__device__ __forceinline__ void zero_rows(float* C, int64_t N, int64_t r0, int64_t r1) {
+  if (r1 <= r0) return;
+  int64_t total = (r1 - r0) * N;
+  float* base = C + r0 * N;
+  if ((N & 3) == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = lane_id(); i < total / 4; i += 32) reinterpret_cast<float4*>(base)[i] = z;
+  } else {
+    for (int64_t i = lane_id(); i < total; i += 32) base[i] = 0.f;
+  }
+}
+
+template <int VEC, int T, bool PERM>
+__global__ void __launch_bounds__(kThreads, 2) spmm_groupcoo_kernel(SpmmArgs a) {
+  using V = typename VecT<VEC>::T;
+  constexpr int kColsPerPass = 32 * VEC * T;
+  constexpr int kUnroll = T >= 4 ? 4 : 8;  // 8-16 independent gathers in flight per lane
+  const int lane = lane_id();
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t base = warp * a.chunk;
+  if (base >= a.G) return;
+  const uint64_t keep = policy_evict_last();
+  const uint64_t stream = policy_evict_first();
+
+  // Segment starts inside this warp's chunk.
+  const int64_t p_lane = base + lane;
+  const bool in_chunk = lane < a.chunk && p_lane < a.G;
+  int am_here = in_chunk ? __ldg(a.AM + p_lane) : 0;
+  int am_prev = (in_chunk && p_lane > 0) ? __ldg(a.AM + p_lane - 1) : -1;
+  unsigned starts = __ballot_sync(0xffffffffu, in_chunk && (p_lane == 0 || am_here != am_prev));
+
+  while (starts) {
+    const int sl = __ffs(starts) - 1;
+    starts &= starts - 1;
+    const int64_t s = base + sl;
+    const int row = __shfl_sync(0xffffffffu, am_here, sl);
+    const int prev_row = __shfl_sync(0xffffffffu, am_prev, sl);
+    // Segment end: first p > s with AM[p] != row (windows of 32, coalesced).
+    int64_t e = s + 1;
+    for (;;) {
+      const int64_t pp = e + lane;
+      const bool diff = pp >= a.G || __ldg(a.AM + pp) != row;
+      const unsigned m = __ballot_sync(0xffffffffu, diff);
+      if (m) {
+        e += __ffs(m) - 1;
+        break;
+      }
+      e += 32;
+    }
+    const bool row_ok = row >= 0 && static_cast<int64_t>(row) < a.M;
+    if (!a.accumulate) {
+      // Empty rows between the previous segment and this one; the tail.
+      int64_t z0 = prev_row + 1 < 0 ? 0 : prev_row + 1;
+      int64_t z1 = row < 0 ? 0 : (row > a.M ? a.M : row);
+      zero_rows(a.C, a.N, z0, z1);
+      if (e == a.G) zero_rows(a.C, a.N, row + 1 < 0 ? 0 : row + 1, a.M);
+    }
+    if (!row_ok) {
+      if (a.check) {
+        // First offending AM position of this value is the segment start.
+        if (lane == 0) report_index_error(a.err, 1, PERM ? __ldg(a.perm + s) : s, row);
+        // Gathers are checked before scatters (plan.cpp:544-561): still
+        // validate this segment's AK so a gather error keeps priority.
+        for (int64_t p = s; p < e; ++p) {
+          const int64_t gp = PERM ? __ldg(a.perm + p) : p;
+          for (int64_t q = lane; q < a.g; q += 32) {
+            const int k = __ldg(a.AK + gp * a.g + q);
+            if (k < 0 || static_cast<int64_t>(k) >= a.K) report_index_error(a.err, 0, gp * a.g + q, k);
+          }
+        }
+      }
+      continue;
+    }
+    float* crow = a.C + static_cast<int64_t>(row) * a.N;
+    for (int64_t c0 = 0; c0 < a.N; c0 += kColsPerPass) {
+      V acc[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) vzero(acc[t]);
+      int64_t col[T];
+      bool col_ok[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        col[t] = c0 + (t * 32 + lane) * VEC;
+        col_ok[t] = col[t] < a.N;
+      }
+      for (int64_t p = s; p < e; ++p) {
+        const int64_t gp = PERM ? __ldg(a.perm + p) : p;
+        const int32_t* ak = a.AK + gp * a.g;
+        const float* av = a.AV + gp * a.g;
+        for (int64_t q0 = 0; q0 < a.g; q0 += 32) {
+          const int qn = static_cast<int>(a.g - q0 < 32 ? a.g - q0 : 32);
+          int my_k = 0;
+          float my_v = 0.f;
+          if (lane < qn) {
+            my_k = ldg_i_stream(ak + q0 + lane, stream);
+            my_v = ldg_f_stream(av + q0 + lane, stream);
+            if (my_k < 0 || static_cast<int64_t>(my_k) >= a.K) {
+              if (a.check) report_index_error(a.err, 0, gp * a.g + q0 + lane, my_k);
+              my_k = 0;
+              my_v = 0.f;
+            }
+          }
+          for (int q = 0; q < qn; q += kUnroll) {
+            int kk[kUnroll];
+            float vv[kUnroll];
+#pragma unroll
+            for (int j = 0; j < kUnroll; ++j) {
+              kk[j] = __shfl_sync(0xffffffffu, my_k, (q + j) & 31);
+              vv[j] = __shfl_sync(0xffffffffu, my_v, (q + j) & 31);
+            }
+            V bv[kUnroll][T];
+#pragma unroll
+            for (int j = 0; j < kUnroll; ++j) {
+              const float* brow = a.B + static_cast<int64_t>(kk[j]) * a.N;
+#pragma unroll
+              for (int t = 0; t < T; ++t) {
+                if (q + j < qn && col_ok[t]) bv[j][t] = ld_b<VEC>(brow + col[t], keep);
+                else vzero(bv[j][t]);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < kUnroll; ++j) {
+#pragma unroll
+              for (int t = 0; t < T; ++t) vfma(acc[t], vv[j], bv[j][t]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (!col_ok[t]) continue;
+        V* dst = reinterpret_cast<V*>(crow + col[t]);
+        if (a.accumulate) {
+          V old = *dst;
+          vadd(old, acc[t]);
+          *dst = old;
+        } else {
+          *dst = acc[t];
+        }
+      }
+    }
+  }
+}
+
+__global__ void not_sorted_kernel(const int32_t* AM, int64_t G, int* flag) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i > 0 && i < G && AM[i] < AM[i - 1]) *flag = 1;
+}
+
+__global__ void iota_kernel(int32_t* x, int64_t n) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = static_cast<int32_t>(i);
+}
+
+template <int VEC, bool PERM>
+void launch_vec(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
+  const int64_t passes = ceil_div(a.N, 32 * VEC);
+  if (passes >= 4) {
+    spmm_groupcoo_kernel<VEC, 4, PERM><<<grid, kThreads, 0, s>>>(a);
+  } else if (passes >= 2) {
+    spmm_groupcoo_kernel<VEC, 2, PERM><<<grid, kThreads, 0, s>>>(a);
+  } else {
+    spmm_groupcoo_kernel<VEC, 1, PERM><<<grid, kThreads, 0, s>>>(a);
+  }
+  IXB_LAUNCH_CHECK("spmm_groupcoo_kernel");
+}
+
+}  // namespace
+
+// Returns true when AM is non-decreasing (one pass + sync).
+bool groups_sorted(const int32_t* AM, int64_t G, cudaStream_t s) {
+  if (G < 2) return true;
+  Scratch<int> flag(1, s);
+  IXB_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  not_sorted_kernel<<<ceil_div(G, 256), 256, 0, s>>>(AM, G, flag.p);
+  IXB_LAUNCH_CHECK("not_sorted_kernel");
+  int h = 0;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
+// Stable permutation of groups by AM (CUB LSD radix sort is stable).
+void sort_groups(const int32_t* AM, int64_t G, cudaStream_t s, Scratch<int32_t>& am_sorted,
+                 Scratch<int32_t>& perm) {
+  Scratch<int32_t> iota(G, s);
+  am_sorted = Scratch<int32_t>(G, s);
+  perm = Scratch<int32_t>(G, s);
+  iota_kernel<<<ceil_div(G, 256), 256, 0, s>>>(iota.p, G);
+  IXB_LAUNCH_CHECK("iota_kernel");
+  size_t tmp_bytes = 0;
+  IXB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, AM, am_sorted.p, iota.p,
+                                                 perm.p, static_cast<int>(G), 0, 32, s));
+  Scratch<char> tmp(tmp_bytes, s);
+  // CUB orders signed int32 keys correctly (negative = invalid rows first).
+  IXB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, AM, am_sorted.p, iota.p,
+                                                 perm.p, static_cast<int>(G), 0, 32, s));
+  note_launch(4);
+}
+
+void spmm_groupcoo(const int32_t* AM, const int32_t* AK, const float* AV, int64_t G, int64_t g,
+                   const float* B, int64_t K, int64_t N, float* C, int64_t M, int accumulate,
+                   int flags, cudaStream_t s) {
+  if (G < 0 || g < 1 || K < 0 || N < 0 || M < 0) fail(IXB_SHAPE, "ixb_spmm_groupcoo: bad extents");
+  if (G > INT32_MAX) fail(IXB_SHAPE, "ixb_spmm_groupcoo: more than 2^31 groups");
+  const bool check = !(flags & IXB_UNCHECKED);
+  if (N == 0 || M == 0) return;
+  if (G == 0) {
+    if (!accumulate) IXB_CUDA_CHECK(cudaMemsetAsync(C, 0, M * N * sizeof(float), s));
+    return;
+  }
+  Scratch<int32_t> am_sorted, perm;
+  bool use_perm = false;
+  if (!(flags & IXB_GROUPS_SORTED) && !groups_sorted(AM, G, s)) {
+    sort_groups(AM, G, s, am_sorted, perm);
+    use_perm = true;
+  }
+  if (check) reset_error_record(s);
+  SpmmArgs a;
+  a.AM = use_perm ? am_sorted.p : AM;
+  a.perm = use_perm ? perm.p : nullptr;
+  a.AK = AK;
+  a.AV = AV;
+  a.B = B;
+  a.C = C;
+  a.G = G;
+  a.g = g;
+  a.K = K;
+  a.N = N;
+  a.M = M;
+  int64_t ch = M > 0 ? G / M : 1;
+  a.chunk = static_cast<int>(ch < 1 ? 1 : (ch > 32 ? 32 : ch));
+  a.accumulate = accumulate;
+  a.check = check;
+  a.err = device_error_record();
+  const int64_t warps = ceil_div(G, a.chunk);
+  const int64_t grid = ceil_div(warps * 32, kThreads);
+  const bool vec_ok = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+  if (vec_ok) {
+    use_perm ? launch_vec<4, true>(a, grid, s) : launch_vec<4, false>(a, grid, s);
+  } else {
+    use_perm ? launch_vec<1, true>(a, grid, s) : launch_vec<1, false>(a, grid, s);
+  }
+  if (check && !(flags & IXB_ASYNC)) {
+    OperandInfo ops[2] = {{"AK", "B", 0, K, AK, G * g}, {"AM", "C", 0, M, AM, G}};
+    check_error_record(s, ops, 2);
+  }
+}
+
+}  // namespace ixb
+
+extern "C" int ixb_spmm_groupcoo(const int32_t* AM, const int32_t* AK, const float* AV, int64_t G,
+                                 int64_t g, const float* B, int64_t K, int64_t N, float* C,
+                                 int64_t M, int accumulate, int flags, ixb_stream stream) {
+  return ixb_guard([&] {
+    ixb::spmm_groupcoo(AM, AK, AV, G, g, B, K, N, C, M, accumulate, flags,
+                       reinterpret_cast<cudaStream_t>(stream));
+  });
+}
