@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 Insum executor.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfgX] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0). A "step" is one pass of the hot path over one
+batch of synthetic input: one indirect-Einsum evaluation (the evaluator
+kernel) over operands already packed and resident in HBM. Workloads are the
+BASELINE.json configs (see WORKLOADS); the default is configs[1], the
+BlockGroupCOO SpMM on tcgen05 (falls back to configs[0] only if asked).
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by a
+barrier + cuda.synchronize on both sides; each step is bracketed by CUDA
+events on the launching stream, with an L2 flush (256 MiB memset) between
+steps outside the events; ms_per_step = mean; multi-GPU = max over ranks.
+`e2e` re-times the same step through the public API with pinned host
+buffers: H2D of the step's inputs + evaluation + D2H of the result.
+`cpu_baseline` times the reference's own CPU path (oracle/_ref, the
+unmodified reference compiled in place) on a bounded row slab of the same
+matrix on this host.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_WORKLOAD = "cfg1"
+
+
+# --------------------------------------------------------------- helpers
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu_index):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 3:
+                continue
+            try:
+                mhz, mmax, mask = float(f[0]), float(f[1]), int(f[2], 16)
+            except ValueError:
+                continue
+            mx = mmax
+            if mask & 0x1:  # idle sample: not under load
+                continue
+            sm.append(mhz)
+            for bit, name in REASONS.items():
+                if mask & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples_under_load": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------- workloads
+class GroupCooWorkload:
+    """configs[0] / configs[2]: unstructured GroupCOO SpMM, fp32 (K3)."""
+    expr = "C[AM[p],n] = AV[p,q] * B[AK[p,q],n]"
+    kernel = "spmm_groupcoo_kernel"
+
+    def __init__(self, name, M, K, density, N, seed=1):
+        self.name, self.M, self.K, self.density, self.N, self.seed = name, M, K, density, N, seed
+
+    def config(self):
+        return {"workload": self.name,
+                "desc": f"GroupCOO SpMM fp32 {self.M}x{self.K} density {self.density} x N={self.N}",
+                "expr": self.expr, "M": self.M, "K": self.K, "density": self.density,
+                "N": self.N, "seed": self.seed}
+
+    def setup(self, torch, P, S, dev, seed):
+        rng = S.Rng(seed)
+        # materialize order (driver.cpp:169-186): dense B first, then sparse A
+        B = S.synth_dense(rng, (self.K, self.N), S.REAL, torch.float32)
+        A = S.synth_sparse_matrix(rng, self.M, self.K, self.density, S.REAL, torch.float32)
+        self.B = B.to(dev)
+        fmt = P.dense_to_groupcoo(A.to(dev), g=0)  # format: auto (tuner)
+        del A
+        self.fmt = fmt
+        self.G, self.g = fmt.num_groups(), fmt.group_size
+        self.nnz = int(fmt.mask.sum().item())
+        self.rows_nz = int(torch.unique(fmt.AM).numel())
+        self.C = torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
+        self.flops = 2.0 * self.nnz * self.N
+        # gather model: B row per stored nonzero + format once + C rows once
+        self.alg_bytes = (self.nnz * self.N * 4 + self.G * self.g * (4 + 4) + self.G * 4 +
+                          self.rows_nz * self.N * 4)
+        self.info = {"nnz": self.nnz, "G": self.G, "g": self.g, "nonempty_rows": self.rows_nz}
+        # pinned host copies for e2e
+        self.h_in = [fmt.AM.cpu().pin_memory(), fmt.AK.cpu().pin_memory(),
+                     fmt.AV.cpu().pin_memory(), self.B.cpu().pin_memory()]
+        self.h_out = torch.empty_like(self.C, device="cpu").pin_memory()
+        self.d_in = [torch.empty_like(x, device=dev) for x in self.h_in]
+
+    def step(self, P, stream=None):
+        P.spmm_groupcoo(self.fmt.AM, self.fmt.AK, self.fmt.AV, self.B, self.C, accumulate=False,
+                        flags=1 | 2)
+
+    def e2e_step(self, P):
+        for d, h in zip(self.d_in, self.h_in):
+            d.copy_(h, non_blocking=True)
+        AM, AK, AV, B = self.d_in
+        P.spmm_groupcoo(AM, AK, AV, B, self.C, accumulate=False, flags=1 | 2)
+        self.h_out.copy_(self.C, non_blocking=True)
+
+    def e2e_bytes(self):
+        return sum(x.numel() * x.element_size() for x in self.h_in), \
+            self.h_out.numel() * self.h_out.element_size()
+
+    def roofline_bound(self):
+        return "hbm"
+
+    # reference CPU path on a bounded slab of the same matrix
+    def cpu_sample(self, ref, budget_rows=None):
+        # ~40M reference iteration points (G*g*N), ~1-2 s per reference run
+        rows = budget_rows or int(4.0e7 / max(self.K * self.density * self.N, 1))
+        rows = max(1, min(rows, self.M))
+        rng = ref.Rng(self.seed)
+        B = ref.synth_dense(rng, (self.K, self.N), 0)
+        A = ref.synth_sparse_matrix(rng, rows, self.K, self.density, 0)  # first `rows` rows
+        r, c, v = ref.dense_to_coo(A)
+        import numpy as np
+        g = ref.tune(np.bincount(r, minlength=rows))["chosen"]  # format: auto
+        gc = ref.coo_to_groupcoo(rows, self.K, r, c, v, 0, g)
+        t = {"AM": gc["AM"], "AK": gc["AK"], "AV": gc["AV"], "B": B}
+        import numpy as np
+        out = np.zeros((rows, self.N))
+        return t, self.expr, "C", out, 2.0 * len(r) * self.N, f"first {rows} of {self.M} rows (nnz {len(r)}), g={g}"
+
+
+class BlockGroupCooWorkload:
+    """configs[1]: structured BlockGroupCOO SpMM, bf16 in / fp32 accumulate (K4, tcgen05)."""
+    expr = "C[AM[p],bm,n] = AV[p,q,bm,bk] * B[AK[p,q],bk,n]"
+    kernel = "bgcoo_tc_kernel"
+
+    def __init__(self, name, M, K, b, bdens, N, seed=1):
+        self.name, self.M, self.K, self.b, self.bdens, self.N, self.seed = \
+            name, M, K, b, bdens, N, seed
+
+    def config(self):
+        return {"workload": self.name,
+                "desc": f"BlockGroupCOO SpMM bf16 {self.M}x{self.K}, {self.b}x{self.b} blocks, "
+                        f"{100 * (1 - self.bdens):.0f}% block sparsity x N={self.N}",
+                "expr": self.expr, "M": self.M, "K": self.K, "block": self.b,
+                "block_density": self.bdens, "N": self.N, "seed": self.seed}
+
+    def setup(self, torch, P, S, dev, seed):
+        rng = S.Rng(seed)
+        b = self.b
+        B = S.synth_dense(rng, (self.K // b, b, self.N), S.REAL, torch.bfloat16)
+        A = S.synth_block_sparse_matrix(rng, self.M, self.K, b, b, self.bdens, S.REAL,
+                                        torch.bfloat16)
+        self.B = B.to(dev)
+        fmt = P.dense_to_blockgroupcoo(A.to(dev), b, b, 0)  # g by the tuner on block occupancy
+        del A
+        self.fmt = fmt
+        self.G, self.g = fmt.num_groups(), fmt.group_size
+        self.nblk = fmt.num_blocks
+        self.rows_nz = int(torch.unique(fmt.AM).numel())
+        self.C = torch.empty((self.M // b, b, self.N), dtype=torch.float32, device=dev)
+        self.flops = 2.0 * self.nblk * b * b * self.N
+        slots = self.G * self.g
+        # compulsory bytes: format once, dense operand once, C written once
+        self.alg_bytes = (slots * b * b * 2 + slots * 4 + self.G * 4 + self.K * self.N * 2 +
+                          self.rows_nz * b * self.N * 4)
+        self.gather_bytes = slots * b * self.N * 2
+        self.info = {"blocks": self.nblk, "G": self.G, "g": self.g,
+                     "nonempty_block_rows": self.rows_nz,
+                     "gathered_B_tile_bytes": self.gather_bytes}
+        self.h_in = [fmt.AM.cpu().pin_memory(), fmt.AK.cpu().pin_memory(),
+                     fmt.AV.cpu().pin_memory(), self.B.cpu().pin_memory()]
+        self.h_out = torch.empty_like(self.C, device="cpu").pin_memory()
+        self.d_in = [torch.empty_like(x, device=dev) for x in self.h_in]
+
+    def step(self, P, stream=None):
+        P.spmm_blockgroupcoo(self.fmt.AM, self.fmt.AK, self.fmt.AV, self.B, self.C,
+                             accumulate=False, flags=1 | 2)
+
+    def e2e_step(self, P):
+        for d, h in zip(self.d_in, self.h_in):
+            d.copy_(h, non_blocking=True)
+        AM, AK, AV, B = self.d_in
+        P.spmm_blockgroupcoo(AM, AK, AV, B, self.C, accumulate=False, flags=1 | 2)
+        self.h_out.copy_(self.C, non_blocking=True)
+
+    def e2e_bytes(self):
+        return sum(x.numel() * x.element_size() for x in self.h_in), \
+            self.h_out.numel() * self.h_out.element_size()
+
+    def roofline_bound(self):
+        return "tensor"
+
+    def cpu_sample(self, ref, budget_rows=None):
+        import numpy as np
+        b = self.b
+        brows = budget_rows or 2
+        rng = ref.Rng(self.seed)
+        B = ref.synth_dense(rng, (self.K // b, b, self.N), 0)
+        A = ref.synth_block_sparse_matrix(rng, brows * b, self.K, b, b, self.bdens, 0)
+        occ = (np.abs(A).reshape(brows, b, self.K // b, b).sum(axis=(1, 3)) > 0).sum(axis=1)
+        g = ref.tune(occ)["chosen"]
+        bg = ref.dense_to_blockgroupcoo(A, b, b, g, 0)
+        nblk = int(bg["mask"].sum())
+        t = {"AM": bg["AM"], "AK": bg["AK"], "AV": bg["AV"], "B": B}
+        out = np.zeros((brows, b, self.N))
+        return t, self.expr, "C", out, 2.0 * nblk * b * b * self.N, \
+            f"first {brows} of {self.M // b} block rows ({nblk} blocks), g={g}"
+
+
+WORKLOADS = {
+    "cfg1": lambda: GroupCooWorkload("cfg1", 4096, 4096, 0.01, 128),
+    "cfg2": lambda: BlockGroupCooWorkload("cfg2", 8192, 8192, 16, 0.10, 512),
+}
+for _d in ("0.30", "0.20", "0.10", "0.05", "0.02"):
+    WORKLOADS[f"cfg3_d{_d}"] = (lambda d: lambda: GroupCooWorkload(
+        f"cfg3_d{d}", 16384, 16384, float(d), 256))(_d)
+
+METRIC = "SpMM GFLOP/s (useful nnz)"
+
+
+# ------------------------------------------------------------- arms
+def cpu_reference_time(wl, steps=1, warmup=0, budget_rows=None):
+    """Times the reference's CPU path (oracle/_ref) on a slab; returns dict."""
+    from oracle import ref
+    kind = "reference"
+    if not ref.available():
+        raise RuntimeError("oracle/_ref not built")
+    t, expr, on, out, flops, sample = wl.cpu_sample(ref, budget_rows)
+    cores = os.cpu_count() or 1
+    # choose the faster reference path on this host: plan (1 core) vs the
+    # threaded fused-lazy interpreter (kernel.cpp:1344-1411, all cores)
+    modes = {}
+    for mode, thr in (("plan", 1), ("fused-lazy", cores)):
+        _, sc = ref.run(t, expr, on, out, mode, thr)
+        modes[mode] = (sc["wall_ms"], thr)
+    mode = min(modes, key=lambda m: modes[m][0])
+    thr = modes[mode][1]
+    for _ in range(warmup):
+        ref.run(t, expr, on, out, mode, thr)
+    times = []
+    for _ in range(max(steps, 1)):
+        _, sc = ref.run(t, expr, on, out, mode, thr)
+        times.append(sc["wall_ms"])
+    ms = statistics.mean(times)
+    return {"value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "cores": thr, "kind": kind,
+            "sample": f"{sample}; reference execute_mode('{mode}', threads={thr}) "
+                      f"(plan {modes['plan'][0]:.1f} ms vs fused-lazy x{cores} "
+                      f"{modes['fused-lazy'][0]:.1f} ms)",
+            "ms_per_step": ms, "mode": mode}
+
+
+def run_reference_arm(args, wl):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    r = cpu_reference_time(wl, steps=args.steps, warmup=args.warmup)
+    line = {"metric": METRIC, "value": r["value"], "unit": "GFLOP/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference synth, seed 1)",
+            "config": wl.config(),
+            "cpu_baseline": {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"],
+                             "kind": r["kind"], "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def load_ncu_traffic(name):
+    path = os.path.join(ROOT, "profiles", f"ncu_{name}.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_b200(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_17505_b200 as P
+    from paper_2510_17505_b200 import synth as S
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P.lib()
+    # weak scaling: every rank evaluates its own independent instance of the
+    # per-GPU workload (seed + rank); no data-path collective.
+    wl.setup(torch, P, S, dev, wl.seed + rank)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        wl.step(P)
+    torch.cuda.synchronize()
+    P.lib().ixb_check_errors(None)
+
+    clocks = Clocks(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = P.lib().ixb_launch_count()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        wl.step(P)
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = P.lib().ixb_launch_count() - launches0
+    clk = clocks.stop()
+    rc = P.lib().ixb_check_errors(None)
+    if rc != 0:
+        raise RuntimeError("index error during bench: " + P.lib().ixb_last_error().decode())
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = t.item()
+    ms = total_ms / args.steps
+    value = wl.flops * ws / (ms * 1e-3) / 1e9
+
+    # e2e through the public API with pinned host buffers
+    for _ in range(2):
+        wl.e2e_step(P)
+    torch.cuda.synchronize()
+    e_evs = []
+    for _ in range(max(3, min(args.steps, 20))):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        wl.e2e_step(P)
+        b.record(stream)
+        e_evs.append((a, b))
+    torch.cuda.synchronize()
+    e_ms = statistics.mean(a.elapsed_time(b) for a, b in e_evs)
+    et = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e_ms = et.item()
+    h2d, d2h = wl.e2e_bytes()
+
+    hbm, tc, tc_sus, peak_src = load_peaks()
+    kern_s = ms * 1e-3
+    if wl.roofline_bound() == "hbm":
+        achieved = wl.alg_bytes / kern_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": load_ncu_traffic(wl.name),
+                "algorithmic_bytes_per_launch": wl.alg_bytes,
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        achieved = wl.flops / kern_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
+                "frac": achieved / tc, "traffic": load_ncu_traffic(wl.name),
+                "algorithmic_flops_per_launch": wl.flops,
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops (burst)",
+                "hbm_compulsory_frac": wl.alg_bytes / kern_s / 1e9 / hbm,
+                "l2_gather_GBps": wl.gather_bytes / kern_s / 1e9}
+
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if wl.roofline_bound() == "tensor" else "f32",
+            "data": "synthetic (reference synth streams, seed 1 + rank)",
+            "config": dict(wl.config(), l2="flushed between steps (256 MiB memset outside the "
+                                         "timed events)", parallelism=f"weak x{ws}", **wl.info),
+            "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
+            "e2e": {"value": wl.flops * ws / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e_ms}}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_time(wl)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": "GFLOP/s", "cores": None,
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]()
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    else:
+        run_b200(args, wl)
+
+
+if __name__ == "__main__":
+    main()

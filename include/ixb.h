@@ -202,6 +202,25 @@ int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ, c
  * ==================================================================== */
 int ixb_shard_groups(const int32_t* group_coord_host, int64_t G, int parts, int64_t* bounds);
 
+/* ======================================================================
+ * Seeded synthetic inputs, host side (synth.hpp:13-29): std::mt19937_64 and
+ * libstdc++'s distributions consumed exactly like synth.cpp:10-106, so one
+ * seed reproduces the reference's operands. `kind` 0 = real (+-U[0.125,1]),
+ * 1 = int (+-{1..4}); `out` 0 = f32, 1 = bf16, 2 = f64, 3 = i64 (host arrays).
+ * ==================================================================== */
+typedef struct ixb_rng ixb_rng;
+ixb_rng* ixb_rng_new(uint64_t seed);
+void ixb_rng_free(ixb_rng* rng);
+uint64_t ixb_rng_next(ixb_rng* rng);
+int ixb_synth_dense(ixb_rng* rng, int kind, int64_t numel, int out, void* dst);
+int ixb_synth_sparse_matrix(ixb_rng* rng, int kind, int64_t rows, int64_t cols, double density,
+                            int out, void* dst);
+int ixb_synth_block_sparse_matrix(ixb_rng* rng, int kind, int64_t rows, int64_t cols, int64_t br,
+                                  int64_t bc, double block_density, int out, void* dst);
+/* coords: [rank, nnz] int32 (capacity >= min(nnz, prod(shape))); *nnz_out = realised nnz. */
+int ixb_synth_coo_tensor(ixb_rng* rng, int kind, int rank, const int64_t* shape, int64_t nnz,
+                         int out, int32_t* coords, void* values, int64_t* nnz_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,11 +87,12 @@ class Rng:
     """std::mt19937_64 with libstdc++'s distributions (synth.hpp:17)."""
 
     def __init__(self, seed):
+        self._free = lib().ixo_rng_free
         self.h = lib().ixo_rng_new(seed)
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().ixo_rng_free(self.h)
+            self._free(self.h)
             self.h = None
 
     def next(self):

@@ -92,11 +92,12 @@ class Bag:
     """Named reference Tensors (+ scalars) owned by the C++ side."""
 
     def __init__(self, h=-1):
+        self._free = lib().ixr_free
         self.h = lib().ixr_bag_new() if h == -1 else _check(h)
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().ixr_free(self.h)
+            self._free(self.h)
             self.h = None
 
     def names(self):
@@ -137,11 +138,12 @@ class Bag:
 
 class Rng:
     def __init__(self, seed):
+        self._free = lib().ixr_rng_free
         self.h = lib().ixr_rng_new(seed)
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().ixr_rng_free(self.h)
+            self._free(self.h)
             self.h = None
 
     def next(self):

@@ -81,6 +81,17 @@ _SIGS = {
     "ixb_tp_grouped": (C.c_int, [C.c_void_p] * 5 + [C.c_int64, C.c_int64] + [C.c_void_p] * 3 +
                        [C.c_int] + [C.c_int64] * 7 + [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "ixb_shard_groups": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "ixb_rng_new": (C.c_void_p, [C.c_uint64]),
+    "ixb_rng_free": (None, [C.c_void_p]),
+    "ixb_rng_next": (C.c_uint64, [C.c_void_p]),
+    "ixb_synth_dense": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p]),
+    "ixb_synth_sparse_matrix": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_double,
+                                          C.c_int, C.c_void_p]),
+    "ixb_synth_block_sparse_matrix": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64,
+                                                C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                                C.c_void_p]),
+    "ixb_synth_coo_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64,
+                                       C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

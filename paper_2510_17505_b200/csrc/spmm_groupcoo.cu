@@ -298,7 +298,6 @@ void spmm_groupcoo(const int32_t* AM, const int32_t* AK, const float* AV, int64_
     sort_groups(AM, G, s, am_sorted, perm);
     use_perm = true;
   }
-  if (check) reset_error_record(s);
   SpmmArgs a;
   a.AM = use_perm ? am_sorted.p : AM;
   a.perm = use_perm ? perm.p : nullptr;

@@ -13,8 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "ixb.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*|int64_t)\s+(ixb_\w+)\s*\(",
-                                 text, re.M)))
+    return sorted(set(re.findall(r"^[A-Za-z_][\w \*]*?\b(ixb_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
