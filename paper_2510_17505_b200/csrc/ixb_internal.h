@@ -85,6 +85,18 @@ struct Scratch {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// K8 — index range validation (checked_index, plan.cpp:249-259): records the
+// first position of `idx` outside [0, extent) as `operand` in the error record.
+void validate_range(const int32_t* idx, int64_t n, int64_t extent, int operand, cudaStream_t s);
+// Whether a group-coordinate array is non-decreasing (one pass + sync).
+bool groups_sorted(const int32_t* AM, int64_t G, cudaStream_t s);
+// Stable permutation of groups by group coordinate (CUB radix sort).
+void sort_groups(const int32_t* AM, int64_t G, cudaStream_t s, Scratch<int32_t>& am_sorted,
+                 Scratch<int32_t>& perm);
+// dst[i, :] = src[perm[i], :] for rows of `row_bytes` bytes (multiple of 4).
+void gather_rows(const int32_t* perm, const void* src, void* dst, int64_t rows, int64_t row_bytes,
+                 cudaStream_t s);
+
 }  // namespace ixb
 
 // ABI guard: converts exceptions into status codes + thread-local message.

@@ -1,0 +1,468 @@
+// K4 — BlockGroupCOO SpMM on tcgen05 / TMEM / TMA (sm_100a):
+//   C[AM[p],bm,n] += AV[p,q,bm,bk] * B[AK[p,q],bk,n]   (corpus/structured_spmm.json:2)
+// bf16 operands, fp32 accumulation in TMEM. Reference semantics: oracle
+// plan.cpp:579-594 (vars p,bm,n,q,bk), plan executor plan.cpp:383-534.
+//
+// Formulation. bM = 16 is below the smallest UMMA M, so the
+// block product is computed transposed, with the dense operand as the M side:
+//     D^T[n, bm] += B_tile^T[n, bk] . AV_blk^T[bk, bm]
+//   A operand = B[AK*16 : +16, n0 : n0+128]   (128 x 16, MN-major, SW128, TMA)
+//   B operand = AV[p,q]                        (16 x 16,  K-major,  SW32,  TMA)
+//   D         = TMEM, 128 lanes (n) x 16 columns (bm) per 128-wide n subtile.
+// One UMMA M=128,N=16,K=16 per stored block and n subtile.
+//
+// Work split: CTA (chunk of CH group positions, n tile of 128*NSUB columns)
+// owns every row segment (run of equal AM) that starts in its chunk, so each
+// C block-row slice has exactly one writer (deterministic, no atomics).
+// Warp roles: warp 0 = segment scan + TMA producer, warp 1 = TMEM allocator +
+// single-thread UMMA issuer, warps 2..5 = epilogue (TMEM -> registers ->
+// coalesced fp32 stores along n). A STAGES-deep full/empty mbarrier ring
+// feeds the tensor core; accumulators are double buffered in TMEM so the
+// epilogue of segment j overlaps the main loop of segment j+1.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace ixb {
+namespace {
+
+using namespace sm100;
+
+constexpr int kMaxSeg = 32;
+constexpr int kThreadsTC = 192;  // 6 warps
+constexpr uint32_t kAvBytes = 16 * 16 * 2;
+constexpr uint32_t kSubBytes = 16 * 128 * 2;  // one 128-wide n subtile of a B tile
+
+struct TcArgs {
+  const int32_t* AM;
+  const int32_t* AK;
+  float* C;
+  int64_t G, g, KB, N, MB;
+  int chunk;
+  int accumulate;
+  int check;
+  ErrorRecord* err;
+};
+
+template <int NSUB, int STAGES>
+struct TcSmem {
+  static constexpr uint32_t kStageBytes =
+      ((NSUB * kSubBytes + kAvBytes + 1023) / 1024) * 1024;
+  static constexpr uint32_t kTileBytes = STAGES * kStageBytes;
+  static constexpr uint32_t kTotal = kTileBytes + 1024 /*barriers+table*/ + 1024 /*align*/;
+};
+
+template <int NSUB, int STAGES>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    bgcoo_tc_kernel(const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmAV, TcArgs a) {
+  using L = TcSmem<NSUB, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* tiles = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kTileBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int32_t* seg_s = reinterpret_cast<int32_t*>(tmem_base_slot + 4);
+  int32_t* seg_e = seg_s + kMaxSeg;
+  int32_t* seg_row = seg_e + kMaxSeg;
+  int32_t* seg_prev = seg_row + kMaxSeg;
+  int32_t* nseg_slot = seg_prev + kMaxSeg;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * a.chunk;
+  const int n_tile0 = blockIdx.y * 128 * NSUB;
+
+  // ---- prologue: barriers, TMEM, segment table ---------------------------
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&acc_full[b], 1);
+        mbar_init(&acc_empty[b], 4);
+      }
+      fence_barrier_init();
+      tma_prefetch_desc(&tmB);
+      tma_prefetch_desc(&tmAV);
+    }
+    // segment starts inside [base, base + chunk): AM[p] != AM[p-1]
+    const int64_t p = base + lane;
+    const bool in = lane < a.chunk && p < a.G;
+    const int am = in ? __ldg(a.AM + p) : 0;
+    const int amp = (in && p > 0) ? __ldg(a.AM + p - 1) : -1;
+    unsigned starts = __ballot_sync(0xffffffffu, in && (p == 0 || am != amp));
+    int n = 0;
+    while (starts) {
+      const int sl = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int64_t s = base + sl;
+      const int row = __shfl_sync(0xffffffffu, am, sl);
+      const int prev = __shfl_sync(0xffffffffu, amp, sl);
+      int64_t e = s + 1;
+      for (;;) {
+        const int64_t pp = e + lane;
+        const bool diff = pp >= a.G || __ldg(a.AM + pp) != row;
+        const unsigned m = __ballot_sync(0xffffffffu, diff);
+        if (m) {
+          e += __ffs(m) - 1;
+          break;
+        }
+        e += 32;
+      }
+      if (lane == 0) {
+        seg_s[n] = static_cast<int32_t>(s);
+        seg_e[n] = static_cast<int32_t>(e);
+        seg_row[n] = row;
+        seg_prev[n] = prev;
+      }
+      ++n;
+    }
+    if (lane == 0) *nseg_slot = n;
+  } else if (warp == 1) {
+    tmem_alloc(tmem_base_slot, 2 * 16 * NSUB < 32 ? 32 : 2 * 16 * NSUB);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int nseg = *nseg_slot;
+  const uint32_t tmem_base = *tmem_base_slot;
+  constexpr uint32_t kAccCols = 16 * NSUB;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    const uint64_t keep = l2_evict_last();    // dense operand: re-read by many blocks
+    const uint64_t stream = l2_evict_first();  // format: read once
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int j = 0; j < nseg; ++j) {
+      const int64_t s0 = static_cast<int64_t>(seg_s[j]) * a.g;
+      const int64_t s1 = static_cast<int64_t>(seg_e[j]) * a.g;
+      for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+        const int64_t slot = i0 + lane;
+        int k = 0;
+        if (slot < s1) {
+          k = __ldg(a.AK + slot);
+          if (k < 0 || static_cast<int64_t>(k) >= a.KB) {
+            if (a.check) report_index_error(a.err, 0, slot, k);
+            k = 0;
+          }
+        }
+        const int cnt = static_cast<int>(s1 - i0 < 32 ? s1 - i0 : 32);
+        for (int t = 0; t < cnt; ++t) {
+          const int kk = __shfl_sync(0xffffffffu, k, t);
+          if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = tiles + stage * L::kStageBytes;
+            mbar_arrive_expect_tx(&full[stage], NSUB * kSubBytes + kAvBytes);
+#pragma unroll
+            for (int sub = 0; sub < NSUB; ++sub) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                tma_load_2d(st + sub * kSubBytes + h * 2048, &tmB, &full[stage],
+                            n_tile0 + sub * 128 + h * 64, kk * 16, keep);
+              }
+            }
+            tma_load_2d(st + NSUB * kSubBytes, &tmAV, &full[stage], 0,
+                        static_cast<int32_t>((i0 + t) * 16), stream);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- UMMA issuer
+    constexpr uint32_t idesc = idesc_bf16_f32(128, 16, /*A MN-major*/ true, /*B K-major*/ false);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int j = 0; j < nseg; ++j) {
+      const int buf = j & 1;
+      mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const int64_t nslots = (static_cast<int64_t>(seg_e[j]) - seg_s[j]) * a.g;
+      for (int64_t i = 0; i < nslots; ++i) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
+          const uint64_t bdesc = smem_desc(st + NSUB * kSubBytes, 16, 256, kLayoutSW32);
+#pragma unroll
+          for (int sub = 0; sub < NSUB; ++sub) {
+            // A: 2 MN atoms (64 n each) at +2048, K groups of 8 rows at +1024
+            const uint64_t adesc = smem_desc(st + sub * kSubBytes, 2048, 1024, kLayoutSW128);
+            umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc, i > 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
+          if (i + 1 == nslots) umma_commit(&acc_full[buf]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+    const int nloc = quarter * 32 + lane;
+    for (int j = 0; j < nseg; ++j) {
+      const int buf = j & 1;
+      const int row = seg_row[j];
+      const bool row_ok = row >= 0 && static_cast<int64_t>(row) < a.MB;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int sub = 0; sub < NSUB; ++sub) {
+        uint32_t r[16];
+        tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               buf * kAccCols + sub * 16,
+                           r);
+        tmem_ld_wait();
+        if (row_ok) {
+          float* c = a.C + static_cast<int64_t>(row) * 16 * a.N + n_tile0 + sub * 128 + nloc;
+#pragma unroll
+          for (int bm = 0; bm < 16; ++bm) {
+            float v = __uint_as_float(r[bm]);
+            if (a.accumulate) v += c[static_cast<int64_t>(bm) * a.N];
+            c[static_cast<int64_t>(bm) * a.N] = v;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (!row_ok && a.check && warp == 2 && lane == 0 && blockIdx.y == 0) {
+        report_index_error(a.err, 1, seg_s[j], row);
+      }
+      if (!a.accumulate) {
+        // `=`: zero the empty block-rows before this segment (and after the last)
+        const int64_t z0 = seg_prev[j] + 1 < 0 ? 0 : seg_prev[j] + 1;
+        const int64_t z1 = row < 0 ? 0 : (row > a.MB ? a.MB : row);
+        const bool last = seg_e[j] == a.G;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int64_t r0 = pass == 0 ? z0 : (row + 1 < 0 ? 0 : row + 1);
+          const int64_t r1 = pass == 0 ? z1 : (last ? a.MB : 0);
+          for (int64_t br = r0; br < r1; ++br) {
+            for (int sub = 0; sub < NSUB; ++sub) {
+              float* c = a.C + br * 16 * a.N + n_tile0 + sub * 128 + nloc;
+#pragma unroll
+              for (int bm = 0; bm < 16; ++bm) c[static_cast<int64_t>(bm) * a.N] = 0.f;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * 16 * NSUB < 32 ? 32 : 2 * 16 * NSUB);
+  }
+}
+
+// ----------------------------------------------------- CUDA-core fallback
+// Any bm/bk/N: CTA per (group position chunk of 1) handles segment starts;
+// thread (bm, n) accumulates over the segment's blocks in slot order.
+__global__ void bgcoo_simt_kernel(const int32_t* AM, const int32_t* AK,
+                                  const __nv_bfloat16* AV, const __nv_bfloat16* B, float* C,
+                                  int64_t G, int64_t g, int64_t bm, int64_t bk, int64_t KB,
+                                  int64_t N, int64_t MB, int accumulate, int check,
+                                  ErrorRecord* err) {
+  const int64_t p = blockIdx.x;
+  if (p >= G) return;
+  const int row = AM[p];
+  if (p > 0 && AM[p - 1] == row) return;  // not a segment start
+  int64_t e = p + 1;
+  while (e < G && AM[e] == row) ++e;
+  const int prev = p > 0 ? AM[p - 1] : -1;
+  const bool row_ok = row >= 0 && row < MB;
+  if (!accumulate) {
+    const int64_t z0 = prev + 1 < 0 ? 0 : prev + 1;
+    const int64_t z1 = row < 0 ? 0 : (row > MB ? MB : row);
+    for (int64_t i = z0 * bm * N + threadIdx.x; i < z1 * bm * N; i += blockDim.x) C[i] = 0.f;
+    if (e == G) {
+      const int64_t r0 = row + 1 < 0 ? 0 : row + 1;
+      for (int64_t i = r0 * bm * N + threadIdx.x; i < MB * bm * N; i += blockDim.x) C[i] = 0.f;
+    }
+  }
+  if (!row_ok) {
+    if (check && threadIdx.x == 0) report_index_error(err, 1, p, row);
+  }
+  for (int64_t o = threadIdx.x; o < bm * N; o += blockDim.x) {
+    const int64_t i = o / N, n = o % N;
+    float acc = 0.f;
+    for (int64_t slot = p * g; slot < e * g; ++slot) {
+      const int k = AK[slot];
+      if (k < 0 || k >= KB) {
+        if (check) report_index_error(err, 0, slot, k);
+        continue;
+      }
+      const __nv_bfloat16* av = AV + slot * bm * bk + i * bk;
+      const __nv_bfloat16* b = B + static_cast<int64_t>(k) * bk * N + n;
+      for (int64_t t = 0; t < bk; ++t) {
+        acc = fmaf(__bfloat162float(av[t]), __bfloat162float(b[t * N]), acc);
+      }
+    }
+    if (row_ok) {
+      float* c = C + (static_cast<int64_t>(row) * bm + i) * N + n;
+      *c = accumulate ? *c + acc : acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+  });
+  if (!fn) fail(IXB_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                        uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(IXB_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <int NSUB, int STAGES>
+void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, const TcArgs& a, cudaStream_t s) {
+  using L = TcSmem<NSUB, STAGES>;
+  auto kern = bgcoo_tc_kernel<NSUB, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    IXB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        L::kTotal));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(a.G, a.chunk)),
+            static_cast<unsigned>(a.N / (128 * NSUB)));
+  kern<<<grid, kThreadsTC, L::kTotal, s>>>(tmB, tmAV, a);
+  IXB_LAUNCH_CHECK("bgcoo_tc_kernel");
+}
+
+}  // namespace
+
+
+void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, int64_t G,
+                        int64_t g, int64_t bm, int64_t bk, const void* B, int64_t KB, int64_t N,
+                        float* C, int64_t MB, int accumulate, int flags, cudaStream_t s) {
+  if (G < 0 || g < 1 || bm < 1 || bk < 1 || KB < 0 || N < 0 || MB < 0)
+    fail(IXB_SHAPE, "ixb_spmm_blockgroupcoo: bad extents");
+  const bool check = !(flags & IXB_UNCHECKED);
+  if (N == 0 || MB == 0) return;
+  if (G == 0) {
+    if (!accumulate) IXB_CUDA_CHECK(cudaMemsetAsync(C, 0, MB * bm * N * sizeof(float), s));
+    return;
+  }
+  if (G * g * bk > INT32_MAX || KB * bk > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 rows");
+  // Unsorted group coordinates: validate the original arrays (K8), then
+  // evaluate over a stably sorted copy of the format (rows of AK/AV gathered
+  // by the permutation), which keeps every output row's summation order.
+  Scratch<int32_t> am_sorted, perm, ak_sorted;
+  Scratch<__nv_bfloat16> av_sorted;
+  if (!(flags & IXB_GROUPS_SORTED) && !groups_sorted(AM, G, s)) {
+    if (check) {
+      validate_range(AK, G * g, KB, 0, s);
+      validate_range(AM, G, MB, 1, s);
+      OperandInfo ops[2] = {{"AK", "B", 0, KB, AK, G * g}, {"AM", "C", 0, MB, AM, G}};
+      check_error_record(s, ops, 2);
+    }
+    sort_groups(AM, G, s, am_sorted, perm);
+    ak_sorted = Scratch<int32_t>(G * g, s);
+    av_sorted = Scratch<__nv_bfloat16>(G * g * bm * bk, s);
+    gather_rows(perm.p, AK, ak_sorted.p, G, g * 4, s);
+    gather_rows(perm.p, AV, av_sorted.p, G, g * bm * bk * 2, s);
+    AM = am_sorted.p;
+    AK = ak_sorted.p;
+    AV = av_sorted.p;
+    flags |= IXB_UNCHECKED;
+  }
+  const bool check2 = !(flags & IXB_UNCHECKED);
+  ErrorRecord* err = device_error_record();
+  const bool tc_ok = bm == 16 && bk == 16 && N % 128 == 0 &&
+                     reinterpret_cast<uintptr_t>(B) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(AV) % 16 == 0;
+  if (tc_ok) {
+    TcArgs a;
+    a.AM = AM;
+    a.AK = AK;
+    a.C = C;
+    a.G = G;
+    a.g = g;
+    a.KB = KB;
+    a.N = N;
+    a.MB = MB;
+    int64_t ch = MB > 0 ? G / MB : 1;
+    a.chunk = static_cast<int>(ch < 1 ? 1 : (ch > kMaxSeg ? kMaxSeg : ch));
+    a.accumulate = accumulate;
+    a.check = check2;
+    a.err = err;
+    const CUtensorMap tmB = make_map_2d(B, N, KB * 16, N * 2, 64, 16,
+                                        CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap tmAV = make_map_2d(AV, 16, G * g * 16, 32, 16, 16,
+                                         CU_TENSOR_MAP_SWIZZLE_32B);
+    if (N % 512 == 0) {
+      launch_tc<2, 8>(tmB, tmAV, a, s);
+    } else if (N % 256 == 0) {
+      launch_tc<2, 8>(tmB, tmAV, a, s);
+    } else {
+      launch_tc<1, 8>(tmB, tmAV, a, s);
+    }
+  } else {
+    const int threads = 256;
+    bgcoo_simt_kernel<<<static_cast<unsigned>(G), threads, 0, s>>>(
+        AM, AK, static_cast<const __nv_bfloat16*>(AV), static_cast<const __nv_bfloat16*>(B), C,
+        G, g, bm, bk, KB, N, MB, accumulate, check2, err);
+    IXB_LAUNCH_CHECK("bgcoo_simt_kernel");
+  }
+  if (check2 && !(flags & IXB_ASYNC)) {
+    OperandInfo ops[2] = {{"AK", "B", 0, KB, AK, G * g}, {"AM", "C", 0, MB, AM, G}};
+    check_error_record(s, ops, 2);
+  }
+}
+
+}  // namespace ixb
+
+extern "C" int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV,
+                                      int64_t G, int64_t g, int64_t bm, int64_t bk, const void* B,
+                                      int64_t KB, int64_t N, float* C, int64_t MB, int accumulate,
+                                      int flags, ixb_stream stream) {
+  return ixb_guard([&] {
+    ixb::spmm_blockgroupcoo(AM, AK, AV, G, g, bm, bk, B, KB, N, C, MB, accumulate, flags,
+                            reinterpret_cast<cudaStream_t>(stream));
+  });
+}

@@ -97,7 +97,7 @@ template <int VEC, int T, bool PERM>
 __global__ void __launch_bounds__(kThreads, 2) spmm_groupcoo_kernel(SpmmArgs a) {
   using V = typename VecT<VEC>::T;
   constexpr int kColsPerPass = 32 * VEC * T;
-  constexpr int kUnroll = T >= 4 ? 4 : 8;  // 8-16 independent gathers in flight per lane
+  constexpr int kUnroll = T >= 4 ? 4 : (T == 2 ? 8 : 16);  // 16 gathers in flight per lane
   const int lane = lane_id();
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t base = warp * a.chunk;
@@ -166,48 +166,59 @@ __global__ void __launch_bounds__(kThreads, 2) spmm_groupcoo_kernel(SpmmArgs a) 
         col[t] = c0 + (t * 32 + lane) * VEC;
         col_ok[t] = col[t] < a.N;
       }
-      for (int64_t p = s; p < e; ++p) {
-        const int64_t gp = PERM ? __ldg(a.perm + p) : p;
-        const int32_t* ak = a.AK + gp * a.g;
-        const float* av = a.AV + gp * a.g;
-        for (int64_t q0 = 0; q0 < a.g; q0 += 32) {
-          const int qn = static_cast<int>(a.g - q0 < 32 ? a.g - q0 : 32);
-          int my_k = 0;
-          float my_v = 0.f;
-          if (lane < qn) {
-            my_k = ldg_i_stream(ak + q0 + lane, stream);
-            my_v = ldg_f_stream(av + q0 + lane, stream);
-            if (my_k < 0 || static_cast<int64_t>(my_k) >= a.K) {
-              if (a.check) report_index_error(a.err, 0, gp * a.g + q0 + lane, my_k);
-              my_k = 0;
-              my_v = 0.f;
-            }
-          }
-          for (int q = 0; q < qn; q += kUnroll) {
-            int kk[kUnroll];
-            float vv[kUnroll];
-#pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
-              kk[j] = __shfl_sync(0xffffffffu, my_k, (q + j) & 31);
-              vv[j] = __shfl_sync(0xffffffffu, my_v, (q + j) & 31);
-            }
-            V bv[kUnroll][T];
-#pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
-              const float* brow = a.B + static_cast<int64_t>(kk[j]) * a.N;
-#pragma unroll
-              for (int t = 0; t < T; ++t) {
-                if (q + j < qn && col_ok[t]) bv[j][t] = ld_b<VEC>(brow + col[t], keep);
-                else vzero(bv[j][t]);
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < kUnroll; ++j) {
-#pragma unroll
-              for (int t = 0; t < T; ++t) vfma(acc[t], vv[j], bv[j][t]);
-            }
+      // The segment's slots as one stream (group order, then q): 32 slots of
+      // metadata per coalesced load, the next chunk prefetched while the
+      // current one's gathers are in flight. Summation order = (p, q) order.
+      const int64_t nslots = (e - s) * a.g;
+      auto load_meta = [&](int64_t i0, int& k, float& v) {
+        k = 0;
+        v = 0.f;
+        const int64_t i = i0 + lane;
+        if (i < nslots) {
+          const int64_t grp = s + i / a.g;
+          const int64_t gp = PERM ? __ldg(a.perm + grp) : grp;
+          const int64_t slot = gp * a.g + i % a.g;
+          k = ldg_i_stream(a.AK + slot, stream);
+          v = ldg_f_stream(a.AV + slot, stream);
+          if (k < 0 || static_cast<int64_t>(k) >= a.K) {
+            if (a.check) report_index_error(a.err, 0, slot, k);
+            k = 0;
+            v = 0.f;
           }
         }
+      };
+      int nk, my_k;
+      float nv, my_v;
+      load_meta(0, my_k, my_v);
+      for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
+        load_meta(i0 + 32, nk, nv);  // prefetch next chunk
+        const int qn = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
+        for (int q = 0; q < qn; q += kUnroll) {
+          int kk[kUnroll];
+          float vv[kUnroll];
+#pragma unroll
+          for (int j = 0; j < kUnroll; ++j) {
+            kk[j] = __shfl_sync(0xffffffffu, my_k, (q + j) & 31);
+            vv[j] = __shfl_sync(0xffffffffu, my_v, (q + j) & 31);
+          }
+          V bv[kUnroll][T];
+#pragma unroll
+          for (int j = 0; j < kUnroll; ++j) {
+            const float* brow = a.B + static_cast<int64_t>(kk[j]) * a.N;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+              if (q + j < qn && col_ok[t]) bv[j][t] = ld_b<VEC>(brow + col[t], keep);
+              else vzero(bv[j][t]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kUnroll; ++j) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) vfma(acc[t], vv[j], bv[j][t]);
+          }
+        }
+        my_k = nk;
+        my_v = nv;
       }
 #pragma unroll
       for (int t = 0; t < T; ++t) {
