@@ -54,9 +54,6 @@ def test_blockgroupcoo_builder_bit_exact(P, ixo, dtype):
                                                gd)
                 gsz = got.group_size
                 want = ixo.dense_to_blockgroupcoo(a, bm, bk, gsz, gd)
-                if gg == 0:  # tuner over block occupancy (driver.cpp:106-113 semantics)
-                    occ = np.bincount(want["AM"] if gd == 0 else want["AM"],
-                                      minlength=1) if False else None
                 for k in ("AM", "AK", "mask"):
                     np.testing.assert_array_equal(getattr(got, k).cpu().numpy(),
                                                   want[k].astype(np.int64 if k != "mask" else np.uint8),
