@@ -31,7 +31,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DEFAULT_WORKLOAD = "cfg1"
+DEFAULT_WORKLOAD = "cfg2"
 
 
 # --------------------------------------------------------------- helpers
