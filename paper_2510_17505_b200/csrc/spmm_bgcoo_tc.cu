@@ -21,6 +21,7 @@
 // epilogue of segment j overlaps the main loop of segment j+1.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -31,8 +32,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kMaxSeg = 32;
-constexpr int kThreadsTC = 192;  // 6 warps
+constexpr int kThreadsTC = 224;  // 7 warps
 constexpr uint32_t kAvBytes = 16 * 16 * 2;
 constexpr uint32_t kSubBytes = 16 * 128 * 2;  // one 128-wide n subtile of a B tile
 
@@ -41,21 +41,89 @@ struct TcArgs {
   const int32_t* AK;
   float* C;
   int64_t G, g, KB, N, MB;
-  int chunk;
+  int chunk;    // group positions scanned per work item
+  int nchunks;  // ceil(G / chunk)
+  int ntiles;   // n tiles of 128*NSUB columns
   int accumulate;
   int check;
+  int epi_sleep_ns;  // epilogue warps back off instead of spinning on acc_full
   ErrorRecord* err;
 };
 
 template <int NSUB, int STAGES>
 struct TcSmem {
-  static constexpr uint32_t kStageBytes =
-      ((NSUB * kSubBytes + kAvBytes + 1023) / 1024) * 1024;
+  static constexpr uint32_t kBBytes = NSUB * kSubBytes;
+  static constexpr uint32_t kStageBytes = ((kBBytes + kAvBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t kTileBytes = STAGES * kStageBytes;
-  static constexpr uint32_t kTotal = kTileBytes + 1024 /*barriers+table*/ + 1024 /*align*/;
+  static constexpr uint32_t kTotal = kTileBytes + 1024 /*barriers+queue*/ + 1024 /*align*/;
 };
 
-template <int NSUB, int STAGES>
+// A row segment (run of equal AM) owned by a work item.
+struct Seg {
+  int64_t s, e;   // group range [s, e)
+  int row, prev;  // AM value, AM[s-1] (or -1)
+  int ntile;      // n tile index
+};
+
+// Walks this CTA's work items (chunk, n tile), round-robin over the grid,
+// and yields every segment that starts inside the chunk. Warp-collective;
+// each role warp runs its own copy and sees the identical sequence.
+struct SegIter {
+  int64_t w;        // current work item
+  int64_t base;     // first group position of the chunk
+  unsigned starts;  // pending segment starts (lane bits) in the chunk
+  int am, amp;      // this lane's AM[base+lane], AM[base+lane-1]
+  int ntile;
+
+  __device__ __forceinline__ void load(const TcArgs& a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t chunk_id = w / a.ntiles;
+    ntile = static_cast<int>(w % a.ntiles);
+    base = chunk_id * a.chunk;
+    const int64_t p = base + lane;
+    const bool in = lane < a.chunk && p < a.G;
+    am = in ? __ldg(a.AM + p) : 0;
+    amp = (in && p > 0) ? __ldg(a.AM + p - 1) : -1;
+    starts = __ballot_sync(0xffffffffu, in && (p == 0 || am != amp));
+  }
+  __device__ __forceinline__ void init(const TcArgs& a) {
+    w = blockIdx.x;
+    if (w < static_cast<int64_t>(a.nchunks) * a.ntiles) load(a);
+    else starts = 0;
+  }
+  __device__ __forceinline__ bool next(const TcArgs& a, Seg& out) {
+    const int64_t total = static_cast<int64_t>(a.nchunks) * a.ntiles;
+    while (starts == 0) {
+      w += gridDim.x;
+      if (w >= total) return false;
+      load(a);
+    }
+    const int lane = threadIdx.x & 31;
+    const int sl = __ffs(starts) - 1;
+    starts &= starts - 1;
+    out.s = base + sl;
+    out.row = __shfl_sync(0xffffffffu, am, sl);
+    out.prev = __shfl_sync(0xffffffffu, amp, sl);
+    out.ntile = ntile;
+    int64_t e = out.s + 1;
+    for (;;) {
+      const int64_t pp = e + lane;
+      const bool diff = pp >= a.G || __ldg(a.AM + pp) != out.row;
+      const unsigned m = __ballot_sync(0xffffffffu, diff);
+      if (m) {
+        e += __ffs(m) - 1;
+        break;
+      }
+      e += 32;
+    }
+    out.e = e;
+    return true;
+  }
+};
+
+constexpr int kQN = 16;  // segment queue depth (scheduler -> roles)
+
+template <int NSUB, int STAGES, int NACC>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     bgcoo_tc_kernel(const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmAV, TcArgs a) {
@@ -67,88 +135,94 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kTileBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  int32_t* seg_s = reinterpret_cast<int32_t*>(tmem_base_slot + 4);
-  int32_t* seg_e = seg_s + kMaxSeg;
-  int32_t* seg_row = seg_e + kMaxSeg;
-  int32_t* seg_prev = seg_row + kMaxSeg;
-  int32_t* nseg_slot = seg_prev + kMaxSeg;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint64_t* seg_full = acc_empty + NACC;
+  uint64_t* seg_empty = seg_full + kQN;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(seg_empty + kQN);
+  int4* segq = reinterpret_cast<int4*>(tmem_base_slot + 4);  // {s, e, row, prev}
+  int* segq_tile = reinterpret_cast<int*>(segq + kQN);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * a.chunk;
-  const int n_tile0 = blockIdx.y * 128 * NSUB;
+  constexpr uint32_t kAccCols = 16 * NSUB;  // one accumulator buffer
+  constexpr uint32_t kTmemCols = NACC * kAccCols <= 32    ? 32
+                                 : NACC * kAccCols <= 64  ? 64
+                                 : NACC * kAccCols <= 128 ? 128
+                                 : NACC * kAccCols <= 256 ? 256
+                                                          : 512;
 
-  // ---- prologue: barriers, TMEM, segment table ---------------------------
   if (warp == 0) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
       }
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < NACC; ++b) {
         mbar_init(&acc_full[b], 1);
         mbar_init(&acc_empty[b], 4);
+      }
+      for (int q = 0; q < kQN; ++q) {
+        mbar_init(&seg_full[q], 1);
+        mbar_init(&seg_empty[q], 6);  // producer, UMMA issuer, 4 epilogue warps
       }
       fence_barrier_init();
       tma_prefetch_desc(&tmB);
       tma_prefetch_desc(&tmAV);
     }
-    // segment starts inside [base, base + chunk): AM[p] != AM[p-1]
-    const int64_t p = base + lane;
-    const bool in = lane < a.chunk && p < a.G;
-    const int am = in ? __ldg(a.AM + p) : 0;
-    const int amp = (in && p > 0) ? __ldg(a.AM + p - 1) : -1;
-    unsigned starts = __ballot_sync(0xffffffffu, in && (p == 0 || am != amp));
-    int n = 0;
-    while (starts) {
-      const int sl = __ffs(starts) - 1;
-      starts &= starts - 1;
-      const int64_t s = base + sl;
-      const int row = __shfl_sync(0xffffffffu, am, sl);
-      const int prev = __shfl_sync(0xffffffffu, amp, sl);
-      int64_t e = s + 1;
-      for (;;) {
-        const int64_t pp = e + lane;
-        const bool diff = pp >= a.G || __ldg(a.AM + pp) != row;
-        const unsigned m = __ballot_sync(0xffffffffu, diff);
-        if (m) {
-          e += __ffs(m) - 1;
-          break;
-        }
-        e += 32;
-      }
-      if (lane == 0) {
-        seg_s[n] = static_cast<int32_t>(s);
-        seg_e[n] = static_cast<int32_t>(e);
-        seg_row[n] = row;
-        seg_prev[n] = prev;
-      }
-      ++n;
-    }
-    if (lane == 0) *nseg_slot = n;
   } else if (warp == 1) {
-    tmem_alloc(tmem_base_slot, 2 * 16 * NSUB < 32 ? 32 : 2 * 16 * NSUB);
+    tmem_alloc(tmem_base_slot, kTmemCols);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const int nseg = *nseg_slot;
   const uint32_t tmem_base = *tmem_base_slot;
-  constexpr uint32_t kAccCols = 16 * NSUB;
 
-  if (warp == 0) {
-    // ---------------------------------------------------------- producer
+  // Segment queue consumers: entry q holds {s, e, row, prev} + n tile; s < 0 ends.
+  auto pop = [&](int j, int4& sg, int& tile) {
+    const int q = j % kQN;
+    mbar_wait(&seg_full[q], (j / kQN) & 1);
+    sg = segq[q];
+    tile = segq_tile[q];
+  };
+  auto release = [&](int j) { mbar_arrive(&seg_empty[j % kQN]); };
+
+  if (warp == 6) {
+    // ---------------------------------------------------------- scheduler
+    // Discovers segments ahead of the pipeline so no role stalls on the
+    // dependent AM loads between segments.
+    SegIter it;
+    it.init(a);
+    Seg sg;
+    int j = 0;
+    bool more = true;
+    while (more) {
+      more = it.next(a, sg);
+      const int q = j % kQN;
+      if (lane == 0) {
+        mbar_wait(&seg_empty[q], ((j / kQN) & 1) ^ 1);
+        segq[q] = more ? make_int4(static_cast<int>(sg.s), static_cast<int>(sg.e), sg.row, sg.prev)
+                       : make_int4(-1, -1, 0, 0);
+        segq_tile[q] = more ? sg.ntile : 0;
+        mbar_arrive(&seg_full[q]);
+      }
+      __syncwarp();
+      ++j;
+    }
+  } else if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer
     const uint64_t keep = l2_evict_last();    // dense operand: re-read by many blocks
     const uint64_t stream = l2_evict_first();  // format: read once
     int stage = 0;
     uint32_t phase = 0;
-    for (int j = 0; j < nseg; ++j) {
-      const int64_t s0 = static_cast<int64_t>(seg_s[j]) * a.g;
-      const int64_t s1 = static_cast<int64_t>(seg_e[j]) * a.g;
-      for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+    for (int j = 0;; ++j) {
+      int4 sg;
+      int tile;
+      pop(j, sg, tile);
+      if (sg.x < 0) break;
+      const int n0 = tile * 128 * NSUB;
+      const int64_t s0 = static_cast<int64_t>(sg.x) * a.g, s1 = static_cast<int64_t>(sg.y) * a.g;
+      auto load_k = [&](int64_t i0) {
         const int64_t slot = i0 + lane;
         int k = 0;
         if (slot < s1) {
@@ -158,121 +232,136 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             k = 0;
           }
         }
+        return k;
+      };
+      int k = load_k(s0);
+      for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+        const int k_next = load_k(i0 + 32);  // prefetch the next 32 member coords
         const int cnt = static_cast<int>(s1 - i0 < 32 ? s1 - i0 : 32);
         for (int t = 0; t < cnt; ++t) {
           const int kk = __shfl_sync(0xffffffffu, k, t);
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* st = tiles + stage * L::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], NSUB * kSubBytes + kAvBytes);
-#pragma unroll
-            for (int sub = 0; sub < NSUB; ++sub) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                tma_load_2d(st + sub * kSubBytes + h * 2048, &tmB, &full[stage],
-                            n_tile0 + sub * 128 + h * 64, kk * 16, keep);
-              }
-            }
-            tma_load_2d(st + NSUB * kSubBytes, &tmAV, &full[stage], 0,
+            mbar_arrive_expect_tx(&full[stage], L::kBBytes + kAvBytes);
+            // one 3-D box {64 n, 16 rows, 2*NSUB atoms} lands as [atom][row][64]
+            tma_load_3d(st, &tmB, &full[stage], 0, kk * 16, n0 / 64, keep);
+            tma_load_2d(st + L::kBBytes, &tmAV, &full[stage], 0,
                         static_cast<int32_t>((i0 + t) * 16), stream);
           }
-          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+        k = k_next;
       }
+      __syncwarp();
+      if (lane == 0) release(j);
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- UMMA issuer
     constexpr uint32_t idesc = idesc_bf16_f32(128, 16, /*A MN-major*/ true, /*B K-major*/ false);
     int stage = 0;
     uint32_t phase = 0;
-    for (int j = 0; j < nseg; ++j) {
-      const int buf = j & 1;
-      mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+    for (int j = 0;; ++j) {
+      int4 sg;
+      int tile;
+      pop(j, sg, tile);
+      if (sg.x < 0) break;
+      const int buf = j % NACC;
+      mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
       tc_fence_after();
-      const int64_t nslots = (static_cast<int64_t>(seg_e[j]) - seg_s[j]) * a.g;
+      const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
       for (int64_t i = 0; i < nslots; ++i) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
         if (lane == 0) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
           const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
-          const uint64_t bdesc = smem_desc(st + NSUB * kSubBytes, 16, 256, kLayoutSW32);
+          const uint64_t bdesc = smem_desc(st + L::kBBytes, 16, 256, kLayoutSW32);
 #pragma unroll
           for (int sub = 0; sub < NSUB; ++sub) {
-            // A: 2 MN atoms (64 n each) at +2048, K groups of 8 rows at +1024
+            // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
             const uint64_t adesc = smem_desc(st + sub * kSubBytes, 2048, 1024, kLayoutSW128);
             umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc, i > 0 ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
           if (i + 1 == nslots) umma_commit(&acc_full[buf]);
         }
-        __syncwarp();
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
+      __syncwarp();
+      if (lane == 0) release(j);
     }
   } else {
     // ---------------------------------------------------------- epilogue
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
     const int nloc = quarter * 32 + lane;
-    for (int j = 0; j < nseg; ++j) {
-      const int buf = j & 1;
-      const int row = seg_row[j];
+    for (int j = 0;; ++j) {
+      int4 sg;
+      int tile;
+      pop(j, sg, tile);
+      if (sg.x < 0) break;
+      const int buf = j % NACC;
+      const int row = sg.z;
+      const int n0 = tile * 128 * NSUB;
       const bool row_ok = row >= 0 && static_cast<int64_t>(row) < a.MB;
-      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      mbar_wait_backoff(&acc_full[buf], (j / NACC) & 1, a.epi_sleep_ns);
       tc_fence_after();
+      uint32_t r[NSUB][16];
 #pragma unroll
       for (int sub = 0; sub < NSUB; ++sub) {
-        uint32_t r[16];
         tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                buf * kAccCols + sub * 16,
-                           r);
-        tmem_ld_wait();
-        if (row_ok) {
-          float* c = a.C + static_cast<int64_t>(row) * 16 * a.N + n_tile0 + sub * 128 + nloc;
+                           r[sub]);
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM buffer free for segment j+NACC
+      if (row_ok) {
+#pragma unroll
+        for (int sub = 0; sub < NSUB; ++sub) {
+          float* c = a.C + static_cast<int64_t>(row) * 16 * a.N + n0 + sub * 128 + nloc;
 #pragma unroll
           for (int bm = 0; bm < 16; ++bm) {
-            float v = __uint_as_float(r[bm]);
+            float v = __uint_as_float(r[sub][bm]);
             if (a.accumulate) v += c[static_cast<int64_t>(bm) * a.N];
             c[static_cast<int64_t>(bm) * a.N] = v;
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
-      if (!row_ok && a.check && warp == 2 && lane == 0 && blockIdx.y == 0) {
-        report_index_error(a.err, 1, seg_s[j], row);
+      } else if (a.check && warp == 2 && lane == 0 && tile == 0) {
+        report_index_error(a.err, 1, sg.x, row);
       }
       if (!a.accumulate) {
         // `=`: zero the empty block-rows before this segment (and after the last)
-        const int64_t z0 = seg_prev[j] + 1 < 0 ? 0 : seg_prev[j] + 1;
+        const int64_t z0 = sg.w + 1 < 0 ? 0 : sg.w + 1;
         const int64_t z1 = row < 0 ? 0 : (row > a.MB ? a.MB : row);
-        const bool last = seg_e[j] == a.G;
+        const bool last = sg.y == a.G;
         for (int pass = 0; pass < 2; ++pass) {
           const int64_t r0 = pass == 0 ? z0 : (row + 1 < 0 ? 0 : row + 1);
           const int64_t r1 = pass == 0 ? z1 : (last ? a.MB : 0);
           for (int64_t br = r0; br < r1; ++br) {
             for (int sub = 0; sub < NSUB; ++sub) {
-              float* c = a.C + br * 16 * a.N + n_tile0 + sub * 128 + nloc;
+              float* c = a.C + br * 16 * a.N + n0 + sub * 128 + nloc;
 #pragma unroll
               for (int bm = 0; bm < 16; ++bm) c[static_cast<int64_t>(bm) * a.N] = 0.f;
             }
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) release(j);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * 16 * NSUB < 32 ? 32 : 2 * 16 * NSUB);
+    tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 
@@ -358,24 +447,43 @@ CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer, uint64
   return m;
 }
 
-template <int NSUB, int STAGES>
-void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, const TcArgs& a, cudaStream_t s) {
+CUtensorMap make_map_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                        uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2,
+                        CUtensorMapSwizzle sw) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(IXB_CUDA, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
+  return m;
+}
+
+template <int NSUB, int STAGES, int NACC>
+void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaStream_t s) {
   using L = TcSmem<NSUB, STAGES>;
-  auto kern = bgcoo_tc_kernel<NSUB, STAGES>;
+  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC>;
   static bool attr = false;
   if (!attr) {
     IXB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         L::kTotal));
     attr = true;
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(a.G, a.chunk)),
-            static_cast<unsigned>(a.N / (128 * NSUB)));
-  kern<<<grid, kThreadsTC, L::kTotal, s>>>(tmB, tmAV, a);
+  a.ntiles = static_cast<int>(a.N / (128 * NSUB));
+  const int64_t items = static_cast<int64_t>(a.nchunks) * a.ntiles;
+  int per_sm = static_cast<int>((220u * 1024u) / L::kTotal);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // persistent CTAs
+  if (grid > items) grid = items;
+  kern<<<static_cast<unsigned>(grid), kThreadsTC, L::kTotal, s>>>(tmB, tmAV, a);
   IXB_LAUNCH_CHECK("bgcoo_tc_kernel");
 }
 
 }  // namespace
-
 
 void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, int64_t G,
                         int64_t g, int64_t bm, int64_t bk, const void* B, int64_t KB, int64_t N,
@@ -427,20 +535,35 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     a.N = N;
     a.MB = MB;
     int64_t ch = MB > 0 ? G / MB : 1;
-    a.chunk = static_cast<int>(ch < 1 ? 1 : (ch > kMaxSeg ? kMaxSeg : ch));
+    a.chunk = static_cast<int>(ch < 1 ? 1 : (ch > 32 ? 32 : ch));
     a.accumulate = accumulate;
     a.check = check2;
     a.err = err;
-    const CUtensorMap tmB = make_map_2d(B, N, KB * 16, N * 2, 64, 16,
+    a.nchunks = static_cast<int>(ceil_div(G, a.chunk));
+    const int nsub = N % 256 == 0 ? 2 : 1;
+    // B viewed as {64 n, rows, N/64 atoms}: one TMA box = the whole n tile of
+    // 16 rows, landing as [atom][row][64] (the MN-major SW128 canonical layout)
+    const CUtensorMap tmB = make_map_3d(B, 64, KB * 16, N / 64, N * 2, 128, 64, 16, 2 * nsub,
                                         CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tmAV = make_map_2d(AV, 16, G * g * 16, 32, 16, 16,
                                          CU_TENSOR_MAP_SWIZZLE_32B);
-    if (N % 512 == 0) {
-      launch_tc<2, 8>(tmB, tmAV, a, s);
-    } else if (N % 256 == 0) {
-      launch_tc<2, 8>(tmB, tmAV, a, s);
+    static const int variant = getenv("IXB_BG_VARIANT") ? atoi(getenv("IXB_BG_VARIANT")) : 0;
+    static const int sleep_ns = getenv("IXB_BG_SLEEP") ? atoi(getenv("IXB_BG_SLEEP")) : 256;
+    a.epi_sleep_ns = sleep_ns;
+    if (nsub == 1) {
+      launch_tc<1, 12, 4>(tmB, tmAV, a, s);
+    } else if (variant == 1) {
+      launch_tc<2, 6, 2>(tmB, tmAV, a, s);
+    } else if (variant == 2) {
+      launch_tc<2, 6, 4>(tmB, tmAV, a, s);
+    } else if (variant == 3) {
+      launch_tc<2, 10, 4>(tmB, tmAV, a, s);
+    } else if (variant == 4) {
+      launch_tc<2, 4, 4>(tmB, tmAV, a, s);
+    } else if (variant == 5) {
+      launch_tc<2, 16, 4>(tmB, tmAV, a, s);
     } else {
-      launch_tc<1, 8>(tmB, tmAV, a, s);
+      launch_tc<2, 6, 4>(tmB, tmAV, a, s);
     }
   } else {
     const int threads = 256;
