@@ -123,10 +123,11 @@ int ixb_blockgroupcoo_pack(ixb_pack* plan, int32_t* AM, int32_t* AK, void* AV, u
 
 /* group_coo_tensor (formats.hpp:141, formats.cpp:417-479): rank-n COO
  * (coords: `rank` device arrays of nnz int32) grouped along group_dim; sort
- * key (group coord, then the other dims in order), stable. */
+ * key (group coord, then the other dims in order), stable. `canonical` != 0
+ * asserts the input is already in that order (e.g. ixb_kernel_map output). */
 int ixb_group_coo_tensor_plan(int rank, const int64_t* shape, const int32_t* const* coords,
-                              int64_t nnz, int group_dim, int64_t g, ixb_stream stream,
-                              ixb_pack** plan, int64_t* num_groups);
+                              int64_t nnz, int group_dim, int64_t g, int canonical,
+                              ixb_stream stream, ixb_pack** plan, int64_t* num_groups);
 /* member_coords: rank-1 device arrays [G, g] (dims in order, group_dim skipped). */
 int ixb_group_coo_tensor_pack(ixb_pack* plan, const void* values, int dtype,
                               int32_t* group_coord, int32_t* const* member_coords, void* out_values,
@@ -166,10 +167,12 @@ int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV,
  * unique). Pairs (out i, in j, offset z) with coord[j] == coord[i] + delta(z),
  * z = (dx+1)*9 + (dy+1)*3 + (dz+1), ordered by (z, i) — the canonical order
  * of group_coo_tensor(map, 2, g) input. */
-int ixb_kernel_map_plan(const int32_t* coords, int64_t n, ixb_stream stream, ixb_pack** plan,
+typedef struct ixb_kmap ixb_kmap;
+int ixb_kernel_map_plan(const int32_t* coords, int64_t n, ixb_stream stream, ixb_kmap** plan,
                         int64_t* num_pairs);
-int ixb_kernel_map_pack(ixb_pack* plan, int32_t* map_out, int32_t* map_in, int32_t* map_off,
+int ixb_kernel_map_pack(ixb_kmap* plan, int32_t* map_out, int32_t* map_in, int32_t* map_off,
                         ixb_stream stream);
+void ixb_kernel_map_free(ixb_kmap* plan);
 
 /* K6 — grouped sparse convolution,
  * `Out[MAPX[p,q],m] += MAPV[p,q] * In[MAPY[p,q],c] * Weight[MAPZ[p],c,m]`
@@ -180,6 +183,16 @@ int ixb_conv_grouped(const int32_t* MAPZ, const int32_t* MAPX, const int32_t* MA
                      const float* MAPV, int64_t G, int64_t g, const void* In, int64_t n_in,
                      int64_t Cin, const void* Weight, int64_t n_off, int64_t Cout, float* Out,
                      int64_t n_out, int accumulate, int flags, ixb_stream stream);
+/* Inspector/executor split of K6 for a map reused across calls (one conv
+ * layer stack over one point cloud): the plan validates the map and builds
+ * its (output, offset) index once; run evaluates In/Weight -> Out. */
+typedef struct ixb_conv_plan ixb_conv_plan;
+int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t* MAPY,
+                         const float* MAPV, int64_t G, int64_t g, int64_t n_in, int64_t n_off,
+                         int64_t n_out, int flags, ixb_stream stream, ixb_conv_plan** plan);
+int ixb_conv_plan_run(ixb_conv_plan* plan, const void* In, int64_t Cin, const void* Weight,
+                      int64_t Cout, float* Out, int accumulate, int flags, ixb_stream stream);
+void ixb_conv_plan_free(ixb_conv_plan* plan);
 
 /* K7 — grouped Clebsch–Gordan tensor product,
  * `Z[b,CGI[p,q],w] += CGV[p,q] * X[b,CGJ[p,q],u] * Y[b,CGK[p,q]] * W[CGL[p],u,w]`
@@ -217,6 +230,9 @@ int ixb_synth_sparse_matrix(ixb_rng* rng, int kind, int64_t rows, int64_t cols, 
                             int out, void* dst);
 int ixb_synth_block_sparse_matrix(ixb_rng* rng, int kind, int64_t rows, int64_t cols, int64_t br,
                                   int64_t bc, double block_density, int out, void* dst);
+/* cfg5 point cloud: voxelised sphere shells (R = 282) in (x,y,z) order,
+ * n_target voxels, coords [n, 3] int32 (NULL to count). */
+int ixb_synth_voxel_shells(int64_t n_target, int32_t* coords, int64_t* n_out);
 /* coords: [rank, nnz] int32 (capacity >= min(nnz, prod(shape))); *nnz_out = realised nnz. */
 int ixb_synth_coo_tensor(ixb_rng* rng, int kind, int rank, const int64_t* shape, int64_t nnz,
                          int out, int32_t* coords, void* values, int64_t* nnz_out);

@@ -60,7 +60,8 @@ _SIGS = {
                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     "ixb_blockgroupcoo_pack": (C.c_int, [C.c_void_p] * 6),
     "ixb_group_coo_tensor_plan": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
-                                            C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                            C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]),
     "ixb_group_coo_tensor_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int] + [C.c_void_p] * 5),
     "ixb_tune_group_size": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p,
                                       C.c_void_p, C.c_void_p]),
@@ -74,6 +75,12 @@ _SIGS = {
     "ixb_kernel_map_plan": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p]),
     "ixb_kernel_map_pack": (C.c_int, [C.c_void_p] * 5),
+    "ixb_kernel_map_free": (None, [C.c_void_p]),
+    "ixb_conv_plan_create": (C.c_int, [C.c_void_p] * 4 + [C.c_int64] * 5 +
+                             [C.c_int, C.c_void_p, C.c_void_p]),
+    "ixb_conv_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                    C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ixb_conv_plan_free": (None, [C.c_void_p]),
     "ixb_conv_grouped": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
                                    C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int,
@@ -92,6 +99,7 @@ _SIGS = {
                                                 C.c_void_p]),
     "ixb_synth_coo_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ixb_synth_voxel_shells": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

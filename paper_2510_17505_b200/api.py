@@ -179,8 +179,9 @@ def dense_to_blockgroupcoo(dense, block_rows, block_cols, g, group_dim=0, stream
                          AM, AK, AV, mask, nb.value)
 
 
-def group_coo_tensor(shape, coords, values, group_dim, g, stream=None):
-    """group_coo_tensor (formats.hpp:141). coords: list of rank int32 [nnz] tensors."""
+def group_coo_tensor(shape, coords, values, group_dim, g, canonical=False, stream=None):
+    """group_coo_tensor (formats.hpp:141). coords: list of rank int32 [nnz] tensors.
+    canonical=True asserts the input is already in (group dim, other dims) order."""
     coords = [_dev(c, torch.int32) for c in coords]
     rank = len(coords)
     nnz = coords[0].numel() if rank else 0
@@ -188,8 +189,8 @@ def group_coo_tensor(shape, coords, values, group_dim, g, stream=None):
     sh = (C.c_int64 * rank)(*shape)
     cp = (C.c_void_p * rank)(*[c.data_ptr() for c in coords])
     plan, G = _Plan(), C.c_int64(0)
-    check(lib().ixb_group_coo_tensor_plan(rank, sh, cp, nnz, group_dim, g, _stream(stream),
-                                          C.byref(plan.h), C.byref(G)))
+    check(lib().ixb_group_coo_tensor_plan(rank, sh, cp, nnz, group_dim, g, int(canonical),
+                                          _stream(stream), C.byref(plan.h), C.byref(G)))
     G = G.value
     dev = coords[0].device
     gc = torch.empty(G, dtype=torch.int32, device=dev)
@@ -222,13 +223,42 @@ def tune_group_size(coord, extent, count_empty_rows=False, stream=None):
 def kernel_map(coords, stream=None):
     """K5: submanifold 3x3x3 kernel map (out, in, offset) ordered by (offset, out)."""
     coords = _dev(coords, torch.int32)
-    plan, n = _Plan(), C.c_int64(0)
-    check(lib().ixb_kernel_map_plan(_ptr(coords), coords.shape[0], _stream(stream),
-                                    C.byref(plan.h), C.byref(n)))
-    n = n.value
-    mo, mi, mz = (torch.empty(n, dtype=torch.int32, device=coords.device) for _ in range(3))
-    check(lib().ixb_kernel_map_pack(plan.h, _ptr(mo), _ptr(mi), _ptr(mz), _stream(stream)))
+    h, n = C.c_void_p(), C.c_int64(0)
+    check(lib().ixb_kernel_map_plan(_ptr(coords), coords.shape[0], _stream(stream), C.byref(h),
+                                    C.byref(n)))
+    try:
+        n = n.value
+        mo, mi, mz = (torch.empty(n, dtype=torch.int32, device=coords.device) for _ in range(3))
+        check(lib().ixb_kernel_map_pack(h, _ptr(mo), _ptr(mi), _ptr(mz), _stream(stream)))
+    finally:
+        lib().ixb_kernel_map_free(h)
     return mo, mi, mz
+
+
+class ConvPlan:
+    """Inspector/executor form of K6: validates a grouped kernel map and
+    indexes it by (output, offset) once; run() evaluates one conv."""
+
+    def __init__(self, MAPZ, MAPX, MAPY, MAPV, n_in, n_off, n_out, flags=0, stream=None):
+        self.keep = [t.contiguous() if t is not None else None for t in (MAPZ, MAPX, MAPY, MAPV)]
+        MAPZ, MAPX, MAPY, MAPV = self.keep
+        G, g = MAPX.shape
+        self._free = lib().ixb_conv_plan_free
+        self.h = C.c_void_p()
+        check(lib().ixb_conv_plan_create(_ptr(MAPZ), _ptr(MAPX), _ptr(MAPY), _ptr(MAPV), G, g,
+                                         n_in, n_off, n_out, flags, _stream(stream),
+                                         C.byref(self.h)))
+
+    def run(self, In, Weight, Out, accumulate=True, flags=0, stream=None):
+        check(lib().ixb_conv_plan_run(self.h, _ptr(In), In.shape[1], _ptr(Weight),
+                                      Weight.shape[2], _ptr(Out), int(accumulate), flags,
+                                      _stream(stream)))
+        return Out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._free(self.h)
+            self.h = None
 
 
 def spmm_groupcoo(AM, AK, AV, B, C_out, accumulate=True, flags=0, stream=None):

@@ -1,0 +1,410 @@
+// K6 — grouped sparse convolution (kernel-map gather-GEMM-scatter):
+//   Out[MAPX[p,q],m] += MAPV[p,q] * In[MAPY[p,q],c] * Weight[MAPZ[p],c,m]
+// (corpus/grouped_sparse_conv.json:2; reference vars p,q,m,c, oracle
+// plan.cpp:579-594; fused kernel: dot over c, kernel.cpp:292-357).
+//
+// Output-stationary formulation. The plan indexes every slot
+// by (output row x, offset z) — a table T[x * n_off + z] -> slot — which for
+// a canonical map (group_coo_tensor order (z, x, y), one `in` per (z, x))
+// is collision free. The run then treats the conv as an implicit GEMM over
+// K = (offset, c):
+//   Out[x0:x0+128, :] = sum_z  A_z[128 x Cin] . Weight[z][Cin x Cout]
+// where row r of A_z is MAPV[s] * In[MAPY[s], :] for s = T[(x0+r), z] (zero
+// row if absent). Each CTA owns 128 output rows, so every output row has
+// one writer (deterministic, no atomics) and its per-offset contributions
+// accumulate in z order — the order of the canonical slot list.
+// tcgen05 path (Cin = Cout = 64): A_z gathered by all 128 threads into a
+// SW128 K-major smem tile, Weight[z] by TMA (MN-major SW128), 4 UMMAs
+// M=128,N=64,K=16 per offset into one TMEM accumulator, double-buffered.
+// Maps with colliding (x, z) or other channel counts take the CSR path: slots
+// stable-sorted by output row, one warp per row, fp32 CUDA-core FMAs in slot
+// order (bit-faithful to the reference's summation order).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cudaTypedefs.h>
+
+#include <memory>
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tmap.h"
+
+namespace ixb {
+namespace {
+
+using namespace sm100;
+
+struct PlanArgs {
+  const int32_t* MAPZ;
+  const int32_t* MAPX;
+  const int32_t* MAPY;
+  const float* MAPV;
+  int64_t G, g, n_in, n_off, n_out;
+  int32_t* T;      // [n_out * n_off] slot or -1
+  int* conflict;
+  int check;
+  ErrorRecord* err;
+};
+
+// Validates every index (gathers In/MAPY op 0, Weight/MAPZ op 1, then the
+// scatter Out/MAPX op 2 — plan.cpp:544-561 order) and fills T. A pad slot
+// (same x,y as its predecessor in the group, value 0) is inert and skipped.
+__global__ void conv_index_kernel(PlanArgs a) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= a.G * a.g) return;
+  const int64_t p = s / a.g, q = s % a.g;
+  const int y = a.MAPY[s], x = a.MAPX[s], z = a.MAPZ[p];
+  bool ok = true;
+  if (y < 0 || y >= a.n_in) {
+    if (a.check) report_index_error(a.err, 0, s, y);
+    ok = false;
+  }
+  if (q == 0 && (z < 0 || z >= a.n_off)) {
+    if (a.check) report_index_error(a.err, 1, p, z);
+  }
+  if (z < 0 || z >= a.n_off) ok = false;
+  if (x < 0 || x >= a.n_out) {
+    if (a.check) report_index_error(a.err, 2, s, x);
+    ok = false;
+  }
+  if (!ok) return;
+  const float v = a.MAPV ? a.MAPV[s] : 1.f;
+  if (q > 0 && v == 0.f && a.MAPX[s - 1] == x && a.MAPY[s - 1] == y) return;  // pad
+  const int prev = atomicCAS(&a.T[static_cast<int64_t>(x) * a.n_off + z], -1,
+                             static_cast<int>(s));
+  if (prev != -1) atomicOr(a.conflict, 1);
+}
+
+// ------------------------------------------------------------ tcgen05 path
+constexpr int kConvThreads = 128;
+constexpr uint32_t kATile = 128 * 128;  // 128 rows x 64 bf16
+constexpr uint32_t kWTile = 64 * 128;   // 64 c-rows x 64 bf16
+
+struct RunArgs {
+  const int32_t* T;
+  const int32_t* MAPY;
+  const float* MAPV;
+  const __nv_bfloat16* In;
+  float* Out;
+  int64_t n_out, n_off;
+  int accumulate;
+};
+
+__global__ void __launch_bounds__(kConvThreads, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmW, RunArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* A = smem;                   // [2][16 KB]
+  uint8_t* W = smem + 2 * kATile;      // [2][8 KB]
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(W + 2 * kWTile);
+  uint64_t* mma_done = w_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&w_full[b], 1);
+      mbar_init(&mma_done[b], 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmW);
+  }
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, 64);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * 128 + tid;
+  const bool row_ok = x < a.n_out;
+  constexpr uint32_t idesc = idesc_bf16_f32(128, 64, /*A K-major*/ false, /*B MN-major*/ true);
+  const uint64_t keep = l2_evict_last();
+  int k = 0;  // offsets actually used (buffer use counter)
+  for (int z = 0; z < a.n_off; ++z) {
+    const int s = row_ok ? __ldg(a.T + x * a.n_off + z) : -1;
+    if (!__syncthreads_or(s >= 0)) continue;  // no row of this tile has offset z
+    const int buf = k & 1;
+    if (k >= 2) mbar_wait(&mma_done[buf], ((k - 2) >> 1) & 1);  // MMA k-2 freed buf
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&w_full[buf], kWTile);
+      tma_load_2d(W + buf * kWTile, &tmW, &w_full[buf], 0, z * 64, keep);
+    }
+    // gather row tid of A_z: MAPV[s] * In[MAPY[s], 0:64] -> bf16, SW128 K-major
+    uint4 chunk[8];
+    if (s >= 0) {
+      const int y = __ldg(a.MAPY + s);
+      const float v = a.MAPV ? __ldg(a.MAPV + s) : 1.f;
+      const uint4* src = reinterpret_cast<const uint4*>(a.In + static_cast<int64_t>(y) * 64);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) chunk[j] = __ldg(src + j);
+      if (v != 1.f) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&chunk[j]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(h[e]);
+            h[e] = __floats2bfloat162_rn(f.x * v, f.y * v);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) chunk[j] = make_uint4(0, 0, 0, 0);
+    }
+    uint8_t* arow = A + buf * kATile + tid * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      *reinterpret_cast<uint4*>(arow + ((j ^ (tid & 7)) << 4)) = chunk[j];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&w_full[buf], (k >> 1) & 1);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(A + buf * kATile), w0 = smem_u32(W + buf * kWTile);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        // A: K-major SW128, 8-row atoms at 1024 B; K step of 16 = +32 B
+        const uint64_t ad = smem_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
+        // W[z]: MN-major SW128 (64 m = one atom), K groups of 8 c-rows at 1024 B
+        const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
+        umma_f16(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+      }
+      umma_commit(&mma_done[buf]);
+    }
+    ++k;
+  }
+  float acc[64];
+  if (k > 0) {
+    mbar_wait(&mma_done[(k - 1) & 1], ((k - 1) >> 1) & 1);
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __uint_as_float(r[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+  }
+  if (row_ok) {
+    float4* o = reinterpret_cast<float4*>(a.Out + x * 64);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float4 v = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+      if (a.accumulate) {
+        const float4 old = o[j];
+        v.x += old.x;
+        v.y += old.y;
+        v.z += old.z;
+        v.w += old.w;
+      }
+      o[j] = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+}
+
+// --------------------------------------------------------------- CSR path
+__global__ void iota_conv(int32_t* v, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = static_cast<int32_t>(i);
+}
+
+__global__ void row_hist(const int32_t* MAPX, int64_t n, int64_t n_out, int32_t* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && MAPX[i] >= 0 && MAPX[i] < n_out) atomicAdd(cnt + MAPX[i], 1);
+}
+
+// One warp per output row, slots in (stable) slot order; lanes over Cout.
+template <typename TI>
+__global__ void conv_csr_kernel(const int32_t* perm, const int32_t* rowptr, const int32_t* MAPZ,
+                                const int32_t* MAPY, const float* MAPV, int64_t g, const TI* In,
+                                int64_t Cin, const TI* Wt, int64_t Cout, float* Out,
+                                int64_t n_out, int accumulate) {
+  const int64_t x = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (x >= n_out) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t m0 = 0; m0 < Cout; m0 += 32) {
+    const int64_t m = m0 + lane;
+    float acc = 0.f;
+    for (int32_t i = rowptr[x]; i < rowptr[x + 1]; ++i) {
+      const int s = perm[i];
+      const int y = MAPY[s];
+      const int z = MAPZ[s / g];
+      const float v = MAPV ? MAPV[s] : 1.f;
+      const TI* in = In + static_cast<int64_t>(y) * Cin;
+      const TI* w = Wt + static_cast<int64_t>(z) * Cin * Cout + m;
+      if (m < Cout) {
+        for (int64_t c = 0; c < Cin; ++c) {
+          acc = fmaf(v * static_cast<float>(in[c]), static_cast<float>(w[c * Cout]), acc);
+        }
+      }
+    }
+    if (m < Cout) {
+      float* o = Out + x * Cout + m;
+      *o = accumulate ? *o + acc : acc;
+    }
+  }
+}
+
+}  // namespace
+
+}  // namespace ixb
+
+struct ixb_conv_plan {
+  int64_t G = 0, g = 1, n_in = 0, n_off = 0, n_out = 0;
+  const int32_t *MAPZ = nullptr, *MAPX = nullptr, *MAPY = nullptr;
+  const float* MAPV = nullptr;
+  bool conflict = false;
+  ixb::Scratch<int32_t> T, perm, rowptr;
+};
+
+using namespace ixb;
+
+extern "C" {
+
+int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t* MAPY,
+                         const float* MAPV, int64_t G, int64_t g, int64_t n_in, int64_t n_off,
+                         int64_t n_out, int flags, ixb_stream stream, ixb_conv_plan** plan) {
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (G < 0 || g < 1 || n_in < 0 || n_off < 0 || n_out < 0) fail(IXB_SHAPE, "conv: bad extents");
+    if (G * g > INT32_MAX || n_out * n_off > INT32_MAX) fail(IXB_SHAPE, "conv: map too large");
+    auto P = std::make_unique<ixb_conv_plan>();
+    P->G = G;
+    P->g = g;
+    P->n_in = n_in;
+    P->n_off = n_off;
+    P->n_out = n_out;
+    P->MAPZ = MAPZ;
+    P->MAPX = MAPX;
+    P->MAPY = MAPY;
+    P->MAPV = MAPV;
+    const int64_t slots = G * g;
+    P->T = Scratch<int32_t>(n_out * n_off + 1, s);
+    Scratch<int> conflict(1, s);
+    IXB_CUDA_CHECK(cudaMemsetAsync(P->T.p, 0xff, (n_out * n_off + 1) * 4, s));
+    IXB_CUDA_CHECK(cudaMemsetAsync(conflict.p, 0, 4, s));
+    const bool check = !(flags & IXB_UNCHECKED);
+    if (slots > 0) {
+      PlanArgs a{MAPZ, MAPX, MAPY, MAPV, G, g, n_in, n_off, n_out, P->T.p, conflict.p, check,
+                 device_error_record()};
+      conv_index_kernel<<<ceil_div(slots, 256), 256, 0, s>>>(a);
+      IXB_LAUNCH_CHECK("conv_index_kernel");
+    }
+    if (check) {
+      OperandInfo ops[3] = {{"MAPY", "In", 0, n_in, MAPY, slots},
+                            {"MAPZ", "Weight", 0, n_off, MAPZ, G},
+                            {"MAPX", "Out", 0, n_out, MAPX, slots}};
+      check_error_record(s, ops, 3);
+    }
+    int h = 0;
+    IXB_CUDA_CHECK(cudaMemcpyAsync(&h, conflict.p, 4, cudaMemcpyDeviceToHost, s));
+    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    P->conflict = h != 0;
+    *plan = P.release();
+  });
+}
+
+void ixb_conv_plan_free(ixb_conv_plan* plan) { delete plan; }
+
+int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void* Weight,
+                      int64_t Cout, float* Out, int accumulate, int flags, ixb_stream stream) {
+  return ixb_guard([&] {
+    (void)flags;
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (!P) fail(IXB_FAILURE, "null conv plan");
+    if (Cin < 1 || Cout < 1) fail(IXB_SHAPE, "conv: channel counts must be >= 1");
+    if (P->n_out == 0) return;
+    const bool tc = !P->conflict && Cin == 64 && Cout == 64 &&
+                    reinterpret_cast<uintptr_t>(In) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(Weight) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(Out) % 16 == 0;
+    if (tc) {
+      const CUtensorMap tmW =
+          make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+      RunArgs a{P->T.p, P->MAPY, P->MAPV, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
+                P->n_off, accumulate};
+      const uint32_t smem = 2 * kATile + 2 * kWTile + 1024 + 1024;
+      static std::once_flag once;
+      std::call_once(once, [&] {
+        cuda_check(cudaFuncSetAttribute(conv_tc_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                   "cudaFuncSetAttribute(conv_tc_kernel)");
+      });
+      conv_tc_kernel<<<ceil_div(P->n_out, 128), kConvThreads, smem, s>>>(tmW, a);
+      IXB_LAUNCH_CHECK("conv_tc_kernel");
+      return;
+    }
+    // CSR path: slots stable-sorted by output row.
+    const int64_t slots = P->G * P->g;
+    if (!P->perm.p) {
+      Scratch<int32_t> idx(slots + 1, s), keys_out(slots + 1, s);
+      P->perm = Scratch<int32_t>(slots + 1, s);
+      if (slots > 0) {
+        iota_conv<<<ceil_div(slots, 256), 256, 0, s>>>(idx.p, slots);
+        IXB_LAUNCH_CHECK("iota_conv");
+        size_t tb = 0;
+        IXB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, P->MAPX, keys_out.p, idx.p,
+                                                       P->perm.p, static_cast<int>(slots), 0, 32,
+                                                       s));
+        Scratch<char> tmp(tb, s);
+        IXB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, P->MAPX, keys_out.p, idx.p,
+                                                       P->perm.p, static_cast<int>(slots), 0, 32,
+                                                       s));
+        note_launch(4);
+      }
+      Scratch<int32_t> cnt(P->n_out + 1, s);
+      P->rowptr = Scratch<int32_t>(P->n_out + 1, s);
+      IXB_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, (P->n_out + 1) * 4, s));
+      if (slots > 0) {
+        row_hist<<<ceil_div(slots, 256), 256, 0, s>>>(P->MAPX, slots, P->n_out, cnt.p);
+        IXB_LAUNCH_CHECK("row_hist");
+      }
+      size_t tb = 0;
+      IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, P->rowptr.p,
+                                                   static_cast<int>(P->n_out + 1), s));
+      Scratch<char> tmp(tb, s);
+      IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, P->rowptr.p,
+                                                   static_cast<int>(P->n_out + 1), s));
+      note_launch();
+    }
+    const int64_t grid = ceil_div(P->n_out * 32, 256);
+    conv_csr_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        P->perm.p, P->rowptr.p, P->MAPZ, P->MAPY, P->MAPV, P->g,
+        static_cast<const __nv_bfloat16*>(In), Cin, static_cast<const __nv_bfloat16*>(Weight),
+        Cout, Out, P->n_out, accumulate);
+    IXB_LAUNCH_CHECK("conv_csr_kernel");
+  });
+}
+
+int ixb_conv_grouped(const int32_t* MAPZ, const int32_t* MAPX, const int32_t* MAPY,
+                     const float* MAPV, int64_t G, int64_t g, const void* In, int64_t n_in,
+                     int64_t Cin, const void* Weight, int64_t n_off, int64_t Cout, float* Out,
+                     int64_t n_out, int accumulate, int flags, ixb_stream stream) {
+  ixb_conv_plan* plan = nullptr;
+  int rc = ixb_conv_plan_create(MAPZ, MAPX, MAPY, MAPV, G, g, n_in, n_off, n_out, flags, stream,
+                                &plan);
+  if (rc != IXB_OK) return rc;
+  rc = ixb_conv_plan_run(plan, In, Cin, Weight, Cout, Out, accumulate, flags, stream);
+  ixb_conv_plan_free(plan);
+  return rc;
+}
+
+}  // extern "C"

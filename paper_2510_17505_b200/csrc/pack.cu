@@ -839,8 +839,8 @@ int ixb_blockgroupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint
 }
 
 int ixb_group_coo_tensor_plan(int rank, const int64_t* shape, const int32_t* const* coords,
-                              int64_t nnz, int group_dim, int64_t g, ixb_stream stream,
-                              ixb_pack** plan, int64_t* num_groups) {
+                              int64_t nnz, int group_dim, int64_t g, int canonical,
+                              ixb_stream stream, ixb_pack** plan, int64_t* num_groups) {
   return ixb_guard([&] {
     if (g < 1) fail(IXB_SHAPE, "group size must be >= 1");
     if (group_dim < 0 || group_dim >= rank) fail(IXB_SHAPE, "group_dim out of range");
@@ -852,7 +852,7 @@ int ixb_group_coo_tensor_plan(int rank, const int64_t* shape, const int32_t* con
     P->rank = rank;
     P->group_dim = group_dim;
     P->coords.assign(coords, coords + rank);
-    plan_sorted_runs(P.get(), false, g, shape ? shape[group_dim] : 0, 0, nullptr);
+    plan_sorted_runs(P.get(), canonical != 0, g, shape ? shape[group_dim] : 0, 0, nullptr);
     *num_groups = P->G;
     *plan = P.release();
   });

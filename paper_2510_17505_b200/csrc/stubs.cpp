@@ -3,20 +3,6 @@
 
 extern "C" {
 
-int ixb_kernel_map_plan(const int32_t*, int64_t, ixb_stream, ixb_pack**, int64_t*) {
-  return ixb_guard([] { ixb::fail(IXB_FAILURE, "ixb_kernel_map: not built yet"); });
-}
-
-int ixb_kernel_map_pack(ixb_pack*, int32_t*, int32_t*, int32_t*, ixb_stream) {
-  return ixb_guard([] { ixb::fail(IXB_FAILURE, "ixb_kernel_map: not built yet"); });
-}
-
-int ixb_conv_grouped(const int32_t*, const int32_t*, const int32_t*, const float*, int64_t,
-                     int64_t, const void*, int64_t, int64_t, const void*, int64_t, int64_t,
-                     float*, int64_t, int, int, ixb_stream) {
-  return ixb_guard([] { ixb::fail(IXB_FAILURE, "ixb_conv_grouped: not built yet"); });
-}
-
 int ixb_tp_grouped(const int32_t*, const int32_t*, const int32_t*, const int32_t*, const float*,
                    int64_t, int64_t, const void*, const void*, const void*, int, int64_t, int64_t,
                    int64_t, int64_t, int64_t, int64_t, int64_t, float*, int, int, ixb_stream) {

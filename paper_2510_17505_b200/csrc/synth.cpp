@@ -104,6 +104,37 @@ int ixb_synth_block_sparse_matrix(ixb_rng* r, int kind, int64_t rows, int64_t co
   });
 }
 
+// Voxelised sphere shells (no reference counterpart; the cfg5 point cloud of
+// BASELINE.json): voxels with R-1/2 <= |v - c| < R+1/2 for R = 282, shells
+// centred 1000 apart along x until n_target voxels, emitted in (x, y, z)
+// order (unique, sorted) and truncated to n_target. Deterministic, no RNG.
+int ixb_synth_voxel_shells(int64_t n_target, int32_t* coords, int64_t* n_out) {
+  return ixb_guard([&] {
+    const int R = 282;
+    const double lo = (R - 0.5) * (R - 0.5), hi = (R + 0.5) * (R + 0.5);
+    int64_t n = 0;
+    for (int shell = 0; n < n_target; ++shell) {
+      const int cx = shell * 1000;
+      for (int x = -R - 1; x <= R + 1 && n < n_target; ++x) {
+        for (int y = -R - 1; y <= R + 1 && n < n_target; ++y) {
+          for (int z = -R - 1; z <= R + 1 && n < n_target; ++z) {
+            const double d = static_cast<double>(x) * x + static_cast<double>(y) * y +
+                             static_cast<double>(z) * z;
+            if (d < lo || d >= hi) continue;
+            if (coords) {
+              coords[3 * n] = cx + x;
+              coords[3 * n + 1] = y;
+              coords[3 * n + 2] = z;
+            }
+            ++n;
+          }
+        }
+      }
+    }
+    *n_out = n;
+  });
+}
+
 // synth_coo_tensor (synth.cpp:80-106): coords [rank, nnz_realised] int32.
 int ixb_synth_coo_tensor(ixb_rng* r, int kind, int rank, const int64_t* shape, int64_t nnz,
                          int out, int32_t* coords, void* vals, int64_t* nnz_out) {

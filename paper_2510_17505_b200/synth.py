@@ -67,3 +67,12 @@ def synth_coo_tensor(rng, shape, nnz, kind=REAL, dtype=torch.float32):
                                      C.c_void_p(coords.data_ptr()), C.c_void_p(vals.data_ptr()),
                                      C.byref(got)))
     return coords, vals
+
+
+def synth_voxel_shells(n_target):
+    """cfg5 point cloud: voxelised sphere shells, sorted (x, y, z), int32 [n, 3]."""
+    n = C.c_int64(0)
+    check(lib().ixb_synth_voxel_shells(n_target, None, C.byref(n)))
+    coords = torch.empty((n.value, 3), dtype=torch.int32)
+    check(lib().ixb_synth_voxel_shells(n_target, C.c_void_p(coords.data_ptr()), C.byref(n)))
+    return coords
