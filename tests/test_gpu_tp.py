@@ -1,0 +1,135 @@
+"""GPU parity of K7 (grouped Clebsch–Gordan tensor product) against the C
+oracle: the reference corpus form (per-edge W, CUDA-core path, bit-exact in
+integer mode) and the shared-weight e3nn form on tcgen05 (bf16 operands,
+fp32 accumulation; tolerance 1e-2), including the real-basis l_max = 3 CG
+table grouped by path on the device."""
+import numpy as np
+import pytest
+
+import instances
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+EXPR_B = "Z[b,CGI[p,q],w] += CGV[p,q] * X[b,CGJ[p,q],u] * Y[b,CGK[p,q]] * W[b,CGL[p],u,w]"
+EXPR_S = "Z[b,CGI[p,q],w] += CGV[p,q] * X[b,CGJ[p,q],u] * Y[b,CGK[p,q]] * W[CGL[p],u,w]"
+TOL_BF16 = 1e-2
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_17505_b200 as P
+    P.lib()
+    return P
+
+
+def bf16_round(x):
+    return torch.from_numpy(np.asarray(x, np.float64)).to(torch.bfloat16).double().numpy()
+
+
+def cuda(x, dtype):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dtype).cuda()
+
+
+def run_tp(P, t, out, accumulate=True):
+    Z = cuda(out, torch.float32)
+    P.tp_grouped(cuda(t["CGL"], torch.int32), cuda(t["CGI"], torch.int32),
+                 cuda(t["CGJ"], torch.int32), cuda(t["CGK"], torch.int32),
+                 cuda(t["CGV"], torch.float32), cuda(t["X"], torch.bfloat16),
+                 cuda(t["Y"], torch.bfloat16), cuda(t["W"], torch.bfloat16), Z,
+                 accumulate=accumulate)
+    return Z.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("kind", [1, 0])
+def test_tp_acceptance_instances(P, ixo, kind):
+    """acceptance.cpp make_grouped_tp (per-edge W): CUDA-core path."""
+    for i in range(30 if kind else 15):
+        t, expr, on, out = instances.make(ixo, "grouped_tp", kind, 1000 + i)
+        if kind == 0:
+            t = {k: (bf16_round(v) if k in ("X", "Y", "W") else v) for k, v in t.items()}
+        want = ixo.einsum(expr, t, on, out)
+        got = run_tp(P, t, out)
+        if kind:
+            np.testing.assert_array_equal(got.astype(np.int64), want)
+        else:
+            assert ixo.max_rel_error(want, got) <= TOL_BF16
+
+
+def cg_grouped(P, ixo, g):
+    """Real-basis CG (l_max 3) grouped by path on the device; checked vs oracle."""
+    t = ixo.cg_table(3)
+    coords = np.stack([t["i"], t["j"], t["k"], t["l"]])
+    shape = [16, 16, 16, len(t["paths"])]
+    want = ixo.group_coo_tensor(shape, coords, t["v"], 3, g)
+    got = P.group_coo_tensor(shape, [cuda(c, torch.int32) for c in coords],
+                             cuda(t["v"], torch.float32), 3, g)
+    np.testing.assert_array_equal(got.group_coord.cpu().numpy(), want["group_coord"])
+    for m in range(3):
+        np.testing.assert_array_equal(got.member_coords[m].cpu().numpy(), want["member_coords"][m])
+    return {"CGL": want["group_coord"], "CGI": want["member_coords"][0],
+            "CGJ": want["member_coords"][1], "CGK": want["member_coords"][2],
+            "CGV": want["values"].astype(np.float32).astype(np.float64)}, len(t["paths"])
+
+
+@pytest.mark.parametrize("g", [4, 16])
+def test_tp_tcgen05_real_cg_shared_w(P, ixo, g):
+    cg, nl = cg_grouped(P, ixo, g)
+    rng = ixo.Rng(3)
+    B = 70  # crosses a 64-edge tile
+    t = dict(cg)
+    t["X"] = bf16_round(ixo.synth_dense(rng, (B, 16, 64)))
+    t["Y"] = bf16_round(ixo.synth_dense(rng, (B, 16)))
+    t["W"] = bf16_round(ixo.synth_dense(rng, (nl, 64, 64)))
+    out = np.zeros((B, 16, 64))
+    want = ixo.einsum(EXPR_S, t, "Z", out)
+    got = run_tp(P, t, out)
+    assert ixo.max_rel_error(want, got) <= TOL_BF16
+    primed = ixo.synth_dense(rng, (B, 16, 64))
+    want = ixo.einsum(EXPR_S.replace("+=", "="), t, "Z", primed)
+    got = run_tp(P, t, primed, accumulate=False)
+    assert ixo.max_rel_error(want, got) <= TOL_BF16
+
+
+def test_tp_tcgen05_random_cg_and_missing_components(P, ixo):
+    rng = ixo.Rng(11)
+    ni, nj, nk, nl = 12, 9, 7, 5
+    coords, vals = ixo.synth_coo_tensor(rng, (ni, nj, nk, nl), 60)
+    gt = ixo.group_coo_tensor((ni, nj, nk, nl), coords, vals, 3, 3)
+    t = {"CGL": gt["group_coord"], "CGI": gt["member_coords"][0], "CGJ": gt["member_coords"][1],
+         "CGK": gt["member_coords"][2], "CGV": gt["values"]}
+    B = 130
+    t["X"] = bf16_round(ixo.synth_dense(rng, (B, nj, 64)))
+    t["Y"] = bf16_round(ixo.synth_dense(rng, (B, nk)))
+    t["W"] = bf16_round(ixo.synth_dense(rng, (nl, 64, 64)))
+    primed = ixo.synth_dense(rng, (B, ni, 64))
+    want = ixo.einsum(EXPR_S, t, "Z", primed)
+    got = run_tp(P, t, primed)
+    assert ixo.max_rel_error(want, got) <= TOL_BF16
+
+
+def test_tp_shared_w_other_widths_simt(P, ixo):
+    rng = ixo.Rng(5)
+    coords, vals = ixo.synth_coo_tensor(rng, (5, 6, 4, 3), 25, 1)
+    gt = ixo.group_coo_tensor((5, 6, 4, 3), coords, vals, 3, 2)
+    t = {"CGL": gt["group_coord"], "CGI": gt["member_coords"][0], "CGJ": gt["member_coords"][1],
+         "CGK": gt["member_coords"][2], "CGV": gt["values"]}
+    t["X"] = ixo.synth_dense(rng, (9, 6, 8), 1)
+    t["Y"] = ixo.synth_dense(rng, (9, 4), 1)
+    t["W"] = ixo.synth_dense(rng, (3, 8, 5), 1)
+    out = np.zeros((9, 5, 5), np.int64)
+    want = ixo.einsum(EXPR_S, t, "Z", out)
+    got = run_tp(P, t, out)
+    np.testing.assert_array_equal(got.astype(np.int64), want)
+
+
+def test_tp_index_errors(P, ixo):
+    t, expr, on, out = instances.make(ixo, "grouped_tp", 1, 1234)
+    t = dict(t)
+    t["CGK"] = t["CGK"].copy()
+    t["CGK"].flat[1] = 99
+    with pytest.raises(P.IndexRangeError) as e:
+        run_tp(P, t, out)
+    assert "index tensor CGK value 99 at position [1] out of range for dim 1 of Y" in str(e.value)
