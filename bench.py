@@ -254,8 +254,172 @@ class BlockGroupCooWorkload:
             f"first {brows} of {self.M // b} block rows ({nblk} blocks), g={g}"
 
 
+class TensorProductWorkload:
+    """configs[3]: e3nn-style CG tensor product, l_max 3, 64 channels, shared
+    W[path,u,w] (K7, tcgen05). Metric: ms per call (lower is better)."""
+    expr = "Z[b,CGI[p,q],w] = CGV[p,q] * X[b,CGJ[p,q],u] * Y[b,CGK[p,q]] * W[CGL[p],u,w]"
+    kernel = "tp_tc_kernel"
+    metric = "TP ms/call"
+
+    def __init__(self, name, batch, seed=1):
+        self.name, self.batch, self.seed = name, batch, seed
+
+    def config(self):
+        return {"workload": self.name, "expr": self.expr,
+                "desc": f"CG tensor product l_max=3 (23 paths, 353 real-basis CG nnz), 64 ch, "
+                        f"batch {self.batch} edges, shared W, bf16 in / fp32 Z",
+                "batch": self.batch, "seed": self.seed}
+
+    def setup(self, torch, P, S, dev, seed):
+        rng = S.Rng(seed)
+        B = self.batch
+        self.X = S.synth_dense(rng, (B, 16, 64), S.REAL, torch.bfloat16).to(dev)
+        self.Y = S.synth_dense(rng, (B, 16), S.REAL, torch.bfloat16).to(dev)
+        cg = S.cg_table(3)
+        nl = cg["npaths"]
+        self.W = S.synth_dense(rng, (nl, 64, 64), S.REAL, torch.bfloat16).to(dev)
+        l = cg["l"].to(dev)
+        g, _ = P.tune_group_size(l, nl)
+        gt = P.group_coo_tensor([16, 16, 16, nl], [cg["i"].to(dev), cg["j"].to(dev),
+                                                   cg["k"].to(dev), l], cg["v"].to(dev), 3, g)
+        self.CGL, (self.CGI, self.CGJ, self.CGK), self.CGV = \
+            gt.group_coord, gt.member_coords, gt.values
+        self.Z = torch.empty((B, 16, 64), dtype=torch.float32, device=dev)
+        self.flops = 2.0 * 99 * 64 * 64 * B  # factorised form (sum over paths of 2*l3+1 = 99)
+        self.alg_bytes = B * (16 * 64 * 2 + 16 * 2 + 16 * 64 * 4) + nl * 64 * 64 * 2
+        self.info = {"paths": nl, "cg_nnz": int(cg["v"].numel()), "G": gt.num_groups(), "g": g,
+                     "formulation": "output-side factorised (99 GEMMs of 64x64 per edge)"}
+        self.h_in = [self.X.cpu().pin_memory(), self.Y.cpu().pin_memory()]
+        self.h_out = torch.empty_like(self.Z, device="cpu").pin_memory()
+        self.d_in = [torch.empty_like(x, device=dev) for x in self.h_in]
+
+    def step(self, P, stream=None):
+        P.tp_grouped(self.CGL, self.CGI, self.CGJ, self.CGK, self.CGV, self.X, self.Y, self.W,
+                     self.Z, accumulate=False, flags=1 | 2)
+
+    def e2e_step(self, P):
+        for d, h in zip(self.d_in, self.h_in):
+            d.copy_(h, non_blocking=True)
+        P.tp_grouped(self.CGL, self.CGI, self.CGJ, self.CGK, self.CGV, self.d_in[0],
+                     self.d_in[1], self.W, self.Z, accumulate=False, flags=1 | 2)
+        self.h_out.copy_(self.Z, non_blocking=True)
+
+    def e2e_bytes(self):
+        return sum(x.numel() * x.element_size() for x in self.h_in), \
+            self.h_out.numel() * self.h_out.element_size()
+
+    def roofline_bound(self):
+        return "hbm"
+
+    def units_total(self):
+        return self.batch
+
+    def cpu_sample(self, ref, budget_rows=None):
+        import numpy as np
+        from paper_2510_17505_b200 import synth as S
+        cg = S.cg_table(3)
+        nl = cg["npaths"]
+        coords = np.stack([cg[k].numpy().astype(np.int64) for k in ("i", "j", "k", "l")])
+        gt = ref.group_coo_tensor([16, 16, 16, nl], coords, cg["v"].double().numpy(), 3, 4)
+        bs = budget_rows or 6
+        rng = ref.Rng(self.seed)
+        t = {"CGL": gt["group_coord"], "CGI": gt["member_coords"][0],
+             "CGJ": gt["member_coords"][1], "CGK": gt["member_coords"][2], "CGV": gt["values"],
+             "X": ref.synth_dense(rng, (bs, 16, 64), 0), "Y": ref.synth_dense(rng, (bs, 16), 0),
+             "W": ref.synth_dense(rng, (nl, 64, 64), 0)}
+        out = np.zeros((bs, 16, 64))
+        return t, self.expr, "Z", out, bs, (f"{bs} of {self.batch} edges (same CG/W shapes, "
+                                            f"own seed), extrapolated linearly to the batch")
+
+
+class SparseConvWorkload:
+    """configs[4]: submanifold 3x3x3 sparse conv, 1M voxels (sphere shells),
+    C_in = C_out = 64, bf16 in / fp32 out (K5 kernel map + K6 on tcgen05).
+    Metric: ms per call; the (output, offset) index of the map is built once
+    (ConvPlan) outside the timed call and reported as plan_ms."""
+    expr = "Out[MAPX[p,q],m] = MAPV[p,q] * In[MAPY[p,q],c] * Weight[MAPZ[p],c,m]"
+    kernel = "conv_tc_kernel"
+    metric = "sparse-conv ms/call"
+
+    def __init__(self, name, voxels, seed=1):
+        self.name, self.voxels, self.seed = name, voxels, seed
+
+    def config(self):
+        return {"workload": self.name, "expr": self.expr,
+                "desc": f"submanifold sparse conv 3x3x3, {self.voxels} voxels (sphere shells), "
+                        f"C_in=C_out=64, bf16 in / fp32 out", "voxels": self.voxels,
+                "seed": self.seed}
+
+    def setup(self, torch, P, S, dev, seed):
+        import time as _t
+        coords = S.synth_voxel_shells(self.voxels).to(dev)
+        n = coords.shape[0]
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        mo, mi, mz = P.kernel_map(coords)
+        g, _ = P.tune_group_size(mz, 27)
+        ones = torch.ones(mo.numel(), dtype=torch.float32, device=dev)
+        gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], ones, 2, g, canonical=True)
+        torch.cuda.synchronize()
+        t1 = _t.perf_counter()
+        self.MAPZ, (self.MAPX, self.MAPY), self.MAPV = gt.group_coord, gt.member_coords, gt.values
+        self.plan = P.ConvPlan(self.MAPZ, self.MAPX, self.MAPY, self.MAPV, n, 27, n)
+        torch.cuda.synchronize()
+        t2 = _t.perf_counter()
+        rng = S.Rng(seed)
+        self.In = S.synth_dense(rng, (n, 64), S.REAL, torch.bfloat16).to(dev)
+        self.Wt = S.synth_dense(rng, (27, 64, 64), S.REAL, torch.bfloat16).to(dev)
+        self.Out = torch.empty((n, 64), dtype=torch.float32, device=dev)
+        pairs = mo.numel()
+        self.pairs_total = pairs
+        self.flops = 2.0 * pairs * 64 * 64
+        G = gt.num_groups()
+        # gather model (SURVEY.md §8d): In row gathered + Out row updated per pair, map once
+        self.alg_bytes = pairs * 64 * (2 + 4) + G * g * (4 + 2 * 4) + G * 4
+        self.info = {"voxels": n, "pairs": pairs, "kappa": pairs / n, "G": G, "g": g,
+                     "kernel_map_and_group_ms": (t1 - t0) * 1e3, "plan_ms": (t2 - t1) * 1e3}
+        self.h_in = [self.In.cpu().pin_memory()]
+        self.h_out = torch.empty_like(self.Out, device="cpu").pin_memory()
+        self.d_in = [torch.empty_like(self.In)]
+
+    def step(self, P, stream=None):
+        self.plan.run(self.In, self.Wt, self.Out, accumulate=False)
+
+    def e2e_step(self, P):
+        self.d_in[0].copy_(self.h_in[0], non_blocking=True)
+        self.plan.run(self.d_in[0], self.Wt, self.Out, accumulate=False)
+        self.h_out.copy_(self.Out, non_blocking=True)
+
+    def e2e_bytes(self):
+        return self.h_in[0].numel() * 2, self.h_out.numel() * 4
+
+    def roofline_bound(self):
+        return "hbm"
+
+    def units_total(self):
+        return getattr(self, "pairs_total", 9.12 * self.voxels)
+
+    def cpu_sample(self, ref, budget_rows=None):
+        import numpy as np
+        from oracle import ixo
+        from paper_2510_17505_b200 import synth as S
+        nv = budget_rows or 3000
+        pts = S.synth_voxel_shells(nv).numpy()
+        mo, mi, mz = ixo.kernel_map(pts)
+        gt = ref.group_coo_tensor([nv, nv, 27], np.stack([mo, mi, mz]), np.ones(len(mo)), 2, 64)
+        rng = ref.Rng(self.seed)
+        t = {"MAPZ": gt["group_coord"], "MAPX": gt["member_coords"][0],
+             "MAPY": gt["member_coords"][1], "MAPV": gt["values"],
+             "In": ref.synth_dense(rng, (nv, 64), 0), "Weight": ref.synth_dense(rng, (27, 64, 64), 0)}
+        out = np.zeros((nv, 64))
+        return t, self.expr, "Out", out, len(mo), (
+            f"first {nv} shell voxels ({len(mo)} map pairs), extrapolated linearly in pairs")
+
+
 WORKLOADS = {
     "cfg1": lambda: GroupCooWorkload("cfg1", 4096, 4096, 0.01, 128),
+    "cfg4": lambda: TensorProductWorkload("cfg4", 1_000_000),
+    "cfg5": lambda: SparseConvWorkload("cfg5", 1_000_000),
     "cfg2": lambda: BlockGroupCooWorkload("cfg2", 8192, 8192, 16, 0.10, 512),
 }
 for _d in ("0.30", "0.20", "0.10", "0.05", "0.02"):
@@ -289,10 +453,15 @@ def cpu_reference_time(wl, steps=1, warmup=0, budget_rows=None):
         _, sc = ref.run(t, expr, on, out, mode, thr)
         times.append(sc["wall_ms"])
     ms = statistics.mean(times)
-    return {"value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "cores": thr, "kind": kind,
-            "sample": f"{sample}; reference execute_mode('{mode}', threads={thr}) "
-                      f"(plan {modes['plan'][0]:.1f} ms vs fused-lazy x{cores} "
-                      f"{modes['fused-lazy'][0]:.1f} ms)",
+    desc = (f"{sample}; reference execute_mode('{mode}', threads={thr}) "
+            f"(plan {modes['plan'][0]:.1f} ms vs fused-lazy x{cores} "
+            f"{modes['fused-lazy'][0]:.1f} ms)")
+    if getattr(wl, "metric", METRIC) == METRIC:
+        value, unit = flops / (ms * 1e-3) / 1e9, "GFLOP/s"
+    else:  # time-like metric: the sample's time scaled to the whole call
+        value, unit = ms * wl.units_total() / flops, "ms"
+        desc += "; EXTRAPOLATED"
+    return {"value": value, "unit": unit, "cores": thr, "kind": kind, "sample": desc,
             "ms_per_step": ms, "mode": mode}
 
 
@@ -301,14 +470,15 @@ def run_reference_arm(args, wl):
     if rank != 0:
         return
     r = cpu_reference_time(wl, steps=args.steps, warmup=args.warmup)
-    line = {"metric": METRIC, "value": r["value"], "unit": "GFLOP/s", "impl": "reference",
+    metric = getattr(wl, "metric", METRIC)
+    line = {"metric": metric, "value": r["value"], "unit": r["unit"], "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference synth, seed 1)",
-            "config": wl.config(),
-            "cpu_baseline": {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"],
+            "ms_per_step": r["ms_per_step"], "higher_is_better": metric == METRIC,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference synth, seed 1)", "config": wl.config(),
+            "cpu_baseline": {"value": r["value"], "unit": r["unit"], "cores": r["cores"],
                              "kind": r["kind"], "sample": r["sample"]},
-            "e2e": {"value": r["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -416,17 +586,23 @@ def run_b200(args, wl):
                 "hbm_compulsory_frac": wl.alg_bytes / kern_s / 1e9 / hbm,
                 "l2_gather_GBps": wl.gather_bytes / kern_s / 1e9}
 
-    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws,
+    metric = getattr(wl, "metric", METRIC)
+    timelike = metric != METRIC
+    line = {"metric": metric, "value": ms if timelike else value,
+            "unit": "ms" if timelike else "GFLOP/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16" if wl.roofline_bound() == "tensor" else "f32",
+            "higher_is_better": not timelike, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if wl.roofline_bound() == "tensor" or timelike else "f32",
             "data": "synthetic (reference synth streams, seed 1 + rank)",
             "config": dict(wl.config(), l2="flushed between steps (256 MiB memset outside the "
                                          "timed events)", parallelism=f"weak x{ws}", **wl.info),
             "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
-            "e2e": {"value": wl.flops * ws / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "e2e": {"value": e_ms if timelike else wl.flops * ws / (e_ms * 1e-3) / 1e9,
+                    "unit": "ms" if timelike else "GFLOP/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e_ms}}
+    if timelike:
+        line["config"]["useful_GFLOPs"] = value
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference_time(wl)

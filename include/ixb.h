@@ -230,6 +230,12 @@ int ixb_synth_sparse_matrix(ixb_rng* rng, int kind, int64_t rows, int64_t cols, 
                             int out, void* dst);
 int ixb_synth_block_sparse_matrix(ixb_rng* rng, int kind, int64_t rows, int64_t cols, int64_t br,
                                   int64_t bc, double block_density, int out, void* dst);
+/* Real-basis Clebsch–Gordan table for l_max (cfg4's CG operand; host
+ * arrays, NULL to count): entries (i, j, k, path, value) in (path, i, j, k)
+ * generation order; paths (l1,l2,l3) with the triangle rule and even
+ * l1+l2+l3 (23 paths / 353 entries for l_max = 3). */
+int ixb_cg_table(int l_max, int32_t* ci, int32_t* cj, int32_t* ck, int32_t* cl, float* cv,
+                 int64_t* count, int32_t* npaths);
 /* cfg5 point cloud: voxelised sphere shells (R = 282) in (x,y,z) order,
  * n_target voxels, coords [n, 3] int32 (NULL to count). */
 int ixb_synth_voxel_shells(int64_t n_target, int32_t* coords, int64_t* n_out);

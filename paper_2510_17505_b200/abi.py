@@ -100,6 +100,7 @@ _SIGS = {
     "ixb_synth_coo_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ixb_synth_voxel_shells": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p]),
+    "ixb_cg_table": (C.c_int, [C.c_int] + [C.c_void_p] * 7),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -76,3 +76,15 @@ def synth_voxel_shells(n_target):
     coords = torch.empty((n.value, 3), dtype=torch.int32)
     check(lib().ixb_synth_voxel_shells(n_target, C.c_void_p(coords.data_ptr()), C.byref(n)))
     return coords
+
+
+def cg_table(l_max=3):
+    """Real-basis CG table (host): dict of int32 i, j, k, l, float32 v, npaths."""
+    n, npaths = C.c_int64(0), C.c_int32(0)
+    check(lib().ixb_cg_table(l_max, None, None, None, None, None, C.byref(n), C.byref(npaths)))
+    out = {k: torch.empty(n.value, dtype=torch.int32) for k in ("i", "j", "k", "l")}
+    out["v"] = torch.empty(n.value, dtype=torch.float32)
+    p = [C.c_void_p(out[k].data_ptr()) for k in ("i", "j", "k", "l", "v")]
+    check(lib().ixb_cg_table(l_max, *p, C.byref(n), C.byref(npaths)))
+    out["npaths"] = npaths.value
+    return out
