@@ -7,14 +7,15 @@
 // paths; BASELINE configs[3]). Output-side factorisation:
 //   U_{l,i}[b,u] = sum_{(j,k,v) in path l, output i} v * Y[b,k] * X[b,j,u]
 //   Z[b,i,:]     = sum_l U_{l,i}[b,:] . W[l]        (99 GEMMs for l_max = 3)
-// A CTA is persistent over tiles of 64 edges. 512 threads = (edge, 8-wide
-// u slice); each thread holds its edge's X[b, :, slice] and Y[b, :] in
-// registers, so the CG contraction reads no shared memory. U tiles (bf16,
-// K-major SW128) are double-buffered in smem and fed to UMMA M=64,N=64,K=16
-// against W[l] (all paths resident in smem, loaded once per CTA by TMA,
-// MN-major SW128). Z accumulates in TMEM: 16 components x 64 columns as two
-// M=64 half-subpartition sets (lane offset 16), i.e. the full 512 columns.
-// The CG contraction of pair n+1 overlaps the UMMAs of pair n.
+// A CTA is persistent over tiles of 64 edges: X[tile] (64 x 16 x 64 bf16)
+// lands in smem by TMA, Y[tile] as fp32. 512 threads = (edge, 8-wide u
+// slice) contract the CG entries of one (path, component) pair per step
+// (one LDS.128 of X + 8 FMAs per entry). U is split hi + lo bf16, written as
+// K-major SW128 tiles (double-buffered) and fed to UMMA M=64,N=64,K=16
+// against W[l] (3-slot TMA ring prefetching the next path's W). Z
+// accumulates in TMEM: 16 components x 64 columns as two M=64
+// half-subpartition sets (lane offset 16), i.e. the full 512 columns. The
+// contraction of pair n+1 overlaps the UMMAs of pair n.
 // Any other shape, and the per-edge W[b,l,u,w] form, run a CUDA-core kernel
 // that follows the reference's summation order exactly.
 #include <cudaTypedefs.h>
@@ -40,6 +41,7 @@ constexpr int kMaxEntries = 480;
 constexpr int kMaxPaths = 23;
 constexpr uint32_t kUTile = kEdges * 128;  // 64 rows x 64 bf16
 constexpr uint32_t kWTileTp = 64 * 128;    // 64 u-rows x 64 bf16
+constexpr uint32_t kXTile = kEdges * 16 * 128;  // 64 edges x 16 irrep rows x 64 bf16
 
 struct TpMeta {
   int npairs, nentries, nl, ni;
@@ -60,21 +62,25 @@ struct TpArgs {
 };
 
 __global__ void __launch_bounds__(kTpThreads, 1)
-    tp_tc_kernel(const __grid_constant__ CUtensorMap tmW, TpArgs a) {
+    tp_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                 TpArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* Wsm = smem;                              // [nl][8 KB]
-  uint8_t* Usm = smem + kMaxPaths * kWTileTp;       // [2][8 KB]
-  uint64_t* w_full = reinterpret_cast<uint64_t*>(Usm + 4 * kUTile);
-  uint64_t* mma_done = w_full + 1;                  // [2]
+  uint8_t* Us = smem;                        // [2 bufs][hi, lo][8 KB]  (SW128 K-major)
+  uint8_t* Ws = Us + 4 * kUTile;             // [3][8 KB]               (SW128 MN-major)
+  uint8_t* Xs = Ws + 3 * kWTileTp;           // [64 edges * nj rows][128 B]
+  float* Ys = reinterpret_cast<float*>(Xs + kXTile);  // [64][16]
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(Ys + kEdges * 16);
+  uint64_t* w_full = x_full + 1;  // [3]
+  uint64_t* mma_done = w_full + 3;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
   __shared__ int4 s_pair[kMaxPairs];  // {l | is_first_of_component << 16, i, entry0, count}
   __shared__ int4 s_entry[kMaxEntries];
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int b_loc = tid >> 3, slice = tid & 7;  // edge in tile, u slice [8*slice, +8)
-  const int npairs = a.meta->npairs, nl = a.meta->nl;
+  const int npairs = a.meta->npairs;
   for (int i = tid; i < npairs; i += kTpThreads) {
     int4 pr = a.meta->pair[i];
     pr.x |= (a.meta->first[i] == i) ? (1 << 16) : 0;
@@ -82,13 +88,13 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   }
   for (int i = tid; i < a.meta->nentries; i += kTpThreads) s_entry[i] = a.meta->entry[i];
   if (tid == 0) {
-    mbar_init(w_full, 1);
+    mbar_init(x_full, 1);
+    for (int b = 0; b < 3; ++b) mbar_init(&w_full[b], 1);
     mbar_init(&mma_done[0], 1);
     mbar_init(&mma_done[1], 1);
     fence_barrier_init();
-    // every path's W[l] once per CTA (persistent over edge tiles)
-    mbar_arrive_expect_tx(w_full, nl * kWTileTp);
-    for (int l = 0; l < nl; ++l) tma_load_2d(Wsm + l * kWTileTp, &tmW, w_full, 0, l * 64, 0);
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
   }
   if (warp == 0) {
     tmem_alloc(tmem_slot, 512);
@@ -99,37 +105,66 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t idesc = idesc_bf16_f32(64, 64, /*A K-major*/ false, /*B MN-major*/ true);
-  if (tid == 0) mbar_wait(w_full, 0);
+  // whole 256-row boxes land (out-of-range rows zero-filled), so expect them all
+  const uint32_t x_bytes = static_cast<uint32_t>(((kEdges * a.nj + 255) / 256) * 256 * 128);
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
 
+  // thread-0 state for the W ring (3 buffers, one per upcoming path)
+  uint32_t w_loads[3] = {0, 0, 0};
   int n_global = 0;  // pairs issued by this CTA (U buffer / barrier phase counter)
+  int tiles_done = 0;
   const int64_t ntiles = (a.batch + kEdges - 1) / kEdges;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t b = tile * kEdges + b_loc;
-    const bool bok = b < a.batch;
-    // this thread's X[b, j, slice] (16 x 8 bf16) and Y[b, :] in registers
-    uint4 xr[16];
-    float yr[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      xr[j] = (bok && j < a.nj)
-                  ? __ldg(reinterpret_cast<const uint4*>(a.X + (b * a.nj + j) * 64 + 8 * slice))
-                  : make_uint4(0, 0, 0, 0);
-      yr[j] = (bok && j < a.nk) ? __bfloat162float(a.Y[b * a.nk + j]) : 0.f;
+  auto issue_w = [&](int path, int slot) {
+    mbar_arrive_expect_tx(&w_full[slot], kWTileTp);
+    tma_load_2d(Ws + slot * kWTileTp, &tmW, &w_full[slot], 0, path * 64, keep);
+    ++w_loads[slot];
+  };
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tiles_done) {
+    // ---- stage the tile: X by TMA (rows b*nj + j), Y as fp32, first paths' W
+    if (tid == 0) {
+      mbar_arrive_expect_tx(x_full, x_bytes);
+      const int rows = kEdges * a.nj;
+      for (int r0 = 0; r0 < rows; r0 += 256) {
+        tma_load_2d(Xs + r0 * 128, &tmX, x_full, 0,
+                    static_cast<int32_t>(tile * kEdges * a.nj + r0), stream);
+      }
+      if (npairs > 0) issue_w(s_pair[0].x & 0xFFFF, 0);
     }
+    for (int e = tid; e < kEdges * 16; e += kTpThreads) {
+      const int bb = e >> 4, k = e & 15;
+      const int64_t b = tile * kEdges + bb;
+      Ys[e] = (b < a.batch && k < a.nk) ? __bfloat162float(a.Y[b * a.nk + k]) : 0.f;
+    }
+    mbar_wait(x_full, tiles_done & 1);
+    __syncthreads();
+    const uint8_t* xrow = Xs + b_loc * a.nj * 128 + slice * 16;
+    const float* yrow = Ys + b_loc * 16;
+    int cur_path = -1, path_idx = -1;
     for (int n = 0; n < npairs; ++n, ++n_global) {
       const int4 pr = s_pair[n];
+      const int path = pr.x & 0xFFFF;
+      const bool new_path = path != cur_path;
+      if (new_path) {
+        cur_path = path;
+        ++path_idx;
+        if (tid == 0) {
+          // prefetch the next path's W into the slot last used two paths ago
+          for (int m = n + 1; m < npairs; ++m) {
+            const int pth = s_pair[m].x & 0xFFFF;
+            if (pth != path) {
+              issue_w(pth, (path_idx + 1) % 3);
+              break;
+            }
+          }
+        }
+      }
       float acc[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = 0.f;
       for (int e = pr.z; e < pr.z + pr.w; ++e) {
         const int4 en = s_entry[e];
-        float yk = 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) yk = (k == en.y) ? yr[k] : yk;
-        const float coef = __int_as_float(en.z) * yk;
-        uint4 xv = xr[0];
-#pragma unroll
-        for (int j = 1; j < 16; ++j) xv = (j == en.x) ? xr[j] : xv;
+        const float coef = __int_as_float(en.z) * yrow[en.y];
+        const uint4 xv = *reinterpret_cast<const uint4*>(xrow + en.x * 128);
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xv);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -138,10 +173,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           acc[2 * q + 1] = fmaf(coef, f.y, acc[2 * q + 1]);
         }
       }
-      const int buf = n_global & 1;
-      if (n_global >= 2) mbar_wait(&mma_done[buf], ((n_global - 2) >> 1) & 1);
-      // U = hi + lo, both bf16: the pair of UMMAs below sees U to ~2^-16
-      // relative, so the only bf16 roundings are the operands X, Y, W.
+      // U = hi + lo, both bf16: the UMMA pair sees U to ~2^-16 relative, so the
+      // only bf16 roundings are the operands X, Y, W themselves.
       uint4 hi, lo;
       __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&hi);
       __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&lo);
@@ -151,18 +184,22 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         const float2 back = __bfloat1622float2(ph[q]);
         pl[q] = __floats2bfloat162_rn(acc[2 * q] - back.x, acc[2 * q + 1] - back.y);
       }
+      const int buf = n_global & 1;
+      if (n_global >= 2) mbar_wait(&mma_done[buf], ((n_global - 2) >> 1) & 1);
       const uint32_t off = b_loc * 128 + ((slice ^ (b_loc & 7)) << 4);
-      *reinterpret_cast<uint4*>(Usm + (2 * buf) * kUTile + off) = hi;
-      *reinterpret_cast<uint4*>(Usm + (2 * buf + 1) * kUTile + off) = lo;
+      *reinterpret_cast<uint4*>(Us + (2 * buf) * kUTile + off) = hi;
+      *reinterpret_cast<uint4*>(Us + (2 * buf + 1) * kUTile + off) = lo;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
+        const int wslot = path_idx % 3;
+        if (new_path) mbar_wait(&w_full[wslot], (w_loads[wslot] - 1) & 1);
         tc_fence_after();
         const int i = pr.y;
         // component i: columns 64*(i%8), lane set 16*(i/8) (M=64 half subpartitions)
         const uint32_t d = tmem + (static_cast<uint32_t>((i >> 3) * 16) << 16) + (i & 7) * 64;
-        const uint32_t u0 = smem_u32(Usm + (2 * buf) * kUTile);
-        const uint32_t w0 = smem_u32(Wsm + (pr.x & 0xFFFF) * kWTileTp);
+        const uint32_t u0 = smem_u32(Us + (2 * buf) * kUTile);
+        const uint32_t w0 = smem_u32(Ws + wslot * kWTileTp);
         const bool first = (pr.x >> 16) & 1;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -174,7 +211,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         umma_commit(&mma_done[buf]);
       }
     }
-    // epilogue: all UMMAs of this tile done -> TMEM -> Z
+    // ---- epilogue: all UMMAs of this tile done -> TMEM -> Z
     if (npairs > 0) {
       const int last = n_global - 1;
       mbar_wait(&mma_done[last & 1], (last >> 1) & 1);
@@ -217,7 +254,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       }
     }
     tc_fence_before();
-    __syncthreads();  // TMEM drained before the next tile's first UMMAs
+    __syncthreads();  // TMEM drained and Xs/Ys free before the next tile
   }
   __syncthreads();
   if (warp == 0) {
@@ -344,10 +381,12 @@ extern "C" int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int3
       IXB_CUDA_CHECK(cudaMemcpyAsync(dmeta.p, &meta, sizeof meta, cudaMemcpyHostToDevice, s));
       const CUtensorMap tmW = make_tmap_2d(W, 64, static_cast<uint64_t>(nl) * 64, 128, 64, 64,
                                            CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap tmX = make_tmap_2d(X, 64, static_cast<uint64_t>(batch) * nj, 128, 64, 256,
+                                           CU_TENSOR_MAP_SWIZZLE_NONE);
       TpArgs args{static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(Y), Z,
                   batch, static_cast<int>(nj), static_cast<int>(nk), static_cast<int>(ni),
                   accumulate, dmeta.p};
-      const uint32_t smem = kMaxPaths * kWTileTp + 4 * kUTile + 256 + 1024;
+      const uint32_t smem = 4 * kUTile + 3 * kWTileTp + kXTile + kEdges * 16 * 4 + 256 + 1024;
       static std::once_flag once;
       std::call_once(once, [&] {
         cuda_check(cudaFuncSetAttribute(tp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -356,7 +395,7 @@ extern "C" int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int3
       });
       int64_t grid = ceil_div(batch, kEdges);
       if (grid > sm_count()) grid = sm_count();
-      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, smem, s>>>(tmW, args);
+      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, smem, s>>>(tmW, tmX, args);
       IXB_LAUNCH_CHECK("tp_tc_kernel");
       IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // host meta buffer lifetime
       return;
