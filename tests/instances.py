@@ -94,6 +94,70 @@ def make(mod, name, kind, seed):
     return t, EXPR[name], OUT[name], out
 
 
+def materialize(mod, spec):
+    """Restates materialize (driver.cpp:165-233) for a run spec dict over a
+    backend module: one Rng(seed); dense specs, then index specs, then sparse
+    specs in spec order; formats bound like bind_matrix_format /
+    bind_tensor_format (driver.cpp:98-161). Returns (tensors, out)."""
+    kind = 1 if spec.get("elem") == "int64" else 0
+    rng = mod.Rng(spec.get("seed", 0))
+    t = {}
+    for d in spec.get("dense", []):
+        t[d["name"]] = mod.synth_dense(rng, tuple(d["shape"]), kind)
+    for ix in spec.get("index", []):
+        t[ix["name"]] = np.array([rng.uniform_int(0, max(ix["bound"] - 1, 0))
+                                  for _ in range(int(np.prod(ix["shape"])))],
+                                 np.int64).reshape(ix["shape"])
+    for s in spec.get("sparse", []):
+        name, shape, fmt = s["name"], s["shape"], s.get("format", "coo")
+        g, gd = s.get("g", 1), s.get("groupDim", 0)
+        if len(shape) == 2:
+            suf = s.get("suffixes", ["M", "K"])
+            if "genBlock" in s:
+                a = mod.synth_block_sparse_matrix(rng, shape[0], shape[1], s["genBlock"][0],
+                                                  s["genBlock"][1], s.get("blockDensity", 0.1),
+                                                  kind)
+            else:
+                a = mod.synth_sparse_matrix(rng, shape[0], shape[1], s.get("density", 0.1), kind)
+            r, c, v = mod.dense_to_coo(a)
+            if fmt == "coo":
+                t[name + "V"], t[name + suf[0]], t[name + suf[1]] = v, r, c
+                continue
+            if fmt == "blockgroupcoo":
+                b = mod.dense_to_blockgroupcoo(a, s["formatBlock"][0], s["formatBlock"][1], g, gd)
+            else:
+                if fmt == "auto":
+                    occ = np.bincount(r if gd == 0 else c,
+                                      minlength=shape[0] if gd == 0 else shape[1])
+                    from oracle import ixo
+                    g = ixo.select(occ.astype(np.int64))
+                b = mod.coo_to_groupcoo(shape[0], shape[1], r, c, v, gd, g)
+            gs, ms = (suf[0], suf[1]) if gd == 0 else (suf[1], suf[0])
+            t[name + "V"], t[name + gs], t[name + ms] = b["AV"], b["AM"], b["AK"]
+        else:
+            suf = s.get("suffixes", [chr(ord("I") + i) for i in range(len(shape))])
+            nnz = s.get("nnz", -1)
+            if nnz < 0:
+                nnz = max(1, int(s.get("density", 0.1) * np.prod(shape)))
+            coords, vals = mod.synth_coo_tensor(rng, tuple(shape), nnz, kind)
+            if fmt == "coo":
+                for dd in range(len(shape)):
+                    t[name + suf[dd]] = coords[dd].copy()
+                t[name + "V"] = vals
+            else:
+                gt = mod.group_coo_tensor(tuple(shape), coords, vals, gd, g)
+                t[name + suf[gd]] = gt["group_coord"]
+                m = 0
+                for dd in range(len(shape)):
+                    if dd != gd:
+                        t[name + suf[dd]] = gt["member_coords"][m]
+                        m += 1
+                t[name + "V"] = gt["values"]
+    o = spec["output"]
+    out = np.zeros(o["shape"], np.int64 if kind else np.float64)
+    return t, out
+
+
 def occ3112_matrix():
     """The paper's Fig. 4 matrix, occupancy [3,1,1,2] (tests/helpers.hpp:16-21)."""
     return np.array([[1, 2, 0, 3], [0, 4, 0, 0], [0, 0, 5, 0], [6, 0, 0, 7]], dtype=np.float64)
