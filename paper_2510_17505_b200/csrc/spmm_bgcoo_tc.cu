@@ -48,6 +48,7 @@ struct TcArgs {
   int accumulate;
   int check;
   int epi_sleep_ns;  // epilogue warps back off instead of spinning on acc_full
+  int debug;         // perf experiments: 1 = skip UMMA issue, 2 = gather B tile 0 only
   ErrorRecord* err;
 };
 
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             uint8_t* st = tiles + stage * L::kStageBytes;
             mbar_arrive_expect_tx(&full[stage], L::kBBytes + kAvBytes);
             // one 3-D box {64 n, 16 rows, 2*NSUB atoms} lands as [atom][row][64]
-            tma_load_3d(st, &tmB, &full[stage], 0, kk * 16, n0 / 64, keep);
+            tma_load_3d(st, &tmB, &full[stage], 0, (a.debug & 2) ? 0 : kk * 16, n0 / 64, keep);
             tma_load_2d(st + L::kBBytes, &tmAV, &full[stage], 0,
                         static_cast<int32_t>((i0 + t) * 16), stream);
           }
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int sub = 0; sub < NSUB; ++sub) {
             // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
             const uint64_t adesc = smem_desc(st + sub * kSubBytes, 2048, 1024, kLayoutSW128);
-            umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc, i > 0 ? 1u : 0u);
+            if (!(a.debug & 1))
+              umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc, i > 0 ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
           if (i + 1 == nslots) umma_commit(&acc_full[buf]);
@@ -504,6 +506,8 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     static const int variant = getenv("IXB_BG_VARIANT") ? atoi(getenv("IXB_BG_VARIANT")) : 0;
     static const int sleep_ns = getenv("IXB_BG_SLEEP") ? atoi(getenv("IXB_BG_SLEEP")) : 256;
     a.epi_sleep_ns = sleep_ns;
+    static const int debug = getenv("IXB_BG_DEBUG") ? atoi(getenv("IXB_BG_DEBUG")) : 0;
+    a.debug = debug;
     if (nsub == 1) {
       launch_tc<1, 12, 4>(tmB, tmAV, a, s);
     } else if (variant == 1) {
