@@ -51,46 +51,96 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    """Clock / throttle-reason sampler running DURING the timed region
+    (B200_PROFILING.md clocks line). The kernels here run for tens of µs, so
+    `nvidia-smi -lms 100` (one sample per 100 ms, ~200 ms start-up) sees none
+    of them; this polls NVML (the library nvidia-smi reads) from a thread as
+    fast as it answers, from start() to stop(). Falls back to nvidia-smi when
+    pynvml is absent."""
 
-    def __init__(self, gpu_index):
+    def __init__(self, torch_device):
+        import threading
+        self.samples = []  # (sm_mhz, reasons mask)
+        self.max_mhz = None
+        self.h = None
+        self.nv = None
         self.p = None
+        self._stop = threading.Event()
+        self._thread = None
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(gpu_index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(torch_device)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(int(torch_device.index or 0))
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
         except Exception:
-            self.p = None
+            self.nv = None
+
+    def _poll(self):
+        nv, h = self.nv, self.h
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(mhz), int(mask)))
+            except Exception:
+                return
+            time.sleep(0.0005)
+
+    def start(self):
+        import threading
+        if self.nv is not None:
+            self._thread = threading.Thread(target=self._poll, daemon=True)
+            self._thread.start()
+        else:
+            try:
+                self.p = subprocess.Popen(
+                    ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.p = None
+        return self
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        self.p.terminate()
-        try:
-            out, _ = self.p.communicate(timeout=5)
-        except Exception:
-            self.p.kill()
-            out = ""
-        sm, mx, reasons = [], None, set()
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 3:
-                continue
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
+        elif self.p is not None:
+            self.p.terminate()
             try:
-                mhz, mmax, mask = float(f[0]), float(f[1]), int(f[2], 16)
-            except ValueError:
-                continue
-            mx = mmax
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out = ""
+            for line in out.strip().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                try:
+                    self.samples.append((float(f[0]), int(f[2], 16)))
+                    self.max_mhz = float(f[1])
+                except (ValueError, IndexError):
+                    continue
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"],
+                    "samples_under_load": 0}
+        sm, reasons = [], set()
+        for mhz, mask in self.samples:
             if mask & 0x1:  # idle sample: not under load
                 continue
             sm.append(mhz)
             for bit, name in REASONS.items():
                 if mask & bit and bit != 0x1:
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples_under_load": len(sm)}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples_under_load": len(sm),
+                "samples": len(self.samples),
+                "sampler": "nvml-thread" if self.nv is not None else "nvidia-smi"}
 
 
 def dist_env():
@@ -211,6 +261,7 @@ class BlockGroupCooWorkload:
         self.alg_bytes = (slots * b * b * 2 + slots * 4 + self.G * 4 + self.K * self.N * 2 +
                           self.rows_nz * b * self.N * 4)
         self.gather_bytes = slots * b * self.N * 2
+        self.mma_count = slots * (self.N // 128)  # one M=128 (n) x N=16 (bm) UMMA per slot per n tile
         self.info = {"blocks": self.nblk, "G": self.G, "g": self.g,
                      "nonempty_block_rows": self.rows_nz,
                      "gathered_B_tile_bytes": self.gather_bytes}
@@ -517,10 +568,11 @@ def run_b200(args, wl):
     torch.cuda.synchronize()
     P.lib().ixb_check_errors(None)
 
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    clocks.start()
     launches0 = P.lib().ixb_launch_count()
     evs = []
     for _ in range(args.steps):
@@ -585,6 +637,13 @@ def run_b200(args, wl):
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops (burst)",
                 "hbm_compulsory_frac": wl.alg_bytes / kern_s / 1e9 / hbm,
                 "l2_gather_GBps": wl.gather_bytes / kern_s / 1e9}
+        if hasattr(wl, "mma_count"):
+            # measured tcgen05 cost of an M=128,K=16 MMA with N <= 64 (tools/umma_rate.cu,
+            # profiles/k4_diag_r1.md): the per-instruction floor, not flops, bounds 16-wide blocks
+            floor_s = wl.mma_count * 48.0 / (torch.cuda.get_device_properties(dev).multi_processor_count
+                                              * 1.965e9)
+            roof["mma_issue_floor_us"] = floor_s * 1e6
+            roof["frac_of_mma_issue_floor"] = floor_s / kern_s
 
     metric = getattr(wl, "metric", METRIC)
     timelike = metric != METRIC

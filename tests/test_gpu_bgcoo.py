@@ -140,6 +140,45 @@ def test_tcgen05_long_rows_many_stages(P, ixo):
     np.testing.assert_array_equal(got.astype(np.int64).reshape(4800, 128), ref)
 
 
+def test_tcgen05_mixed_long_and_short_rows(P, ixo):
+    """Rows over the column-merge capacity (> 256 slots) keep slot order and
+    share a row-block (and its TMEM accumulators) with column-merged rows."""
+    rng = ixo.Rng(21)
+    a = ixo.synth_block_sparse_matrix(rng, 80, 6720, 16, 16, 0.7, 1)
+    b = ixo.synth_dense(rng, (420, 16, 128), 1)
+    a[32:48] = 0  # empty block-row 2
+    for r in (1, 3):  # short rows (<= 256 slots) next to long rows 0 and 4
+        a[r * 16:(r + 1) * 16, 16 * 40:] = 0
+    f = ixo.dense_to_blockgroupcoo(a, 16, 16, 4)
+    t = {"AM": f["AM"], "AK": f["AK"], "AV": f["AV"], "B": b}
+    ref = (a.reshape(80, 6720).astype(np.int64) @ b.reshape(6720, 128).astype(np.int64))
+    got = run(P, t, np.zeros((5, 16, 128)), flags=2)
+    np.testing.assert_array_equal(got.astype(np.int64).reshape(80, 128), ref)
+    rows = np.bincount(t["AM"], minlength=5) * t["AK"].shape[1]
+    assert rows.max() > 256  # the slot-order path ran
+
+
+def test_tcgen05_more_items_than_sms(P, ixo):
+    """Many row-blocks x n tiles: persistent CTAs cycle both TMEM sets."""
+    t, a, b = make16(ixo, 31, 3000, 12, 256, 0.2, 2)
+    ref = (a.reshape(48000, 192).astype(np.int64) @ b.reshape(192, 256).astype(np.int64))
+    got = run(P, t, np.zeros((3000, 16, 256)), accumulate=False, flags=2)
+    np.testing.assert_array_equal(got.astype(np.int64).reshape(48000, 256), ref)
+
+
+def test_tcgen05_deterministic_and_row_block_invariant(P, ixo):
+    """Real values: repeated runs are bit-identical, and evaluating a row
+    slab alone (different row-block height R) gives the same bits."""
+    t, a, b = make16(ixo, 41, 64, 40, 512, 0.3, 4, kind=0)
+    full1 = run(P, t, np.zeros((64, 16, 512)), flags=2)
+    full2 = run(P, t, np.zeros((64, 16, 512)), flags=2)
+    np.testing.assert_array_equal(full1, full2)
+    sel = t["AM"] >= 32
+    sub = {"AM": t["AM"][sel] - 32, "AK": t["AK"][sel], "AV": t["AV"][sel], "B": t["B"]}
+    part = run(P, sub, np.zeros((32, 16, 512)), flags=2)
+    np.testing.assert_array_equal(part, full1[32:])
+
+
 def test_tcgen05_unsorted_groups(P, ixo):
     g_np = np.random.default_rng(4)
     G, g, MB, KB, N = 60, 2, 7, 9, 128
