@@ -205,6 +205,19 @@ int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ, c
                    const void* W, int w_per_batch, int64_t batch, int64_t ni, int64_t nj,
                    int64_t nk, int64_t nl, int64_t U, int64_t Wd, float* Z, int accumulate,
                    int flags, ixb_stream stream);
+/* Inspector/executor split of K7 for a CG table reused across calls (every
+ * layer of an equivariant network applies the same table): the plan
+ * validates the table (same errors as ixb_tp_grouped) and reshapes it once;
+ * run evaluates X/Y/W -> Z for any batch. The CG arrays must outlive the
+ * plan. ixb_tp_grouped == create + run + free. */
+typedef struct ixb_tp_plan ixb_tp_plan;
+int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ,
+                       const int32_t* CGK, const float* CGV, int64_t G, int64_t g, int w_per_batch,
+                       int64_t ni, int64_t nj, int64_t nk, int64_t nl, int64_t U, int64_t Wd,
+                       int flags, ixb_stream stream, ixb_tp_plan** plan);
+int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, const void* W, int64_t batch,
+                    float* Z, int accumulate, int flags, ixb_stream stream);
+void ixb_tp_plan_free(ixb_tp_plan* plan);
 
 /* ======================================================================
  * Multi-GPU sharding (host-side planning). Cuts G sorted

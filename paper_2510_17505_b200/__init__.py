@@ -17,7 +17,7 @@ from .abi import (BindError, IxbError, IndexRangeError, ParseError, ShapeError, 
 from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupcoo,
                   dense_to_coo, dense_to_groupcoo, coo_to_groupcoo, emit_operands,
                   group_coo_tensor, kernel_map, tune_group_size, spmm_groupcoo,
-                  spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups, ConvPlan,
+                  spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups, ConvPlan, TpPlan,
                   count_accesses_model)
 from .executor import execute_mode, match_workload, WORKLOADS
 
@@ -26,6 +26,6 @@ __all__ = [
     "GroupCoo", "BlockGroupCoo", "GroupCooTensor", "dense_to_coo", "coo_to_groupcoo",
     "dense_to_groupcoo", "dense_to_blockgroupcoo", "group_coo_tensor", "emit_operands",
     "kernel_map", "tune_group_size", "spmm_groupcoo", "spmm_blockgroupcoo", "conv_grouped",
-    "tp_grouped", "shard_groups", "ConvPlan", "count_accesses_model", "execute_mode", "match_workload",
+    "tp_grouped", "shard_groups", "ConvPlan", "TpPlan", "count_accesses_model", "execute_mode", "match_workload",
     "WORKLOADS",
 ]

@@ -87,6 +87,11 @@ _SIGS = {
                                    C.c_void_p]),
     "ixb_tp_grouped": (C.c_int, [C.c_void_p] * 5 + [C.c_int64, C.c_int64] + [C.c_void_p] * 3 +
                        [C.c_int] + [C.c_int64] * 7 + [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ixb_tp_plan_create": (C.c_int, [C.c_void_p] * 5 + [C.c_int64, C.c_int64, C.c_int] +
+                           [C.c_int64] * 6 + [C.c_int, C.c_void_p, C.c_void_p]),
+    "ixb_tp_plan_run": (C.c_int, [C.c_void_p] * 4 + [C.c_int64, C.c_void_p, C.c_int, C.c_int,
+                                                     C.c_void_p]),
+    "ixb_tp_plan_free": (None, [C.c_void_p]),
     "ixb_shard_groups": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
     "ixb_rng_new": (C.c_void_p, [C.c_uint64]),
     "ixb_rng_free": (None, [C.c_void_p]),

@@ -305,6 +305,35 @@ def tp_grouped(CGL, CGI, CGJ, CGK, CGV, X, Y, W, Z, accumulate=True, flags=0, st
     return Z
 
 
+class TpPlan:
+    """Inspector/executor form of K7: validates a grouped CG table and
+    reshapes it (tensor-core job table / CUDA-core slot lists) once;
+    run() evaluates one tensor product for any batch. The CG tensors are
+    kept alive by the plan."""
+
+    def __init__(self, CGL, CGI, CGJ, CGK, CGV, ni, nj, nk, nl, U=64, Wd=64, w_per_batch=False,
+                 flags=0, stream=None):
+        self.keep = [t.contiguous() for t in (CGL, CGI, CGJ, CGK, CGV)]
+        CGL, CGI, CGJ, CGK, CGV = self.keep
+        G, g = CGI.shape
+        self.ni, self.Wd = ni, Wd
+        self._free = lib().ixb_tp_plan_free
+        self.h = C.c_void_p()
+        check(lib().ixb_tp_plan_create(_ptr(CGL), _ptr(CGI), _ptr(CGJ), _ptr(CGK), _ptr(CGV), G,
+                                       g, int(w_per_batch), ni, nj, nk, nl, U, Wd, flags,
+                                       _stream(stream), C.byref(self.h)))
+
+    def run(self, X, Y, W, Z, accumulate=True, flags=0, stream=None):
+        check(lib().ixb_tp_plan_run(self.h, _ptr(X), _ptr(Y), _ptr(W), X.shape[0], _ptr(Z),
+                                    int(accumulate), flags, _stream(stream)))
+        return Z
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._free(self.h)
+            self.h = None
+
+
 def shard_groups(group_coord_host, parts):
     """Row-boundary group shards for `parts` ranks."""
     import numpy as np

@@ -101,6 +101,12 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
   return p;
 }
 
+// Orders this thread's generic-proxy shared-memory writes before later
+// async-proxy (TMA / tcgen05) accesses.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // --------------------------------------------------------------- tcgen05
 // TMEM allocation: one full warp executes alloc; result written to smem.
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {

@@ -3,25 +3,17 @@
 // (corpus/grouped_tensor_product.json:2; reference vars b,p,q,w,u; oracle
 // plan.cpp:579-594; fused: dot over u, batch [b,p], kernel.cpp:292-357).
 //
-// tcgen05 path (shared W[l,u,w], U = W = 64, <= 16 irrep components, <= 23
-// paths; BASELINE configs[3]). Output-side factorisation:
-//   U_{l,i}[b,u] = sum_{(j,k,v) in path l, output i} v * Y[b,k] * X[b,j,u]
-//   Z[b,i,:]     = sum_l U_{l,i}[b,:] . W[l]        (99 GEMMs for l_max = 3)
-// A CTA is persistent over tiles of 64 edges: X[tile] (64 x 16 x 64 bf16)
-// lands in smem by TMA, Y[tile] as fp32. 512 threads = (edge, 8-wide u
-// slice) contract the CG entries of one (path, component) pair per step
-// (one LDS.128 of X + 8 FMAs per entry). U is split hi + lo bf16, written as
-// K-major SW128 tiles (double-buffered) and fed to UMMA M=64,N=64,K=16
-// against W[l] (3-slot TMA ring prefetching the next path's W). Z
-// accumulates in TMEM: 16 components x 64 columns as two M=64
-// half-subpartition sets (lane offset 16), i.e. the full 512 columns. The
-// contraction of pair n+1 overlaps the UMMAs of pair n.
+// tcgen05 path (shared W[l,u,w], U = W = 64, <= 16 irrep components;
+// BASELINE configs[3]): see tp_tc_kernel. U is split hi + lo bf16 (a single
+// bf16 U loses ~3e-2 to cancellation across paths on the l_max = 3 table).
 // Any other shape, and the per-edge W[b,l,u,w] form, run a CUDA-core kernel
 // that follows the reference's summation order exactly.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -34,69 +26,100 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kEdges = 64;       // edges per tile (UMMA M)
-constexpr int kTpThreads = 512;  // 64 edges x 8 u-slices
-constexpr int kMaxPairs = 128;
+constexpr int kEdges = 64;                         // edges per tile
+constexpr int kMathWarps = 16;                     // 64 edges x 8 u-slices
+constexpr int kMathThreads = kMathWarps * 32;
+constexpr int kTpThreads = kMathThreads + 64;      // + UMMA warp + TMA warp
+constexpr int kMaxJobs = 192;
 constexpr int kMaxEntries = 480;
-constexpr int kMaxPaths = 23;
-constexpr uint32_t kUTile = kEdges * 128;  // 64 rows x 64 bf16
-constexpr uint32_t kWTileTp = 64 * 128;    // 64 u-rows x 64 bf16
-constexpr uint32_t kXTile = kEdges * 16 * 128;  // 64 edges x 16 irrep rows x 64 bf16
+constexpr int kMaxPathSeq = 64;
+constexpr int kNU = 2;                              // U ring (job operands, hi + lo)
+constexpr int kNW = 3;                              // W ring (one path each)
+constexpr uint32_t kUHalf = 128 * 128;              // 128 rows (2 comps x 64 edges) x 64 bf16
+constexpr uint32_t kUSlot = 2 * kUHalf;             // hi, lo
+constexpr uint32_t kWTileTp = 64 * 128;             // 64 u-rows x 64 bf16
+constexpr uint32_t kXTile = kEdges * 16 * 128;      // 64 edges x 16 irrep rows x 64 bf16
 
+// CG table reshaped for the tensor-core path, passed by value (constant bank:
+// every lane reads the same entry, which the constant cache broadcasts).
 struct TpMeta {
-  int npairs, nentries, nl, ni;
-  int4 pair[kMaxPairs];    // {l, i, first entry, entry count}
-  int first[kMaxPairs];    // first pair of component i in the list
-  int present[16];         // component i receives at least one pair
-  int4 entry[kMaxEntries]; // {j, k, float bits of v, 0}
+  int njobs, npaths, ni, present;  // present: bit i = component i receives a job
+  // job: {l | first-touch-of-cp << 8 | last-job-of-path << 9 | first-job-of-path << 10,
+  //       cp | path-seq << 8, e1 | n1 << 16, e2 | n2 << 16}
+  int4 job[kMaxJobs];
+  int2 entry[kMaxEntries];  // {j | k << 8, float bits of v}
+  int path_l[kMaxPathSeq];  // W index of each path in job order
 };
 
+// acc(2 lanes) += coef * x(2 lanes): one FFMA2.
+__device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
+  unsigned long long d, xv, cv, av;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xv) : "f"(x.x), "f"(x.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cv) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(coef));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(av), "l"(xv), "l"(cv));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+
 struct TpArgs {
-  const __nv_bfloat16* X;  // [B, nj, 64]
   const __nv_bfloat16* Y;  // [B, nk]
   float* Z;                // [B, ni, 64]
   int64_t batch;
   int nj, nk, ni;
   int accumulate;
-  const TpMeta* meta;
 };
 
+// Output-side factorisation, batched two output components at
+// a time so every UMMA has M = 128:
+//   U_{l,i}[b,u] = sum_{(j,k,v) in (l,i)} v * Y[b,k] * X[b,j,u]   (CUDA cores)
+//   Z[b,i,:]    += U_{l,i}[b,:] . W[l]                           (tcgen05)
+// A job = (path l, component pair cp): A rows 0..63 = U_{l,2cp}, rows 64..127
+// = U_{l,2cp+1} (zero when the path has no such component), B = W[l], D =
+// TMEM columns [64 cp, 64 cp + 64) (lanes 0..63 component 2cp, 64..127
+// component 2cp+1): 8 pairs x 64 = all 512 columns.
+// Warps 0..15 compute U for job n into a kNU-deep ring (mbarrier handoff,
+// no block-wide barrier per job), warp 16 issues 4 UMMAs (K = 64) per job and
+// commits the slot back, warp 17 streams X tiles and W[l] (kNW ring) by TMA.
+// X of tile t+1 loads while the math warps drain tile t from TMEM.
 __global__ void __launch_bounds__(kTpThreads, 1)
     tp_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                 TpArgs a) {
+                 const __grid_constant__ TpMeta meta, TpArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* Us = smem;                        // [2 bufs][hi, lo][8 KB]  (SW128 K-major)
-  uint8_t* Ws = Us + 4 * kUTile;             // [3][8 KB]               (SW128 MN-major)
-  uint8_t* Xs = Ws + 3 * kWTileTp;           // [64 edges * nj rows][128 B]
-  float* Ys = reinterpret_cast<float*>(Xs + kXTile);  // [64][16]
+  uint8_t* Xs = smem;                   // [64 edges * nj rows][128 B]
+  uint8_t* Us = Xs + kXTile;            // [kNU][128 rows][128 B]  (SW128 K-major)
+  uint8_t* Ws = Us + kNU * kUSlot;      // [kNW][64 rows][128 B]   (SW128 MN-major)
+  float* Ys = reinterpret_cast<float*>(Ws + kNW * kWTileTp);  // [64][16]
   uint64_t* x_full = reinterpret_cast<uint64_t*>(Ys + kEdges * 16);
-  uint64_t* w_full = x_full + 1;  // [3]
-  uint64_t* mma_done = w_full + 3;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
-  __shared__ int4 s_pair[kMaxPairs];  // {l | is_first_of_component << 16, i, entry0, count}
-  __shared__ int4 s_entry[kMaxEntries];
+  uint64_t* x_empty = x_full + 1;
+  uint64_t* w_full = x_empty + 1;
+  uint64_t* w_empty = w_full + kNW;
+  uint64_t* u_full = w_empty + kNW;
+  uint64_t* u_empty = u_full + kNU;
+  uint64_t* acc_full = u_empty + kNU;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int b_loc = tid >> 3, slice = tid & 7;  // edge in tile, u slice [8*slice, +8)
-  const int npairs = a.meta->npairs;
-  for (int i = tid; i < npairs; i += kTpThreads) {
-    int4 pr = a.meta->pair[i];
-    pr.x |= (a.meta->first[i] == i) ? (1 << 16) : 0;
-    s_pair[i] = pr;
-  }
-  for (int i = tid; i < a.meta->nentries; i += kTpThreads) s_entry[i] = a.meta->entry[i];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     mbar_init(x_full, 1);
-    for (int b = 0; b < 3; ++b) mbar_init(&w_full[b], 1);
-    mbar_init(&mma_done[0], 1);
-    mbar_init(&mma_done[1], 1);
+    mbar_init(x_empty, kMathWarps);
+    for (int s = 0; s < kNW; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < kNU; ++s) {
+      mbar_init(&u_full[s], kMathWarps);
+      mbar_init(&u_empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kMathWarps);
     fence_barrier_init();
-    tma_prefetch_desc(&tmW);
-    tma_prefetch_desc(&tmX);
   }
-  if (warp == 0) {
+  if (warp == kMathWarps) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
   }
@@ -104,160 +127,174 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t idesc = idesc_bf16_f32(64, 64, /*A K-major*/ false, /*B MN-major*/ true);
-  // whole 256-row boxes land (out-of-range rows zero-filled), so expect them all
-  const uint32_t x_bytes = static_cast<uint32_t>(((kEdges * a.nj + 255) / 256) * 256 * 128);
-  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
-
-  // thread-0 state for the W ring (3 buffers, one per upcoming path)
-  uint32_t w_loads[3] = {0, 0, 0};
-  int n_global = 0;  // pairs issued by this CTA (U buffer / barrier phase counter)
-  int tiles_done = 0;
   const int64_t ntiles = (a.batch + kEdges - 1) / kEdges;
-  auto issue_w = [&](int path, int slot) {
-    mbar_arrive_expect_tx(&w_full[slot], kWTileTp);
-    tma_load_2d(Ws + slot * kWTileTp, &tmW, &w_full[slot], 0, path * 64, keep);
-    ++w_loads[slot];
-  };
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tiles_done) {
-    // ---- stage the tile: X by TMA (rows b*nj + j), Y as fp32, first paths' W
-    if (tid == 0) {
-      mbar_arrive_expect_tx(x_full, x_bytes);
-      const int rows = kEdges * a.nj;
-      for (int r0 = 0; r0 < rows; r0 += 256) {
-        tma_load_2d(Xs + r0 * 128, &tmX, x_full, 0,
-                    static_cast<int32_t>(tile * kEdges * a.nj + r0), stream);
+  const int njobs = meta.njobs, npaths = meta.npaths;
+
+  if (warp == kMathWarps + 1) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tmW);
+      tma_prefetch_desc(&tmX);
+      const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+      // whole 256-row boxes land (out-of-range rows zero-filled), so expect them all
+      const uint32_t x_bytes = static_cast<uint32_t>(((kEdges * a.nj + 255) / 256) * 256 * 128);
+      int64_t wc = 0;  // W loads issued
+      int tl = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+        mbar_wait(x_empty, (tl & 1) ^ 1);  // previous tile's X fully consumed
+        mbar_arrive_expect_tx(x_full, x_bytes);
+        for (int r0 = 0; r0 < kEdges * a.nj; r0 += 256)
+          tma_load_2d(Xs + r0 * 128, &tmX, x_full, 0,
+                      static_cast<int32_t>(tile * kEdges * a.nj + r0), stream);
+        for (int ps = 0; ps < npaths; ++ps, ++wc) {
+          const int slot = static_cast<int>(wc % kNW);
+          mbar_wait(&w_empty[slot], ((wc / kNW) & 1) ^ 1);
+          mbar_arrive_expect_tx(&w_full[slot], kWTileTp);
+          tma_load_2d(Ws + slot * kWTileTp, &tmW, &w_full[slot], 0, meta.path_l[ps] * 64, keep);
+        }
       }
-      if (npairs > 0) issue_w(s_pair[0].x & 0xFFFF, 0);
     }
-    for (int e = tid; e < kEdges * 16; e += kTpThreads) {
-      const int bb = e >> 4, k = e & 15;
-      const int64_t b = tile * kEdges + bb;
-      Ys[e] = (b < a.batch && k < a.nk) ? __bfloat162float(a.Y[b * a.nk + k]) : 0.f;
+  } else if (warp == kMathWarps) {
+    // ---------------------------------------------------------- UMMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, 64, /*A K-major*/ false, /*B MN-major*/ true);
+      int tl = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+        mbar_wait(acc_empty, (tl & 1) ^ 1);  // previous tile drained from TMEM
+        tc_fence_after();
+        const int64_t jc0 = static_cast<int64_t>(tl) * njobs;
+        const int64_t wc0 = static_cast<int64_t>(tl) * npaths;
+        for (int n = 0; n < njobs; ++n) {
+          const int4 job = meta.job[n];
+          const int cp = job.y & 0xFF, ps = job.y >> 8;
+          const int64_t wc = wc0 + ps;
+          const int wslot = static_cast<int>(wc % kNW);
+          if ((job.x >> 10) & 1) mbar_wait(&w_full[wslot], (wc / kNW) & 1);
+          const int64_t jc = jc0 + n;
+          const int us = static_cast<int>(jc % kNU);
+          mbar_wait(&u_full[us], (jc / kNU) & 1);
+          tc_fence_after();
+          const uint32_t u0 = smem_u32(Us + us * kUSlot);
+          const uint32_t w0 = smem_u32(Ws + wslot * kWTileTp);
+          const bool first = (job.x >> 8) & 1;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
+            umma_f16(tmem + cp * 64, smem_desc(u0 + kk * 32, 16, 1024, kLayoutSW128), bd, idesc,
+                     (!first || kk > 0) ? 1u : 0u);
+            umma_f16(tmem + cp * 64, smem_desc(u0 + kUHalf + kk * 32, 16, 1024, kLayoutSW128), bd,
+                     idesc, 1u);
+          }
+          umma_commit(&u_empty[us]);                         // U slot reusable
+          if ((job.x >> 9) & 1) umma_commit(&w_empty[wslot]);  // last job of this path
+        }
+        umma_commit(acc_full);
+      }
     }
-    mbar_wait(x_full, tiles_done & 1);
-    __syncthreads();
+  } else {
+    // ---------------------------------------------------------- math warps
+    const int b_loc = tid >> 3, slice = tid & 7;  // edge in tile, u slice [8*slice, +8)
+    const uint32_t row1 = b_loc * 128 + ((slice ^ (b_loc & 7)) << 4);              // comp 2cp
+    const uint32_t row2 = (64 + b_loc) * 128 + ((slice ^ ((64 + b_loc) & 7)) << 4);  // comp 2cp+1
     const uint8_t* xrow = Xs + b_loc * a.nj * 128 + slice * 16;
-    const float* yrow = Ys + b_loc * 16;
-    int cur_path = -1, path_idx = -1;
-    for (int n = 0; n < npairs; ++n, ++n_global) {
-      const int4 pr = s_pair[n];
-      const int path = pr.x & 0xFFFF;
-      const bool new_path = path != cur_path;
-      if (new_path) {
-        cur_path = path;
-        ++path_idx;
-        if (tid == 0) {
-          // prefetch the next path's W into the slot last used two paths ago
-          for (int m = n + 1; m < npairs; ++m) {
-            const int pth = s_pair[m].x & 0xFFFF;
-            if (pth != path) {
-              issue_w(pth, (path_idx + 1) % 3);
-              break;
+    float* yrow = Ys + b_loc * 16;
+    int tl = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+      const int64_t b = tile * kEdges + b_loc;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int k = 2 * slice + q;
+        yrow[k] = (b < a.batch && k < a.nk) ? __bfloat162float(a.Y[b * a.nk + k]) : 0.f;
+      }
+      __syncwarp();  // an edge's 8 threads share one warp
+      mbar_wait(x_full, tl & 1);
+      const int64_t jc0 = static_cast<int64_t>(tl) * njobs;
+      for (int n = 0; n < njobs; ++n) {
+        const int4 job = meta.job[n];
+        // per component of the pair: U = hi + lo, both bf16 (the UMMA pair sees U
+        // to ~2^-16 relative, so the only bf16 roundings are the operands X, Y, W)
+        uint4 u[2], ul[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e0 = h ? (job.w & 0xFFFF) : (job.z & 0xFFFF);
+          const int ne = h ? (job.w >> 16) : (job.z >> 16);
+          float2 a2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
+          for (int e = e0; e < e0 + ne; ++e) {
+            const int2 en = meta.entry[e];
+            const float coef = __int_as_float(en.y) * yrow[(en.x >> 8) & 0xFF];
+            const uint4 xv = *reinterpret_cast<const uint4*>(xrow + (en.x & 0xFF) * 128);
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a2[q] = ffma2(coef, __bfloat1622float2(xh[q]), a2[q]);
+          }
+          __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&u[h]);
+          __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&ul[h]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ph[q] = __floats2bfloat162_rn(a2[q].x, a2[q].y);
+            const float2 back = __bfloat1622float2(ph[q]);
+            pl[q] = __floats2bfloat162_rn(a2[q].x - back.x, a2[q].y - back.y);
+          }
+        }
+        const int64_t jc = jc0 + n;
+        const int us = static_cast<int>(jc % kNU);
+        mbar_wait(&u_empty[us], ((jc / kNU) & 1) ^ 1);
+        uint8_t* U = Us + us * kUSlot;
+        *reinterpret_cast<uint4*>(U + row1) = u[0];
+        *reinterpret_cast<uint4*>(U + row2) = u[1];
+        *reinterpret_cast<uint4*>(U + kUHalf + row1) = ul[0];
+        *reinterpret_cast<uint4*>(U + kUHalf + row2) = ul[1];
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&u_full[us]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(x_empty);  // X of this tile no longer read
+      // ---- epilogue: TMEM -> Z (lanes: quarter q -> comp parity q>>1, edges (q&1)*32+lane)
+      mbar_wait(acc_full, tl & 1);
+      tc_fence_after();
+      const int quarter = warp & 3, grp = warp >> 2;
+      const int64_t be = tile * kEdges + (quarter & 1) * 32 + lane;
+#pragma unroll 1
+      for (int cp = 2 * grp; cp < 2 * grp + 2; ++cp) {
+        const int comp = 2 * cp + (quarter >> 1);
+        const bool has = comp < a.ni && ((meta.present >> comp) & 1);
+        const bool row_ok = be < a.batch && comp < a.ni;
+        float4* z = reinterpret_cast<float4*>(a.Z + (be * a.ni + comp) * 64);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {  // 16 columns at a time keeps register pressure low
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cp * 64 + c * 16,
+                             r);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float4 v = has ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                           __uint_as_float(r[4 * e + 2]),
+                                           __uint_as_float(r[4 * e + 3]))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+              if (a.accumulate) {
+                const float4 o = z[c * 4 + e];
+                v.x += o.x;
+                v.y += o.y;
+                v.z += o.z;
+                v.w += o.w;
+              }
+              z[c * 4 + e] = v;
             }
           }
         }
       }
-      float acc[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-      for (int e = pr.z; e < pr.z + pr.w; ++e) {
-        const int4 en = s_entry[e];
-        const float coef = __int_as_float(en.z) * yrow[en.y];
-        const uint4 xv = *reinterpret_cast<const uint4*>(xrow + en.x * 128);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xv);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f = __bfloat1622float2(h[q]);
-          acc[2 * q] = fmaf(coef, f.x, acc[2 * q]);
-          acc[2 * q + 1] = fmaf(coef, f.y, acc[2 * q + 1]);
-        }
-      }
-      // U = hi + lo, both bf16: the UMMA pair sees U to ~2^-16 relative, so the
-      // only bf16 roundings are the operands X, Y, W themselves.
-      uint4 hi, lo;
-      __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&hi);
-      __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&lo);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        ph[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
-        const float2 back = __bfloat1622float2(ph[q]);
-        pl[q] = __floats2bfloat162_rn(acc[2 * q] - back.x, acc[2 * q + 1] - back.y);
-      }
-      const int buf = n_global & 1;
-      if (n_global >= 2) mbar_wait(&mma_done[buf], ((n_global - 2) >> 1) & 1);
-      const uint32_t off = b_loc * 128 + ((slice ^ (b_loc & 7)) << 4);
-      *reinterpret_cast<uint4*>(Us + (2 * buf) * kUTile + off) = hi;
-      *reinterpret_cast<uint4*>(Us + (2 * buf + 1) * kUTile + off) = lo;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        const int wslot = path_idx % 3;
-        if (new_path) mbar_wait(&w_full[wslot], (w_loads[wslot] - 1) & 1);
-        tc_fence_after();
-        const int i = pr.y;
-        // component i: columns 64*(i%8), lane set 16*(i/8) (M=64 half subpartitions)
-        const uint32_t d = tmem + (static_cast<uint32_t>((i >> 3) * 16) << 16) + (i & 7) * 64;
-        const uint32_t u0 = smem_u32(Us + (2 * buf) * kUTile);
-        const uint32_t w0 = smem_u32(Ws + wslot * kWTileTp);
-        const bool first = (pr.x >> 16) & 1;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
-          umma_f16(d, smem_desc(u0 + kk * 32, 16, 1024, kLayoutSW128), bd, idesc,
-                   (!first || kk > 0) ? 1u : 0u);
-          umma_f16(d, smem_desc(u0 + kUTile + kk * 32, 16, 1024, kLayoutSW128), bd, idesc, 1u);
-        }
-        umma_commit(&mma_done[buf]);
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
     }
-    // ---- epilogue: all UMMAs of this tile done -> TMEM -> Z
-    if (npairs > 0) {
-      const int last = n_global - 1;
-      mbar_wait(&mma_done[last & 1], (last >> 1) & 1);
-    }
-    tc_fence_after();
-    const int quarter = warp & 3, wg = warp >> 2;  // 4 warps per TMEM lane quarter
-    const int t = tid & 31;
-    const int row = quarter * 16 + (t & 15);        // edge within tile
-    const int64_t be = tile * kEdges + row;
-#pragma unroll 1
-    for (int cb = 2 * wg; cb < 2 * wg + 2; ++cb) {  // column block: components cb, cb+8
-      const int comp = cb + 8 * (t >> 4);
-      float outv[64];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[16];
-        tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cb * 64 + c * 16,
-                           r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) outv[c * 16 + e] = __uint_as_float(r[e]);
-      }
-      const bool has = comp < a.ni && a.meta->present[comp];
-      if (be < a.batch && comp < a.ni) {
-        float4* z = reinterpret_cast<float4*>(a.Z + (be * a.ni + comp) * 64);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float4 v = has ? make_float4(outv[4 * e], outv[4 * e + 1], outv[4 * e + 2],
-                                       outv[4 * e + 3])
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (a.accumulate) {
-            const float4 o = z[e];
-            v.x += o.x;
-            v.y += o.y;
-            v.z += o.z;
-            v.w += o.w;
-          }
-          z[e] = v;
-        }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();  // TMEM drained and Xs/Ys free before the next tile
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == kMathWarps) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -295,20 +332,34 @@ __global__ void tp_simt_kernel(const int32_t* rowptr, const int32_t* slots, cons
 
 using namespace ixb;
 
-extern "C" int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ,
-                              const int32_t* CGK, const float* CGV, int64_t G, int64_t g,
-                              const void* X, const void* Y, const void* W, int w_per_batch,
-                              int64_t batch, int64_t ni, int64_t nj, int64_t nk, int64_t nl,
-                              int64_t U, int64_t Wd, float* Z, int accumulate, int flags,
-                              ixb_stream stream) {
+// ------------------------------------------------------------ host side
+// Inspector/executor split (like ixb_conv_plan): the CG table is tiny and
+// fixed across calls, so it is validated and reshaped (job table for the
+// tensor-core path, per-component slot lists for the CUDA-core path) once.
+struct ixb_tp_plan {
+  int64_t G = 0, g = 1, ni = 0, nj = 0, nk = 0, nl = 0, U = 0, Wd = 0;
+  int w_per_batch = 0;
+  const int32_t *CGL = nullptr, *CGJ = nullptr, *CGK = nullptr;
+  const float* CGV = nullptr;
+  bool tc = false;  // shape admits the tensor-core path
+  TpMeta meta{};
+  int32_t* d_rowptr = nullptr;  // CUDA-core path: slots per output component
+  int32_t* d_slots = nullptr;
+};
+
+extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ,
+                                  const int32_t* CGK, const float* CGV, int64_t G, int64_t g,
+                                  int w_per_batch, int64_t ni, int64_t nj, int64_t nk, int64_t nl,
+                                  int64_t U, int64_t Wd, int flags, ixb_stream stream,
+                                  ixb_tp_plan** out) {
   return ixb_guard([&] {
     auto s = reinterpret_cast<cudaStream_t>(stream);
-    if (G < 0 || g < 1 || batch < 0 || ni < 0 || nj < 0 || nk < 0 || nl < 0 || U < 1 || Wd < 1)
+    if (!out) fail(IXB_SHAPE, "ixb_tp_plan_create: null plan pointer");
+    *out = nullptr;
+    if (G < 0 || g < 1 || ni < 0 || nj < 0 || nk < 0 || nl < 0 || U < 1 || Wd < 1)
       fail(IXB_SHAPE, "ixb_tp_grouped: bad extents");
-    if (batch == 0 || ni == 0) return;
-    // The CG table is tiny: bring it to the host, validate it like the plan
-    // executor (gathers X/CGJ, Y/CGK, W/CGL, then scatter Z/CGI), and build
-    // the per-component slot lists.
+    // bring the table to the host and validate it like the plan executor
+    // (gathers X/CGJ, Y/CGK, W/CGL, then scatter Z/CGI; plan.cpp:544-561)
     const int64_t slots = G * g;
     std::vector<int32_t> hl(G), hi(slots), hj(slots), hk(slots);
     std::vector<float> hv(slots);
@@ -338,55 +389,104 @@ extern "C" int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int3
       bad("CGL", "W", w_per_batch ? 1 : 0, nl, hl);
       bad("CGI", "Z", 1, ni, hi);
     }
-    // slots per output component, in slot order (pads v == 0 are inert)
+    auto plan = std::make_unique<ixb_tp_plan>();
+    plan->G = G, plan->g = g, plan->ni = ni, plan->nj = nj, plan->nk = nk, plan->nl = nl;
+    plan->U = U, plan->Wd = Wd, plan->w_per_batch = w_per_batch;
+    plan->CGL = CGL, plan->CGJ = CGJ, plan->CGK = CGK, plan->CGV = CGV;
+    // CUDA-core path: slots per output component, in slot order (pads are inert)
     std::vector<std::vector<int32_t>> by_i(ni);
     for (int64_t sl = 0; sl < slots; ++sl) by_i[hi[sl]].push_back(static_cast<int32_t>(sl));
-    const bool tc = !w_per_batch && U == 64 && Wd == 64 && ni <= 16 && nj <= 16 && nk <= 16 &&
-                    nl >= 1 && nl <= kMaxPaths && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
-                    reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
-                    reinterpret_cast<uintptr_t>(Z) % 16 == 0;
+    std::vector<int32_t> rowptr(ni + 1, 0), flat;
+    for (int64_t i = 0; i < ni; ++i) {
+      rowptr[i + 1] = rowptr[i] + static_cast<int32_t>(by_i[i].size());
+      flat.insert(flat.end(), by_i[i].begin(), by_i[i].end());
+    }
+    IXB_CUDA_CHECK(cudaMalloc(&plan->d_rowptr, (ni + 1) * 4));
+    IXB_CUDA_CHECK(cudaMalloc(&plan->d_slots, (flat.size() + 1) * 4));
+    IXB_CUDA_CHECK(cudaMemcpyAsync(plan->d_rowptr, rowptr.data(), (ni + 1) * 4,
+                                   cudaMemcpyHostToDevice, s));
+    if (!flat.empty())
+      IXB_CUDA_CHECK(cudaMemcpyAsync(plan->d_slots, flat.data(), flat.size() * 4,
+                                     cudaMemcpyHostToDevice, s));
+    // tensor-core path: jobs (l, component pair) in (l, cp) order; entries
+    // (j, k, v) of each component in slot order, pads (v == 0) dropped
+    bool tc = !w_per_batch && U == 64 && Wd == 64 && ni <= 16 && nj <= 16 && nk <= 16 && nl >= 1;
     if (tc) {
-      // pairs (l, i) in (l, i) order; entries (j, k, v) in slot order, pads dropped
-      TpMeta meta{};
-      meta.nl = static_cast<int>(nl);
+      TpMeta& meta = plan->meta;
       meta.ni = static_cast<int>(ni);
       std::vector<std::vector<std::vector<int32_t>>> li(nl, std::vector<std::vector<int32_t>>(ni));
       for (int64_t sl = 0; sl < slots; ++sl) {
         if (hv[sl] == 0.f) continue;
         li[hl[sl / g]][hi[sl]].push_back(static_cast<int32_t>(sl));
       }
-      int np = 0, ne = 0;
-      std::vector<int> first_of_i(ni, -1);
-      for (int l = 0; l < nl; ++l) {
-        for (int i = 0; i < ni; ++i) {
-          if (li[l][i].empty()) continue;
-          if (np >= kMaxPairs || ne + static_cast<int>(li[l][i].size()) > kMaxEntries)
-            fail(IXB_SHAPE, "ixb_tp_grouped: CG table too large for the tensor-core path");
-          if (first_of_i[i] < 0) first_of_i[i] = np;
-          meta.pair[np] = make_int4(l, i, ne, static_cast<int>(li[l][i].size()));
-          for (int32_t sl : li[l][i]) {
-            int vbits;
-            std::memcpy(&vbits, &hv[sl], sizeof vbits);
-            meta.entry[ne++] = make_int4(hj[sl], hk[sl], vbits, 0);
+      int njob = 0, ne = 0, nps = 0;
+      std::vector<bool> touched((ni + 1) / 2, false);
+      for (int l = 0; l < nl && tc; ++l) {
+        const int first_job = njob;
+        for (int cp = 0; cp < (ni + 1) / 2 && tc; ++cp) {
+          int e[2] = {0, 0}, n[2] = {0, 0};
+          for (int h = 0; h < 2 && tc; ++h) {
+            const int i = 2 * cp + h;
+            if (i >= ni) continue;
+            e[h] = ne;
+            for (int32_t sl : li[l][i]) {
+              if (ne >= kMaxEntries) {
+                tc = false;
+                break;
+              }
+              int vbits;
+              std::memcpy(&vbits, &hv[sl], sizeof vbits);
+              meta.entry[ne++] = make_int2(hj[sl] | (hk[sl] << 8), vbits);
+            }
+            n[h] = ne - e[h];
+            if (n[h] > 0) meta.present |= 1 << i;
           }
-          ++np;
+          if (!tc || n[0] + n[1] == 0) continue;
+          if (njob >= kMaxJobs || nps >= kMaxPathSeq) {
+            tc = false;
+            break;
+          }
+          const int ft = touched[cp] ? 0 : 1;
+          touched[cp] = true;
+          const int fp = njob == first_job ? 1 : 0;
+          meta.job[njob] = make_int4(l | (ft << 8) | (fp << 10), cp | (nps << 8),
+                                     e[0] | (n[0] << 16), e[1] | (n[1] << 16));
+          ++njob;
+        }
+        if (tc && njob > first_job) {
+          meta.job[njob - 1].x |= 1 << 9;  // last job of this path
+          meta.path_l[nps++] = l;
         }
       }
-      meta.npairs = np;
-      meta.nentries = ne;
-      for (int n = 0; n < np; ++n) meta.first[n] = first_of_i[meta.pair[n].y];
-      // components that receive no pair get zeros (`=`) / keep their value (`+=`)
-      for (int i = 0; i < 16; ++i) meta.present[i] = (i < ni && first_of_i[i] >= 0) ? 1 : 0;
-      Scratch<TpMeta> dmeta(1, s);
-      IXB_CUDA_CHECK(cudaMemcpyAsync(dmeta.p, &meta, sizeof meta, cudaMemcpyHostToDevice, s));
-      const CUtensorMap tmW = make_tmap_2d(W, 64, static_cast<uint64_t>(nl) * 64, 128, 64, 64,
+      meta.njobs = njob;
+      meta.npaths = nps;
+    }
+    plan->tc = tc;
+    *out = plan.release();
+  });
+}
+
+extern "C" int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, const void* W,
+                               int64_t batch, float* Z, int accumulate, int flags,
+                               ixb_stream stream) {
+  (void)flags;
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (!plan) fail(IXB_SHAPE, "ixb_tp_plan_run: null plan");
+    if (batch < 0) fail(IXB_SHAPE, "ixb_tp_grouped: bad extents");
+    const ixb_tp_plan& p = *plan;
+    if (batch == 0 || p.ni == 0) return;
+    const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(Z) % 16 == 0;
+    if (p.tc && aligned) {
+      const CUtensorMap tmW = make_tmap_2d(W, 64, static_cast<uint64_t>(p.nl) * 64, 128, 64, 64,
                                            CU_TENSOR_MAP_SWIZZLE_128B);
-      const CUtensorMap tmX = make_tmap_2d(X, 64, static_cast<uint64_t>(batch) * nj, 128, 64, 256,
-                                           CU_TENSOR_MAP_SWIZZLE_NONE);
-      TpArgs args{static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(Y), Z,
-                  batch, static_cast<int>(nj), static_cast<int>(nk), static_cast<int>(ni),
-                  accumulate, dmeta.p};
-      const uint32_t smem = 4 * kUTile + 3 * kWTileTp + kXTile + kEdges * 16 * 4 + 256 + 1024;
+      const CUtensorMap tmX = make_tmap_2d(X, 64, static_cast<uint64_t>(batch) * p.nj, 128, 64,
+                                           256, CU_TENSOR_MAP_SWIZZLE_NONE);
+      TpArgs args{static_cast<const __nv_bfloat16*>(Y), Z, batch, static_cast<int>(p.nj),
+                  static_cast<int>(p.nk), static_cast<int>(p.ni), accumulate};
+      const uint32_t smem = kXTile + kNU * kUSlot + kNW * kWTileTp + kEdges * 16 * 4 + 256 + 1024;
       static std::once_flag once;
       std::call_once(once, [&] {
         cuda_check(cudaFuncSetAttribute(tp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -395,28 +495,41 @@ extern "C" int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int3
       });
       int64_t grid = ceil_div(batch, kEdges);
       if (grid > sm_count()) grid = sm_count();
-      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, smem, s>>>(tmW, tmX, args);
+      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, smem, s>>>(tmW, tmX, p.meta, args);
       IXB_LAUNCH_CHECK("tp_tc_kernel");
-      IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // host meta buffer lifetime
       return;
     }
-    std::vector<int32_t> rowptr(ni + 1, 0), flat;
-    for (int64_t i = 0; i < ni; ++i) {
-      rowptr[i + 1] = rowptr[i] + static_cast<int32_t>(by_i[i].size());
-      flat.insert(flat.end(), by_i[i].begin(), by_i[i].end());
-    }
-    Scratch<int32_t> drow(ni + 1, s), dslots(flat.size() + 1, s);
-    IXB_CUDA_CHECK(cudaMemcpyAsync(drow.p, rowptr.data(), (ni + 1) * 4, cudaMemcpyHostToDevice, s));
-    if (!flat.empty()) {
-      IXB_CUDA_CHECK(cudaMemcpyAsync(dslots.p, flat.data(), flat.size() * 4,
-                                     cudaMemcpyHostToDevice, s));
-    }
-    const int64_t n = batch * ni * Wd;
+    const int64_t n = batch * p.ni * p.Wd;
     tp_simt_kernel<<<ceil_div(n, 256), 256, 0, s>>>(
-        drow.p, dslots.p, CGL, CGJ, CGK, CGV, g, static_cast<const __nv_bfloat16*>(X),
-        static_cast<const __nv_bfloat16*>(Y), static_cast<const __nv_bfloat16*>(W), w_per_batch,
-        batch, ni, nj, nk, nl, U, Wd, Z, accumulate);
+        p.d_rowptr, p.d_slots, p.CGL, p.CGJ, p.CGK, p.CGV, p.g,
+        static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(Y),
+        static_cast<const __nv_bfloat16*>(W), p.w_per_batch, batch, p.ni, p.nj, p.nk, p.nl, p.U,
+        p.Wd, Z, accumulate);
     IXB_LAUNCH_CHECK("tp_simt_kernel");
-    IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors' lifetime
   });
+}
+
+extern "C" void ixb_tp_plan_free(ixb_tp_plan* plan) {
+  if (!plan) return;
+  cudaFree(plan->d_rowptr);  // synchronous: in-flight runs finish first
+  cudaFree(plan->d_slots);
+  delete plan;
+}
+
+extern "C" int ixb_tp_grouped(const int32_t* CGL, const int32_t* CGI, const int32_t* CGJ,
+                              const int32_t* CGK, const float* CGV, int64_t G, int64_t g,
+                              const void* X, const void* Y, const void* W, int w_per_batch,
+                              int64_t batch, int64_t ni, int64_t nj, int64_t nk, int64_t nl,
+                              int64_t U, int64_t Wd, float* Z, int accumulate, int flags,
+                              ixb_stream stream) {
+  if (G < 0 || g < 1 || batch < 0 || ni < 0 || nj < 0 || nk < 0 || nl < 0 || U < 1 || Wd < 1)
+    return ixb_guard([] { fail(IXB_SHAPE, "ixb_tp_grouped: bad extents"); });
+  if (batch == 0 || ni == 0) return ixb_guard([] {});
+  ixb_tp_plan* plan = nullptr;
+  int rc = ixb_tp_plan_create(CGL, CGI, CGJ, CGK, CGV, G, g, w_per_batch, ni, nj, nk, nl, U, Wd,
+                              flags, stream, &plan);
+  if (rc != IXB_OK) return rc;
+  rc = ixb_tp_plan_run(plan, X, Y, W, batch, Z, accumulate, flags, stream);
+  ixb_tp_plan_free(plan);
+  return rc;
 }

@@ -133,3 +133,41 @@ def test_tp_index_errors(P, ixo):
     with pytest.raises(P.IndexRangeError) as e:
         run_tp(P, t, out)
     assert "index tensor CGK value 99 at position [1] out of range for dim 1 of Y" in str(e.value)
+
+
+def test_tp_plan_reuse_matches_one_shot(P, ixo):
+    """TpPlan (validated/reshaped once) equals ixb_tp_grouped bit for bit on
+    several batches, on both the tensor-core (shared W) and CUDA-core
+    (per-edge W) paths; create reports index errors like the one-shot call."""
+    cg, nl = cg_grouped(P, ixo, 4)
+    dev = {k: cuda(v, torch.float32 if k == "CGV" else torch.int32) for k, v in cg.items()}
+    plan = P.TpPlan(dev["CGL"], dev["CGI"], dev["CGJ"], dev["CGK"], dev["CGV"], 16, 16, 16, nl)
+    rng = ixo.Rng(21)
+    W = cuda(bf16_round(ixo.synth_dense(rng, (nl, 64, 64))), torch.bfloat16)
+    for B in (1, 64, 200):
+        X = cuda(bf16_round(ixo.synth_dense(rng, (B, 16, 64))), torch.bfloat16)
+        Y = cuda(bf16_round(ixo.synth_dense(rng, (B, 16))), torch.bfloat16)
+        Z1 = torch.zeros((B, 16, 64), device="cuda")
+        Z2 = torch.zeros((B, 16, 64), device="cuda")
+        plan.run(X, Y, W, Z1, accumulate=False)
+        P.tp_grouped(dev["CGL"], dev["CGI"], dev["CGJ"], dev["CGK"], dev["CGV"], X, Y, W, Z2,
+                     accumulate=False)
+        assert torch.equal(Z1, Z2)
+    t, expr, on, out = instances.make(ixo, "grouped_tp", 1, 77)
+    d = {k: cuda(t[k], torch.float32 if k == "CGV" else torch.int32)
+         for k in ("CGL", "CGI", "CGJ", "CGK", "CGV")}
+    Bb, ni, Wd = out.shape
+    nj, nk, nl2, U = t["X"].shape[1], t["Y"].shape[1], t["W"].shape[1], t["X"].shape[2]
+    plan2 = P.TpPlan(d["CGL"], d["CGI"], d["CGJ"], d["CGK"], d["CGV"], ni, nj, nk, nl2, U, Wd,
+                     w_per_batch=True)
+    Z = cuda(out, torch.float32)
+    plan2.run(cuda(t["X"], torch.bfloat16), cuda(t["Y"], torch.bfloat16),
+              cuda(t["W"], torch.bfloat16), Z)
+    np.testing.assert_array_equal(Z.cpu().numpy().astype(np.int64), ixo.einsum(expr, t, on, out))
+    bad = dict(d)
+    bad["CGK"] = bad["CGK"].clone()
+    bad["CGK"].view(-1)[1] = 99
+    with pytest.raises(P.IndexRangeError) as e:
+        P.TpPlan(bad["CGL"], bad["CGI"], bad["CGJ"], bad["CGK"], bad["CGV"], ni, nj, nk, nl2, U,
+                 Wd, w_per_batch=True)
+    assert "index tensor CGK value 99 at position [1] out of range for dim 1 of Y" in str(e.value)
