@@ -16,7 +16,8 @@
  *   IXB_OK 0, IXB_FAILURE 1 (std::runtime_error / std::invalid_argument),
  *   IXB_PARSE 2 (ParseError), IXB_BIND 3 (BindError), IXB_SHAPE 4
  *   (ShapeError / InferenceError), IXB_INDEX_RANGE 6 (IndexRangeError),
- *   IXB_CUDA 7 (device failure — no reference equivalent).
+ *   IXB_CUDA 7 (device failure — no reference equivalent), IXB_IO 8 (IoError;
+ *   the reference CLI reports it with exit code 1).
  * The message of the last failure on the calling thread is ixb_last_error().
  */
 #ifndef IXB_H
@@ -38,10 +39,15 @@ enum ixb_status {
   IXB_BIND = 3,
   IXB_SHAPE = 4,
   IXB_INDEX_RANGE = 6,
-  IXB_CUDA = 7
+  IXB_CUDA = 7,
+  IXB_IO = 8
 };
 
-enum ixb_dtype { IXB_F32 = 0, IXB_BF16 = 1 };
+/* Device element types. Evaluators take IXB_F32 / IXB_BF16 values; the
+ * sorted-run builders (ixb_groupcoo_pack, ixb_group_coo_tensor_pack) also
+ * carry 8-byte values (IXB_F64 / IXB_I64) unchanged, and the file I/O
+ * below converts between the files' real64/int64 and any of these. */
+enum ixb_dtype { IXB_F32 = 0, IXB_BF16 = 1, IXB_F64 = 2, IXB_I32 = 3, IXB_I64 = 4, IXB_U8 = 5 };
 
 /* Evaluator flags. */
 enum ixb_flags {
@@ -135,6 +141,12 @@ int ixb_group_coo_tensor_pack(ixb_pack* plan, const void* values, int dtype,
 
 /* Reference tuner over a device occupancy source (tuner.cpp:31-118):
  * coord: nnz int32 coordinates in [0, extent). */
+/* select's full TuneReport (tuner.hpp:43-63): g*, the power-of-two
+ * candidates (at most 2) and their cost_exact scores, and the chosen g —
+ * what the convert manifest's "tuner" block records (driver.cpp:460-470). */
+int ixb_tune_report(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
+                    ixb_stream stream, int64_t* g, double* gstar, int64_t* cand_g,
+                    double* cand_score, int* ncand);
 int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
                         ixb_stream stream, int64_t* g_out, double* gstar_out);
 
@@ -218,6 +230,36 @@ int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const int32_t* CG
 int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, const void* W, int64_t batch,
                     float* Z, int accumulate, int flags, ixb_stream stream);
 void ixb_tp_plan_free(ixb_tp_plan* plan);
+
+/* ======================================================================
+ * On-disk formats straight to/from the device.
+ * ==================================================================== */
+/* .ixt tensor files (tensor.hpp:65-73, tensor.cpp:158-225,
+ * docs/file-formats.md): header query; load into a device buffer of
+ * `dtype` (int64 files -> IXB_I32 are range-checked; real64 -> int dtypes
+ * refused); save a device array (float dtypes as real64, integer dtypes as
+ * int64), bitwise-compatible with the reference's save_tensor. Errors and
+ * messages follow load_tensor / save_tensor (IXB_IO). */
+int ixb_ixt_info(const char* path, int* kind, int* rank, int64_t* dims16);
+int ixb_ixt_load(const char* path, void* dst, int dtype, ixb_stream stream);
+int ixb_ixt_save(const char* path, const void* src, int dtype, int rank, const int64_t* dims,
+                 ixb_stream stream);
+
+/* MatrixMarket (matrix_market.hpp:16, matrix_market.cpp:30-159): parsed on
+ * the host with the reference's rules and messages (one-based -> zero-based,
+ * duplicates kept, symmetric/skew-symmetric expanded, array files dense
+ * column-major -> row-major); then copied to the device as COO (int32
+ * coordinates + values of `dtype`) or as a dense [rows, cols] array.
+ * kind: 0 real64, 1 int64 (integer field). nnz = entries after expansion
+ * (rows*cols for array files). ixb_mtx_to_host copies the 8-byte host form
+ * (rows/cols int64, values double or int64 by kind). */
+typedef struct ixb_mtx ixb_mtx;
+int ixb_mtx_read(const char* path, ixb_mtx** mtx, int* is_dense, int* kind, int64_t* rows,
+                 int64_t* cols, int64_t* nnz);
+int ixb_mtx_to_device(const ixb_mtx* mtx, int32_t* row, int32_t* col, void* values, int dtype,
+                      ixb_stream stream);
+int ixb_mtx_to_host(const ixb_mtx* mtx, int64_t* row, int64_t* col, void* values);
+void ixb_mtx_free(ixb_mtx* mtx);
 
 /* ======================================================================
  * Multi-GPU sharding (host-side planning). Cuts G sorted

@@ -58,6 +58,8 @@ def lib():
             "ixr_count_model": (C.c_int, [I64, I64, P, S, S, P]),
             "ixr_max_rel_error": (D, [C.c_int, I64, P, P]),
             "ixr_tensor_hash": (U64, [C.c_int, C.c_int, P, P]),
+            "ixr_load_tensor": (P, [S]),
+            "ixr_save_tensor": (C.c_int, [S, C.c_int, C.c_int, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -265,3 +267,46 @@ def tensor_hash(a):
     a = np.ascontiguousarray(a)
     sh = np.asarray(a.shape, np.int64)
     return lib().ixr_tensor_hash(_kind(a), a.ndim, _p(sh), _p(a))
+
+
+# ---- file formats (test fixtures and parity only)
+def ref_io(*args):
+    """Runs oracle/_ref/ref_io (the reference's file-format code in its own
+    process); returns (exit code, stdout)."""
+    import subprocess
+    exe = os.path.join(ORACLE_DIR, "_ref", "ref_io")
+    r = subprocess.run([exe, *map(str, args)], capture_output=True, text=True)
+    return r.returncode, r.stdout
+
+
+def load_matrix_market(path):
+    """The reference's load_matrix_market (matrix_market.cpp:30-159):
+    {"dense"} or {"rows", "cols", "row", "col", "values"}; raises RefError
+    with the reference's message."""
+    _, out = ref_io("mtx", path)
+    d = json.loads(out)
+    if "error" in d:
+        raise RefError(1, d["error"])
+    dt = np.int64 if d["kind"] else np.float64
+    if "dense" in d:
+        return {"dense": np.asarray(d["dense"], dt).reshape(d["shape"])}
+    return {"rows": d["rows"], "cols": d["cols"], "row": np.asarray(d["row"], np.int64),
+            "col": np.asarray(d["col"], np.int64), "values": np.asarray(d["values"], dt)}
+
+
+def cmd_convert(inp, outdir, fmt, g=1, group_dim=0, block=None, prefix="A"):
+    """cmd_convert (driver.cpp:403-514) without --measure; returns the exit code."""
+    bm, bk = block if block else (0, 0)
+    rc, _ = ref_io("convert", inp, outdir, fmt, g, group_dim, bm, bk, prefix)
+    return rc
+
+
+def load_tensor(path):
+    return Bag(lib().ixr_load_tensor(os.fsencode(path)))["t"]
+
+
+def save_tensor(path, arr):
+    arr = np.ascontiguousarray(arr)
+    sh = np.asarray(arr.shape, np.int64)
+    if lib().ixr_save_tensor(os.fsencode(path), _kind(arr), arr.ndim, _p(sh), _p(arr)) != 0:
+        raise RefError(lib().ixr_last_code(), lib().ixr_last_error().decode())

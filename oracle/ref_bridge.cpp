@@ -16,12 +16,15 @@
 #include <exception>
 #include <map>
 #include <memory>
+#include <sstream>
 #include <string>
+#include <variant>
 #include <vector>
 
 #include "ixsum/driver.hpp"
 #include "ixsum/formats.hpp"
 #include "ixsum/kernel.hpp"
+#include "ixsum/matrix_market.hpp"
 #include "ixsum/plan.hpp"
 #include "ixsum/synth.hpp"
 #include "ixsum/tensor.hpp"
@@ -394,6 +397,26 @@ double ixr_max_rel_error(int kind, int64_t n, const void* a, const void* bb) {
 
 uint64_t ixr_tensor_hash(int kind, int rank, const int64_t* shape, const void* data) {
   return tensor_hash(make_tensor(kind, rank, shape, data));
+}
+
+// ---- .ixt files (tensor.cpp:158-225)
+void* ixr_load_tensor(const char* path) {
+  return guard(
+      [&]() -> void* {
+        auto* b = new Bag();
+        b->t["t"] = load_tensor(path);
+        return b;
+      },
+      nullptr);
+}
+
+int ixr_save_tensor(const char* path, int kind, int rank, const int64_t* shape, const void* data) {
+  return guard(
+      [&]() -> int {
+        save_tensor(path, make_tensor(kind, rank, shape, data));
+        return 0;
+      },
+      -1);
 }
 
 }  // extern "C"

@@ -10,9 +10,11 @@ Names and argument meaning follow the reference:
   dense_to_coo, coo_to_groupcoo, dense_to_blockgroupcoo, group_coo_tensor,
   emit_operands, execute_mode("b200", ...)
 Errors raise the reference's exception classes (ParseError, BindError,
-ShapeError, IndexRangeError) with the reference's message content.
+ShapeError, IndexRangeError, IoError) with the reference's message content.
+On-disk formats (.ixt, MatrixMarket, convert directories) load straight to
+the device: see `io`.
 """
-from .abi import (BindError, IxbError, IndexRangeError, ParseError, ShapeError, lib,
+from .abi import (BindError, IxbError, IndexRangeError, IoError, ParseError, ShapeError, lib,
                   lib_path)
 from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupcoo,
                   dense_to_coo, dense_to_groupcoo, coo_to_groupcoo, emit_operands,
@@ -20,12 +22,17 @@ from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupco
                   spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups, ConvPlan, TpPlan,
                   count_accesses_model)
 from .executor import execute_mode, match_workload, WORKLOADS
+from . import io
+from .io import (ixt_info, load_ixt, save_ixt, load_matrix_market, read_matrix_market_host,
+                 save_format, load_format, convert, tune_report)
 
 __all__ = [
     "lib", "lib_path", "IxbError", "ParseError", "BindError", "ShapeError", "IndexRangeError",
+    "IoError",
     "GroupCoo", "BlockGroupCoo", "GroupCooTensor", "dense_to_coo", "coo_to_groupcoo",
     "dense_to_groupcoo", "dense_to_blockgroupcoo", "group_coo_tensor", "emit_operands",
     "kernel_map", "tune_group_size", "spmm_groupcoo", "spmm_blockgroupcoo", "conv_grouped",
     "tp_grouped", "shard_groups", "ConvPlan", "TpPlan", "count_accesses_model", "execute_mode", "match_workload",
-    "WORKLOADS",
+    "WORKLOADS", "io", "ixt_info", "load_ixt", "save_ixt", "load_matrix_market",
+    "read_matrix_market_host", "save_format", "load_format", "convert", "tune_report",
 ]

@@ -34,7 +34,11 @@ class IndexRangeError(IxbError):  # plan.hpp:64-66, exit code 6
     pass
 
 
-_BY_CODE = {2: ParseError, 3: BindError, 4: ShapeError, 6: IndexRangeError}
+class IoError(IxbError):          # tensor.hpp:75-77 (reference CLI exit code 1)
+    pass
+
+
+_BY_CODE = {2: ParseError, 3: BindError, 4: ShapeError, 6: IndexRangeError, 8: IoError}
 
 _SIGS = {
     "ixb_last_error": (C.c_char_p, []),
@@ -93,6 +97,18 @@ _SIGS = {
                                                      C.c_void_p]),
     "ixb_tp_plan_free": (None, [C.c_void_p]),
     "ixb_shard_groups": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "ixb_tune_report": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ixb_ixt_info": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ixb_ixt_load": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "ixb_ixt_save": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                               C.c_void_p]),
+    "ixb_mtx_read": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p]),
+    "ixb_mtx_to_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                    C.c_void_p]),
+    "ixb_mtx_to_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ixb_mtx_free": (None, [C.c_void_p]),
     "ixb_rng_new": (C.c_void_p, [C.c_uint64]),
     "ixb_rng_free": (None, [C.c_void_p]),
     "ixb_rng_next": (C.c_uint64, [C.c_void_p]),

@@ -12,7 +12,9 @@ import torch
 
 from .abi import ShapeError, check, lib
 
-_DT = {torch.float32: 0, torch.bfloat16: 1}
+# ixb_dtype codes: evaluators take f32/bf16; builders also move f64 (and the
+# sorted-run packs int64) values unchanged
+_DT = {torch.float32: 0, torch.bfloat16: 1, torch.float64: 2, torch.int64: 4}
 
 
 def _ptr(t):
@@ -26,7 +28,7 @@ def _stream(stream=None):
 
 def _dtype_code(t):
     if t.dtype not in _DT:
-        raise ShapeError(4, f"unsupported value dtype {t.dtype}; use float32 or bfloat16")
+        raise ShapeError(4, f"unsupported value dtype {t.dtype}; use float32, bfloat16 or float64")
     return _DT[t.dtype]
 
 

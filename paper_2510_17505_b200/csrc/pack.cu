@@ -69,7 +69,8 @@ __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
 
 // select() of tuner.cpp:100-118 over device occupancy counts.
 int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_empty_rows,
-                      cudaStream_t s, double* gstar_out) {
+                      cudaStream_t s, double* gstar_out, int64_t* cand_g = nullptr,
+                      double* cand_score = nullptr, int* ncand = nullptr) {
   Scratch<OccStats> d(1, s);
   IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
   if (n > 0) {
@@ -88,7 +89,14 @@ int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_e
     gs = nn <= 0 ? 1.0 : std::sqrt(static_cast<double>(h.S) / nn);
   }
   if (gstar_out) *gstar_out = gs;
-  if (h.S == 0) return 1;  // candidate_group_sizes: {1}
+  if (h.S == 0) {  // candidate_group_sizes: {1}
+    if (ncand) {
+      *ncand = 1;
+      cand_g[0] = 1;
+      cand_score[0] = 2.0 * static_cast<double>(h.groups_pow2[0]);
+    }
+    return 1;
+  }
   // candidate_group_sizes (tuner.cpp:67-84)
   int64_t lo = 1;
   while (lo * 2 <= static_cast<int64_t>(gs)) lo *= 2;
@@ -106,6 +114,15 @@ int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_e
   int64_t chosen = lo;
   double best = cost(lo);
   if (hi != lo && cost(hi) < best) chosen = hi;
+  if (ncand) {
+    *ncand = hi == lo ? 1 : 2;
+    cand_g[0] = lo;
+    cand_score[0] = cost(lo);
+    if (hi != lo) {
+      cand_g[1] = hi;
+      cand_score[1] = cost(hi);
+    }
+  }
   return chosen;
 }
 
@@ -122,6 +139,22 @@ __device__ __forceinline__ bool nz<__nv_bfloat16>(__nv_bfloat16 v) {
 }
 template <>
 __device__ __forceinline__ bool nz<uint8_t>(uint8_t v) { return v != 0; }
+template <>
+__device__ __forceinline__ bool nz<double>(double v) { return v != 0.0; }
+
+// Dense-source element types: fp32, bf16, fp64 (u8 for block flags).
+template <typename F>
+void dispatch_dense(int dtype, F&& f) {
+  if (dtype == IXB_F32) f(float{});
+  else if (dtype == IXB_BF16) f(__nv_bfloat16{});
+  else if (dtype == IXB_F64) f(double{});
+  else f(uint8_t{});
+}
+void check_dense_dtype(int dtype) {
+  if (dtype != IXB_F32 && dtype != IXB_BF16 && dtype != IXB_F64)
+    fail(IXB_FAILURE, "unsupported dtype");
+}
+int dense_bytes(int dtype) { return dtype == IXB_BF16 ? 2 : dtype == IXB_F64 ? 8 : 4; }
 
 template <typename T>
 struct Vec16 {
@@ -281,7 +314,7 @@ struct RunPackArgs {
   int64_t n, R, g;
   const void* vals;
   void* vout;
-  int vbytes;  // 0 (no values), 2 (bf16) or 4 (f32)
+  int vbytes;  // 0 (no values), 2 (bf16), 4 (f32) or 8 (f64 / i64, copied bitwise)
   uint8_t* mask;
   int32_t* gout;  // group coordinate output [G]
 };
@@ -294,7 +327,10 @@ __global__ void run_pack_elems(RunPackArgs a) {
   const int64_t slot = (a.gofs[r] + k / a.g) * a.g + k % a.g;
   const int64_t src = a.perm ? a.perm[i] : i;
   for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][src];
-  if (a.vbytes == 4) {
+  if (a.vbytes == 8) {
+    static_cast<unsigned long long*>(a.vout)[slot] =
+        static_cast<const unsigned long long*>(a.vals)[src];
+  } else if (a.vbytes == 4) {
     static_cast<float*>(a.vout)[slot] = static_cast<const float*>(a.vals)[src];
   } else if (a.vbytes == 2) {
     static_cast<__nv_bfloat16*>(a.vout)[slot] = static_cast<const __nv_bfloat16*>(a.vals)[src];
@@ -317,7 +353,8 @@ __global__ void run_pack_runs(RunPackArgs a) {
   for (int64_t q = real_last; q < a.g; ++q) {
     const int64_t slot = (g0 + ng - 1) * a.g + q;
     for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][srcl];
-    if (a.vbytes == 4) static_cast<float*>(a.vout)[slot] = 0.f;
+    if (a.vbytes == 8) static_cast<unsigned long long*>(a.vout)[slot] = 0ull;  // 0.0 / 0
+    else if (a.vbytes == 4) static_cast<float*>(a.vout)[slot] = 0.f;
     else if (a.vbytes == 2)
       static_cast<__nv_bfloat16*>(a.vout)[slot] = __float2bfloat16(0.f);
     if (a.mask) a.mask[slot] = 0;
@@ -443,13 +480,10 @@ int64_t exclusive_scan_total(const int32_t* in, int64_t n, int32_t* out, cudaStr
 
 void count_rows(ixb_pack* P) {
   P->occ = Scratch<int32_t>(P->rows + 1, P->s);
-  if (P->dtype == IXB_F32) {
-    launch_row_count(static_cast<const float*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
-  } else if (P->dtype == IXB_BF16) {
-    launch_row_count(static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
-  } else {
-    launch_row_count(static_cast<const uint8_t*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
-  }
+  dispatch_dense(P->dtype, [&](auto tag) {
+    using T = decltype(tag);
+    launch_row_count(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
+  });
 }
 
 // Dense-row grouping plan (group_dim 0): occ -> tuner -> groups per row -> gofs.
@@ -477,9 +511,7 @@ void pack_dense_rows_t(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t*
 }
 
 void pack_dense_rows(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask) {
-  if (P->dtype == IXB_F32) pack_dense_rows_t<float>(P, AM, AK, AV, mask);
-  else if (P->dtype == IXB_BF16) pack_dense_rows_t<__nv_bfloat16>(P, AM, AK, AV, mask);
-  else pack_dense_rows_t<uint8_t>(P, AM, AK, AV, mask);
+  dispatch_dense(P->dtype, [&](auto tag) { pack_dense_rows_t<decltype(tag)>(P, AM, AK, AV, mask); });
 }
 
 // Sorted-run plan over rank coordinate arrays; key order: group_dim, then
@@ -574,7 +606,8 @@ void pack_sorted_runs(ixb_pack* P, const void* vals, int dtype, int32_t* gout,
   a.g = P->g;
   a.vals = vals;
   a.vout = vout;
-  a.vbytes = (vals && vout) ? (dtype == IXB_BF16 ? 2 : 4) : 0;
+  a.vbytes = (vals && vout) ? (dtype == IXB_BF16 ? 2 : (dtype == IXB_F64 || dtype == IXB_I64) ? 8 : 4)
+                            : 0;
   a.mask = mask;
   a.gout = gout;
   if (a.n > 0) {
@@ -585,8 +618,10 @@ void pack_sorted_runs(ixb_pack* P, const void* vals, int dtype, int32_t* gout,
   }
 }
 
-void check_dtype(int dtype) {
-  if (dtype != IXB_F32 && dtype != IXB_BF16) fail(IXB_FAILURE, "unsupported dtype");
+// Sorted-run packs only move values: 8-byte payloads pass through unchanged.
+void check_run_dtype(int dtype) {
+  if (dtype != IXB_F32 && dtype != IXB_BF16 && dtype != IXB_F64 && dtype != IXB_I64)
+    fail(IXB_FAILURE, "unsupported dtype");
 }
 
 }  // namespace
@@ -601,7 +636,7 @@ void ixb_pack_free(ixb_pack* plan) { delete plan; }
 int ixb_dense_to_coo_plan(const void* dense, int dtype, int64_t rows, int64_t cols,
                           ixb_stream stream, ixb_pack** plan, int64_t* nnz) {
   return ixb_guard([&] {
-    check_dtype(dtype);
+    check_dense_dtype(dtype);
     if (rows < 0 || cols < 0) fail(IXB_SHAPE, "dense_to_coo expects a rank-2 tensor");
     auto P = std::make_unique<ixb_pack>();
     P->type = 2;
@@ -623,14 +658,11 @@ int ixb_dense_to_coo_pack(ixb_pack* P, int32_t* row_coord, int32_t* col_coord, v
   return ixb_guard([&] {
     if (!P || P->type != 2) fail(IXB_FAILURE, "not a dense_to_coo plan");
     P->s = reinterpret_cast<cudaStream_t>(stream);
-    if (P->dtype == IXB_F32) {
-      launch_row_pack(static_cast<const float*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p, 1,
-                      1, row_coord, col_coord, static_cast<float*>(values), nullptr, P->s);
-    } else {
-      launch_row_pack(static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->occ.p,
-                      P->offs.p, 1, 1, row_coord, col_coord, static_cast<__nv_bfloat16*>(values),
-                      nullptr, P->s);
-    }
+    dispatch_dense(P->dtype, [&](auto tag) {
+      using T = decltype(tag);
+      launch_row_pack(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p, 1,
+                      1, row_coord, col_coord, static_cast<T*>(values), nullptr, P->s);
+    });
   });
 }
 
@@ -658,7 +690,7 @@ int ixb_groupcoo_pack(ixb_pack* P, const void* values, int dtype, int32_t* AM, i
                       void* AV, uint8_t* mask, ixb_stream stream) {
   return ixb_guard([&] {
     if (!P || P->type != 3 || P->rank != 2) fail(IXB_FAILURE, "not a groupcoo plan");
-    if (values) check_dtype(dtype);
+    if (values) check_run_dtype(dtype);
     P->s = reinterpret_cast<cudaStream_t>(stream);
     int32_t* mo[1] = {AK};
     pack_sorted_runs(P, values, dtype, AM, mo, AV, mask);
@@ -669,7 +701,7 @@ int ixb_dense_groupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t 
                             int group_dim, int64_t g, ixb_stream stream, ixb_pack** plan,
                             int64_t* num_groups, int64_t* g_out, int64_t* nnz) {
   return ixb_guard([&] {
-    check_dtype(dtype);
+    check_dense_dtype(dtype);
     if (g < 0) fail(IXB_SHAPE, "group size must be >= 1, got " + std::to_string(g));
     if (group_dim != 0 && group_dim != 1) fail(IXB_SHAPE, "group_dim must be 0 or 1");
     auto P = std::make_unique<ixb_pack>();
@@ -689,14 +721,11 @@ int ixb_dense_groupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t 
       P->nnz = exclusive_scan_total(P->occ.p, rows, P->offs.p, P->s);
       P->coo_r = Scratch<int32_t>(P->nnz, P->s);
       P->coo_c = Scratch<int32_t>(P->nnz, P->s);
-      if (dtype == IXB_F32) {
-        launch_row_pack(static_cast<const float*>(dense), rows, cols, P->occ.p, P->offs.p, 1, 1,
-                        P->coo_r.p, P->coo_c.p, static_cast<float*>(nullptr), nullptr, P->s);
-      } else {
-        launch_row_pack(static_cast<const __nv_bfloat16*>(dense), rows, cols, P->occ.p, P->offs.p,
-                        1, 1, P->coo_r.p, P->coo_c.p, static_cast<__nv_bfloat16*>(nullptr),
-                        nullptr, P->s);
-      }
+      dispatch_dense(dtype, [&](auto tag) {
+        using T = decltype(tag);
+        launch_row_pack(static_cast<const T*>(dense), rows, cols, P->occ.p, P->offs.p, 1, 1,
+                        P->coo_r.p, P->coo_c.p, static_cast<T*>(nullptr), nullptr, P->s);
+      });
       P->type = 3;
       P->rank = 2;
       P->coords = {P->coo_r.p, P->coo_c.p};
@@ -717,16 +746,13 @@ int ixb_dense_groupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uin
       pack_dense_rows(P, AM, AK, AV, mask);
     } else {
       // values in dense_to_coo order = row-major positions; gather by (r, c)
-      Scratch<char> vals(P->nnz * (P->dtype == IXB_BF16 ? 2 : 4), P->s);
-      if (P->dtype == IXB_F32) {
-        launch_row_pack(static_cast<const float*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p,
-                        1, 1, P->coo_r.p, P->coo_c.p, reinterpret_cast<float*>(vals.p), nullptr,
+      Scratch<char> vals(P->nnz * dense_bytes(P->dtype), P->s);
+      dispatch_dense(P->dtype, [&](auto tag) {
+        using T = decltype(tag);
+        launch_row_pack(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p,
+                        1, 1, P->coo_r.p, P->coo_c.p, reinterpret_cast<T*>(vals.p), nullptr,
                         P->s);
-      } else {
-        launch_row_pack(static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->occ.p,
-                        P->offs.p, 1, 1, P->coo_r.p, P->coo_c.p,
-                        reinterpret_cast<__nv_bfloat16*>(vals.p), nullptr, P->s);
-      }
+      });
       int32_t* mo[1] = {AK};
       pack_sorted_runs(P, vals.p, P->dtype, AM, mo, AV, mask);
     }
@@ -738,7 +764,7 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
                            ixb_pack** plan, int64_t* num_groups, int64_t* g_out,
                            int64_t* num_blocks) {
   return ixb_guard([&] {
-    check_dtype(dtype);
+    check_dense_dtype(dtype);
     if (bm < 1 || bk < 1) fail(IXB_SHAPE, "block dims must be >= 1");
     if (g < 0) fail(IXB_SHAPE, "group size must be >= 1");
     if (group_dim != 0 && group_dim != 1) fail(IXB_SHAPE, "group_dim must be 0 or 1");
@@ -757,21 +783,18 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
     const int64_t nb = P->gr * P->gcn;
     P->flags = Scratch<uint8_t>(nb + 16, P->s);
     if (nb) {
-      if (dtype == IXB_F32) {
+      dispatch_dense(dtype, [&](auto tag) {
+        using T = decltype(tag);
         block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
-            static_cast<const float*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
-      } else {
-        block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
-            static_cast<const __nv_bfloat16*>(dense), rows, cols, bm, bk, P->gr, P->gcn,
-            P->flags.p);
-      }
+            static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
+      });
       IXB_LAUNCH_CHECK("block_flags_kernel");
     }
     // group the block-level COO like coo_to_groupcoo (formats.cpp:265)
     auto I = std::make_unique<ixb_pack>();
     I->s = P->s;
     I->dense = P->flags.p;
-    I->dtype = 2;  // u8 flags
+    I->dtype = IXB_U8;  // block flags
     I->rows = P->gr;
     I->cols = P->gcn;
     I->group_dim = group_dim;
@@ -824,15 +847,12 @@ int ixb_blockgroupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint
     }
     if (AV && slots) {
       const int64_t grid = ceil_div(slots * 32, kTB);
-      if (P->dtype == IXB_F32) {
-        block_copy_kernel<<<grid, kTB, 0, P->s>>>(static_cast<const float*>(P->dense), P->rows,
+      dispatch_dense(P->dtype, [&](auto tag) {
+        using T = decltype(tag);
+        block_copy_kernel<<<grid, kTB, 0, P->s>>>(static_cast<const T*>(P->dense), P->rows,
                                                  P->cols, P->bm, P->bk, P->group_dim, AM, AK, m,
-                                                 slots, P->g, static_cast<float*>(AV));
-      } else {
-        block_copy_kernel<<<grid, kTB, 0, P->s>>>(
-            static_cast<const __nv_bfloat16*>(P->dense), P->rows, P->cols, P->bm, P->bk,
-            P->group_dim, AM, AK, m, slots, P->g, static_cast<__nv_bfloat16*>(AV));
-      }
+                                                 slots, P->g, static_cast<T*>(AV));
+      });
       IXB_LAUNCH_CHECK("block_copy_kernel");
     }
   });
@@ -863,9 +883,26 @@ int ixb_group_coo_tensor_pack(ixb_pack* P, const void* values, int dtype, int32_
                               ixb_stream stream) {
   return ixb_guard([&] {
     if (!P || P->type != 3) fail(IXB_FAILURE, "not a group_coo_tensor plan");
-    if (values) check_dtype(dtype);
+    if (values) check_run_dtype(dtype);
     P->s = reinterpret_cast<cudaStream_t>(stream);
     pack_sorted_runs(P, values, dtype, group_coord, member_coords, out_values, mask);
+  });
+}
+
+int ixb_tune_report(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
+                    ixb_stream stream, int64_t* g_out, double* gstar_out, int64_t* cand_g,
+                    double* cand_score, int* ncand) {
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (!cand_g || !cand_score || !ncand) fail(IXB_SHAPE, "ixb_tune_report: null output");
+    Scratch<int32_t> occ(extent + 1, s);
+    IXB_CUDA_CHECK(cudaMemsetAsync(occ.p, 0, (extent + 1) * 4, s));
+    if (nnz) {
+      occupancy_kernel<<<ceil_div(nnz, kTB), kTB, 0, s>>>(coord, nnz, extent, occ.p);
+      IXB_LAUNCH_CHECK("occupancy_kernel");
+    }
+    *g_out = tune_from_occ(occ.p, extent, extent, count_empty_rows, s, gstar_out, cand_g,
+                           cand_score, ncand);
   });
 }
 

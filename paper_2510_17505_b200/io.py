@@ -1,0 +1,297 @@
+"""On-disk formats straight to and from device memory.
+
+- `.ixt` tensors: `ixt_info`, `load_ixt`, `save_ixt` (tensor.hpp:65-73,
+  tensor.cpp:158-225, docs/file-formats.md).
+- MatrixMarket: `load_matrix_market` (device COO or dense) and
+  `read_matrix_market_host` (numpy; matrix_market.hpp:16,
+  matrix_market.cpp:30-159).
+- Converted format directories: `save_format` / `load_format` and `convert`,
+  the device-side equivalent of `ixsum convert` (cmd_convert,
+  driver.cpp:403-514) — same arrays, same manifest keys, built by the device
+  builders (K1/K2).
+
+File parsing runs in libixb's C++ host code; payloads cross through pinned
+staging into device buffers and are converted there (io.cu). torch is only
+device-memory plumbing here.
+"""
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .abi import ShapeError, check, lib
+from . import api
+
+# ixb_dtype codes (include/ixb.h)
+F32, BF16, F64, I32, I64, U8 = 0, 1, 2, 3, 4, 5
+_TORCH_CODE = {torch.float32: F32, torch.bfloat16: BF16, torch.float64: F64, torch.int32: I32,
+               torch.int64: I64, torch.uint8: U8}
+
+
+def _code(dtype):
+    if dtype not in _TORCH_CODE:
+        raise ShapeError(4, f"unsupported dtype {dtype}")
+    return _TORCH_CODE[dtype]
+
+
+def _device(device):
+    return torch.device(device) if device is not None else torch.device("cuda",
+                                                                          torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------- .ixt
+def ixt_info(path):
+    """Header of an .ixt file: (kind, shape) with kind 0 real64 / 1 int64."""
+    kind, rank = C.c_int(0), C.c_int(0)
+    dims = (C.c_int64 * 16)()
+    check(lib().ixb_ixt_info(os.fsencode(path), C.byref(kind), C.byref(rank), dims))
+    return kind.value, [dims[i] for i in range(rank.value)]
+
+
+def load_ixt(path, dtype=None, device=None, stream=None):
+    """load_tensor (tensor.cpp:197-225) into a device tensor of `dtype`
+    (default: float64 for real64 files, int64 for int64 files)."""
+    kind, shape = ixt_info(path)
+    if dtype is None:
+        dtype = torch.float64 if kind == 0 else torch.int64
+    out = torch.empty(shape, dtype=dtype, device=_device(device))
+    check(lib().ixb_ixt_load(os.fsencode(path), api._ptr(out), _code(dtype), api._stream(stream)))
+    return out
+
+
+def save_ixt(path, tensor, stream=None):
+    """save_tensor (tensor.cpp:176-195) of a device tensor: float dtypes as
+    real64, integer dtypes as int64."""
+    t = tensor.contiguous()
+    if not t.is_cuda:
+        raise ShapeError(4, "save_ixt expects a CUDA tensor")
+    dims = (C.c_int64 * max(t.dim(), 1))(*t.shape)
+    check(lib().ixb_ixt_save(os.fsencode(path), api._ptr(t), _code(t.dtype), t.dim(), dims,
+                             api._stream(stream)))
+
+
+# ---------------------------------------------------------------- MatrixMarket
+@dataclass
+class MtxCoo:
+    """CooMatrix (formats.hpp:15-24) as loaded from a coordinate .mtx file."""
+    rows: int
+    cols: int
+    row: torch.Tensor     # int32 [nnz] (zero-based, duplicates / mirror entries kept)
+    col: torch.Tensor     # int32 [nnz]
+    values: torch.Tensor  # [nnz]
+    integer: bool         # integer field (reference int64 values)
+
+
+class _Mtx:
+    def __init__(self, path):
+        self.h = C.c_void_p()
+        dense, kind = C.c_int(0), C.c_int(0)
+        rows, cols, nnz = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        check(lib().ixb_mtx_read(os.fsencode(path), C.byref(self.h), C.byref(dense),
+                                 C.byref(kind), C.byref(rows), C.byref(cols), C.byref(nnz)))
+        self.dense, self.kind = bool(dense.value), kind.value
+        self.rows, self.cols, self.nnz = rows.value, cols.value, nnz.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ixb_mtx_free(self.h)
+            self.h = None
+
+
+def read_matrix_market_host(path):
+    """load_matrix_market on the host (numpy): {"dense": array} for array
+    files, else {"rows", "cols", "row", "col", "values"} (int64 / float64 or
+    int64 values by field)."""
+    m = _Mtx(path)
+    vdt = np.int64 if m.kind else np.float64
+    if m.dense:
+        v = np.empty((m.rows, m.cols), vdt)
+        check(lib().ixb_mtx_to_host(m.h, None, None, v.ctypes.data_as(C.c_void_p)))
+        return {"dense": v}
+    r, c, v = np.empty(m.nnz, np.int64), np.empty(m.nnz, np.int64), np.empty(m.nnz, vdt)
+    check(lib().ixb_mtx_to_host(m.h, r.ctypes.data_as(C.c_void_p), c.ctypes.data_as(C.c_void_p),
+                                v.ctypes.data_as(C.c_void_p)))
+    return {"rows": m.rows, "cols": m.cols, "row": r, "col": c, "values": v}
+
+
+def load_matrix_market(path, dtype=torch.float32, device=None, stream=None):
+    """load_matrix_market (matrix_market.cpp:30-159) onto the device: MtxCoo
+    for coordinate files, a dense [rows, cols] tensor for array files."""
+    m = _Mtx(path)
+    dev = _device(device)
+    s = api._stream(stream)
+    if m.dense:
+        out = torch.empty((m.rows, m.cols), dtype=dtype, device=dev)
+        check(lib().ixb_mtx_to_device(m.h, None, None, api._ptr(out), _code(dtype), s))
+        return out
+    r = torch.empty(m.nnz, dtype=torch.int32, device=dev)
+    c = torch.empty(m.nnz, dtype=torch.int32, device=dev)
+    v = torch.empty(m.nnz, dtype=dtype, device=dev)
+    check(lib().ixb_mtx_to_device(m.h, api._ptr(r), api._ptr(c), api._ptr(v), _code(dtype), s))
+    return MtxCoo(m.rows, m.cols, r, c, v, bool(m.kind))
+
+
+# ---------------------------------------------------------------- tuner report
+def tune_report(coord, extent, count_empty_rows=False, stream=None):
+    """select's TuneReport (tuner.cpp:100-118): (chosen g, g*, [(g, score)])."""
+    coord = api._dev(coord, torch.int32)
+    g, gs, n = C.c_int64(0), C.c_double(0), C.c_int(0)
+    cg, cs = (C.c_int64 * 2)(), (C.c_double * 2)()
+    check(lib().ixb_tune_report(api._ptr(coord), coord.numel(), extent, int(count_empty_rows),
+                                api._stream(stream), C.byref(g), C.byref(gs), cg, cs,
+                                C.byref(n)))
+    return g.value, gs.value, [(cg[i], cs[i]) for i in range(n.value)]
+
+
+# ---------------------------------------------------------------- format directories
+def _value_dtype(integer, dtype):
+    if dtype is not None:
+        return dtype
+    return torch.int64 if integer else torch.float64
+
+
+def save_format(fmt, outdir, prefix="A", manifest=None):
+    """Writes a device format as the `ixsum convert` directory layout: one
+    .ixt per emitted array (emit_operands names, formats.cpp:340-373; mask as
+    int64) plus manifest.json (docs/file-formats.md). Returns the manifest."""
+    os.makedirs(outdir, exist_ok=True)
+    man = dict(manifest or {})
+    arrays = {}
+    if isinstance(fmt, (api.BlockGroupCoo, api.GroupCoo)):
+        # the group coordinate takes the suffix of the grouped dim (M for rows)
+        gsuf, msuf = ("M", "K") if fmt.group_dim == 0 else ("K", "M")
+        named = {prefix + "V": fmt.AV, prefix + gsuf: fmt.AM, prefix + msuf: fmt.AK,
+                 prefix + "mask": fmt.mask}
+    else:  # plain COO: dict(row, col, values) -> AV, AM, AK as emit_operands(CooMatrix)
+        named = {prefix + "V": fmt["values"], prefix + "M": fmt["row"], prefix + "K": fmt["col"]}
+    for name, t in named.items():
+        if t is None:
+            continue
+        save_ixt(os.path.join(outdir, name + ".ixt"), t)
+        arrays[name] = name + ".ixt"
+    man["arrays"] = dict(sorted(arrays.items()))
+    with open(os.path.join(outdir, "manifest.json"), "w") as f:
+        f.write(json.dumps(man, indent=2, sort_keys=True) + "\n")
+    return man
+
+
+def load_format(outdir, dtype=None, device=None, prefix="A"):
+    """Reads a convert directory back onto the device: GroupCoo /
+    BlockGroupCoo (indices int32, values `dtype`, default the file's 8-byte
+    type) or a COO dict for format "coo"."""
+    with open(os.path.join(outdir, "manifest.json")) as f:
+        man = json.load(f)
+    arr = man["arrays"]
+
+    def get(name, dt):
+        return load_ixt(os.path.join(outdir, arr[name]), dt, device)
+
+    AV = get(prefix + "V", dtype)
+    rows, cols = man["shape"]
+    if man["format"] == "coo":
+        return {"rows": rows, "cols": cols, "row": get(prefix + "M", torch.int32),
+                "col": get(prefix + "K", torch.int32), "values": AV}, man
+    gsuf, msuf = ("M", "K") if man["groupDim"] == 0 else ("K", "M")
+    AM = get(prefix + gsuf, torch.int32)  # group coordinate [G]
+    AK = get(prefix + msuf, torch.int32)  # member coordinates [G, g]
+    mask = get(prefix + "mask", torch.uint8)
+    if man["format"] == "blockgroupcoo":
+        bm, bk = man["block"]
+        nblk = int(mask.sum().item())
+        return api.BlockGroupCoo(rows, cols, bm, bk, man["groupDim"], man["g"], AM, AK, AV, mask,
+                                 nblk), man
+    return api.GroupCoo(rows, cols, man["groupDim"], man["g"], AM, AK, AV, mask), man
+
+
+def convert(input_path, outdir, format="coo", g=1, group_dim=0, block=None, prefix="A",
+            count_empty_rows=False, dtype=None, device=None, stream=None):
+    """cmd_convert (driver.cpp:403-514) with the device builders: input .mtx
+    (coordinate -> canonical COO; array -> dense_to_coo) or .ixt (dense);
+    format coo | groupcoo | auto | blockgroupcoo. `auto` records the tuner's
+    report ("scoredBy": "costExact"; the reference's `--measure` timing mode
+    is not reproduced). Values stay in their file type (fp64 / int64) unless
+    `dtype` says otherwise, so the arrays match the reference bit for bit."""
+    dev = _device(device)
+    if input_path.endswith(".mtx"):
+        m = _Mtx(input_path)
+        integer = bool(m.kind)
+        vdt = _value_dtype(integer, dtype)
+        if m.dense:
+            dense = load_matrix_market(input_path, vdt, dev, stream)
+        else:
+            coo = load_matrix_market(input_path, vdt, dev, stream)
+            dense = None
+    else:
+        kind, _ = ixt_info(input_path)
+        integer = kind == 1
+        vdt = _value_dtype(integer, dtype)
+        dense = load_ixt(input_path, vdt, dev, stream)
+        coo = None
+    if dense is not None:
+        if dense.dim() != 2:
+            raise ShapeError(4, f"dense_to_coo expects a rank-2 tensor, got rank {dense.dim()}")
+        r, c, v = api.dense_to_coo(_run_dtype_view(dense), stream)
+        v = v.view(vdt) if v.dtype != vdt else v
+        coo = MtxCoo(dense.shape[0], dense.shape[1], r, c, v, integer)
+    rows, cols = coo.rows, coo.cols
+    man = {"manifestVersion": 1, "shape": [rows, cols], "nnz": int(coo.row.numel()),
+           "groupDim": group_dim}
+    if format == "coo":
+        # canonicalize (formats.cpp:68-89): stable sort by (row, col) = the
+        # g = 1 GroupCOO order on dim 0
+        gc = _coo_to_groupcoo(coo, 0, 1, stream)
+        man.update({"format": "coo", "g": 1, "maskBytes": 0,
+                    "formatBytes": 8 * 3 * int(coo.row.numel())})
+        return save_format({"row": gc.AM, "col": gc.AK.reshape(-1), "values": gc.AV.reshape(-1)},
+                           outdir, prefix, man)
+    if format in ("groupcoo", "auto"):
+        man["format"] = "groupcoo"
+        if format == "auto":
+            coord = coo.row if group_dim == 0 else coo.col
+            g, gs, cands = tune_report(coord, rows if group_dim == 0 else cols, count_empty_rows,
+                                       stream)
+            man["tuner"] = {"gStar": gs, "scoredBy": "costExact",
+                            "candidates": [{"g": cg, "score": sc} for cg, sc in cands]}
+        gc = _coo_to_groupcoo(coo, group_dim, g, stream)
+        G = gc.num_groups()
+        man.update({"g": g, "numGroups": G, "formatBytes": 8 * (G + 2 * G * g),
+                    "maskBytes": G * g})
+        return save_format(gc, outdir, prefix, man)
+    if format == "blockgroupcoo":
+        if block is None or len(block) != 2:
+            raise ValueError("blockgroupcoo conversion needs --block bMxbK")
+        if dense is None:  # coo_to_dense: duplicates sum (scatter-add semantics)
+            dense = torch.zeros((rows, cols), dtype=vdt, device=dev)
+            dense.view(-1).index_put_((coo.row.long() * cols + coo.col.long(),), coo.values,
+                                      accumulate=True)
+        bf = api.dense_to_blockgroupcoo(_run_dtype_view(dense), block[0], block[1], g, group_dim,
+                                        stream)
+        if bf.AV.dtype != vdt:
+            bf.AV = bf.AV.view(vdt)
+        G = bf.num_groups()
+        man.update({"format": "blockgroupcoo", "g": g, "block": [bf.block_rows, bf.block_cols],
+                    "numGroups": G, "formatBytes": 8 * (G + G * g + G * g * block[0] * block[1]),
+                    "maskBytes": G * g})
+        return save_format(bf, outdir, prefix, man)
+    raise ValueError("unknown format: " + format)
+
+
+def _run_dtype_view(t):
+    """Integer-valued dense sources go through the builders as their 8-byte
+    bit pattern viewed as float64: the builders only test `!= 0` and move
+    values, and an int64 is zero iff its bits are zero."""
+    return t.view(torch.float64) if t.dtype == torch.int64 else t
+
+
+def _coo_to_groupcoo(coo, group_dim, g, stream):
+    vals = coo.values
+    view = vals.view(torch.float64) if vals.dtype == torch.int64 else vals
+    gc = api.coo_to_groupcoo(coo.rows, coo.cols, coo.row, coo.col, view, group_dim, g,
+                             canonical=False, stream=stream)
+    if gc.AV is not None and gc.AV.dtype != vals.dtype:
+        gc.AV = gc.AV.view(vals.dtype)
+    return gc
