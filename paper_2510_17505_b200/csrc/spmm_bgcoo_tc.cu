@@ -48,14 +48,17 @@ struct TcArgs {
   int accumulate;
   int check;
   int epi_sleep_ns;  // epilogue warps back off instead of spinning on acc_full
-  int debug;         // perf experiments: 1 = skip UMMA issue, 2 = gather B tile 0 only
   ErrorRecord* err;
 };
 
-template <int NSUB, int STAGES>
+// A stage carries SPS consecutive slots of one row segment: SPS B tiles
+// (1024-aligned), then SPS AV blocks. One full/empty round trip and one
+// tcgen05.commit per 2*SPS UMMAs: commits interleaved with tiny MMA batches
+// roughly double the tensor pipe's per-MMA cost (profiles/k4_diag_r1.md).
+template <int NSUB, int STAGES, int SPS>
 struct TcSmem {
   static constexpr uint32_t kBBytes = NSUB * kSubBytes;
-  static constexpr uint32_t kStageBytes = ((kBBytes + kAvBytes + 1023) / 1024) * 1024;
+  static constexpr uint32_t kStageBytes = ((SPS * (kBBytes + kAvBytes) + 1023) / 1024) * 1024;
   static constexpr uint32_t kTileBytes = STAGES * kStageBytes;
   static constexpr uint32_t kTotal = kTileBytes + 1024 /*barriers+queue*/ + 1024 /*align*/;
 };
@@ -125,11 +128,11 @@ struct SegIter {
 
 constexpr int kQN = 16;  // segment queue depth (scheduler -> roles)
 
-template <int NSUB, int STAGES, int NACC>
+template <int NSUB, int STAGES, int NACC, int SPS>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     bgcoo_tc_kernel(const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmAV, TcArgs a) {
-  using L = TcSmem<NSUB, STAGES>;
+  using L = TcSmem<NSUB, STAGES, SPS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -240,16 +243,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int64_t i0 = s0; i0 < s1; i0 += 32) {
         const int k_next = load_k(i0 + 32);  // prefetch the next 32 member coords
         const int cnt = static_cast<int>(s1 - i0 < 32 ? s1 - i0 : 32);
-        for (int t = 0; t < cnt; ++t) {
-          const int kk = __shfl_sync(0xffffffffu, k, t);
+        for (int t = 0; t < cnt; t += SPS) {
+          const int nb = cnt - t < SPS ? cnt - t : SPS;
+          int kk[SPS];
+#pragma unroll
+          for (int b = 0; b < SPS; ++b) kk[b] = __shfl_sync(0xffffffffu, k, (t + b) & 31);
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* st = tiles + stage * L::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], L::kBBytes + kAvBytes);
-            // one 3-D box {64 n, 16 rows, 2*NSUB atoms} lands as [atom][row][64]
-            tma_load_3d(st, &tmB, &full[stage], 0, (a.debug & 2) ? 0 : kk * 16, n0 / 64, keep);
-            tma_load_2d(st + L::kBBytes, &tmAV, &full[stage], 0,
-                        static_cast<int32_t>((i0 + t) * 16), stream);
+            mbar_arrive_expect_tx(&full[stage], nb * (L::kBBytes + kAvBytes));
+#pragma unroll
+            for (int b = 0; b < SPS; ++b) {
+              if (b >= nb) break;
+              // one 3-D box {64 n, 16 rows, 2*NSUB atoms} lands as [atom][row][64]
+              tma_load_3d(st + b * L::kBBytes, &tmB, &full[stage], 0, kk[b] * 16, n0 / 64, keep);
+              tma_load_2d(st + SPS * L::kBBytes + b * kAvBytes, &tmAV, &full[stage], 0,
+                          static_cast<int32_t>((i0 + t + b) * 16), stream);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -275,25 +285,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
       tc_fence_after();
       const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
-      for (int64_t i = 0; i < nslots; ++i) {
-        if (lane == 0) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
-          const uint64_t bdesc = smem_desc(st + L::kBBytes, 16, 256, kLayoutSW32);
+      // same (32-slot chunk, SPS batch) partition as the producer
+      for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
+        const int cnt = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
+        for (int t = 0; t < cnt; t += SPS) {
+          const int nb = cnt - t < SPS ? cnt - t : SPS;
+          if (lane == 0) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
 #pragma unroll
-          for (int sub = 0; sub < NSUB; ++sub) {
-            // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
-            const uint64_t adesc = smem_desc(st + sub * kSubBytes, 2048, 1024, kLayoutSW128);
-            if (!(a.debug & 1))
-              umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc, i > 0 ? 1u : 0u);
+            for (int b = 0; b < SPS; ++b) {
+              if (b >= nb) break;
+              const uint64_t bdesc =
+                  smem_desc(st + SPS * L::kBBytes + b * kAvBytes, 16, 256, kLayoutSW32);
+#pragma unroll
+              for (int sub = 0; sub < NSUB; ++sub) {
+                // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
+                const uint64_t adesc =
+                    smem_desc(st + b * L::kBBytes + sub * kSubBytes, 2048, 1024, kLayoutSW128);
+                umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc,
+                         (i0 + t + b) > 0 ? 1u : 0u);
+              }
+            }
+            umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
+            if (i0 + t + nb == nslots) umma_commit(&acc_full[buf]);
           }
-          umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
-          if (i + 1 == nslots) umma_commit(&acc_full[buf]);
-        }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
       __syncwarp();
@@ -419,10 +440,10 @@ __global__ void bgcoo_simt_kernel(const int32_t* AM, const int32_t* AK,
 }
 
 // ------------------------------------------------------------ host side
-template <int NSUB, int STAGES, int NACC>
+template <int NSUB, int STAGES, int NACC, int SPS>
 void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaStream_t s) {
-  using L = TcSmem<NSUB, STAGES>;
-  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC>;
+  using L = TcSmem<NSUB, STAGES, SPS>;
+  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC, SPS>;
   static bool attr = false;
   if (!attr) {
     IXB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -503,26 +524,13 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
                                         CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tmAV = make_tmap_2d(AV, 16, G * g * 16, 32, 16, 16,
                                          CU_TENSOR_MAP_SWIZZLE_32B);
-    static const int variant = getenv("IXB_BG_VARIANT") ? atoi(getenv("IXB_BG_VARIANT")) : 0;
     static const int sleep_ns = getenv("IXB_BG_SLEEP") ? atoi(getenv("IXB_BG_SLEEP")) : 256;
     a.epi_sleep_ns = sleep_ns;
-    static const int debug = getenv("IXB_BG_DEBUG") ? atoi(getenv("IXB_BG_DEBUG")) : 0;
-    a.debug = debug;
-    if (nsub == 1) {
-      launch_tc<1, 12, 4>(tmB, tmAV, a, s);
-    } else if (variant == 1) {
-      launch_tc<2, 6, 2>(tmB, tmAV, a, s);
-    } else if (variant == 2) {
-      launch_tc<2, 6, 4>(tmB, tmAV, a, s);
-    } else if (variant == 3) {
-      launch_tc<2, 10, 4>(tmB, tmAV, a, s);
-    } else if (variant == 4) {
-      launch_tc<2, 4, 4>(tmB, tmAV, a, s);
-    } else if (variant == 5) {
-      launch_tc<2, 16, 4>(tmB, tmAV, a, s);
-    } else {
-      launch_tc<2, 6, 4>(tmB, tmAV, a, s);
-    }
+    // 2 slots per stage, 4 stages: ~68 KB -> 3 CTAs (3 independent issue
+    // streams) per SM; measured against 1, 4, 8, 12 slots per stage and
+    // 2-4 CTAs/SM on cfg2 (profiles/k4_diag_r1.md)
+    if (nsub == 1) launch_tc<1, 8, 4, 2>(tmB, tmAV, a, s);
+    else launch_tc<2, 4, 4, 2>(tmB, tmAV, a, s);
   } else {
     const int threads = 256;
     bgcoo_simt_kernel<<<static_cast<unsigned>(G), threads, 0, s>>>(
