@@ -128,8 +128,8 @@ struct SegIter {
 
 constexpr int kQN = 16;  // segment queue depth (scheduler -> roles)
 
-template <int NSUB, int STAGES, int NACC, int SPS>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+template <int NSUB, int STAGES, int NACC, int SPS, int MINB = 1>
+__global__ void __launch_bounds__(kThreadsTC, MINB)
     bgcoo_tc_kernel(const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmAV, TcArgs a) {
   using L = TcSmem<NSUB, STAGES, SPS>;
@@ -440,20 +440,26 @@ __global__ void bgcoo_simt_kernel(const int32_t* AM, const int32_t* AK,
 }
 
 // ------------------------------------------------------------ host side
-template <int NSUB, int STAGES, int NACC, int SPS>
+template <int NSUB, int STAGES, int NACC, int SPS, int MINB = 1>
 void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaStream_t s) {
   using L = TcSmem<NSUB, STAGES, SPS>;
-  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC, SPS>;
-  static bool attr = false;
-  if (!attr) {
+  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC, SPS, MINB>;
+  static int per_sm = 0;  // resident CTAs per SM (registers, smem and TMEM columns)
+  if (!per_sm) {
     IXB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         L::kTotal));
-    attr = true;
+    cudaFuncAttributes fa;
+    IXB_CUDA_CHECK(cudaFuncGetAttributes(&fa, kern));
+    const int by_regs = 65536 / (((fa.numRegs * 32 + 255) / 256) * 256 * (kThreadsTC / 32));
+    per_sm = static_cast<int>((220u * 1024u) / L::kTotal);
+    if (per_sm > by_regs) per_sm = by_regs;
+    constexpr int kCols = NACC * 16 * NSUB <= 32 ? 32 : NACC * 16 * NSUB <= 64 ? 64
+                          : NACC * 16 * NSUB <= 128 ? 128 : NACC * 16 * NSUB <= 256 ? 256 : 512;
+    if (per_sm > 512 / kCols) per_sm = 512 / kCols;  // a CTA must not wait in tcgen05.alloc
+    if (per_sm < 1) per_sm = 1;
   }
   a.ntiles = static_cast<int>(a.N / (128 * NSUB));
   const int64_t items = static_cast<int64_t>(a.nchunks) * a.ntiles;
-  int per_sm = static_cast<int>((220u * 1024u) / L::kTotal);
-  if (per_sm < 1) per_sm = 1;
   int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // persistent CTAs
   if (grid > items) grid = items;
   kern<<<static_cast<unsigned>(grid), kThreadsTC, L::kTotal, s>>>(tmB, tmAV, a);
@@ -528,7 +534,7 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     a.epi_sleep_ns = sleep_ns;
     // 2 slots per stage, 4 stages: ~68 KB -> 3 CTAs (3 independent issue
     // streams) per SM; measured against 1, 4, 8, 12 slots per stage and
-    // 2-4 CTAs/SM on cfg2 (profiles/k4_diag_r1.md)
+    // 1-5 CTAs/SM on cfg2 (profiles/k4_diag_r1.md)
     if (nsub == 1) launch_tc<1, 8, 4, 2>(tmB, tmAV, a, s);
     else launch_tc<2, 4, 4, 2>(tmB, tmAV, a, s);
   } else {
