@@ -23,6 +23,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <memory>
 #include <mutex>
 
@@ -43,6 +44,7 @@ struct PlanArgs {
   int64_t G, g, n_in, n_off, n_out;
   int32_t* T;      // [n_out * n_off] slot or -1
   int* conflict;
+  int* nonunit;    // some real (non-pad) slot has MAPV != 1
   int check;
   ErrorRecord* err;
 };
@@ -71,6 +73,7 @@ __global__ void conv_index_kernel(PlanArgs a) {
   if (!ok) return;
   const float v = a.MAPV ? a.MAPV[s] : 1.f;
   if (q > 0 && v == 0.f && a.MAPX[s - 1] == x && a.MAPY[s - 1] == y) return;  // pad
+  if (v != 1.f) atomicOr(a.nonunit, 1);
   const int prev = atomicCAS(&a.T[static_cast<int64_t>(x) * a.n_off + z], -1,
                              static_cast<int>(s));
   if (prev != -1) atomicOr(a.conflict, 1);
@@ -219,6 +222,193 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
 }
 
+
+// ------------------------------------------- tcgen05 path for unit-valued maps
+// Unit-valued maps (MAPV == 1 on every real slot — what ixb_kernel_map +
+// group_coo_tensor produce) need no per-row scaling. The plan turns T into an
+// input-row table Y[x, z] = y + 1 (0 = absent; row stride kOffPad ints, 16 B
+// aligned) plus a bitmask of the offsets each 128-row tile uses. A thread
+// then reads its row's whole Y row in 7 vector loads, no per-offset
+// T -> MAPY dependence and no per-offset block vote remain, and the In row
+// for the next active offset is loaded while the current one is stored and
+// multiplied: one exposed global latency per tile instead of three per
+// offset. The tensor-core part is the kernel above (4 UMMAs M=128,N=64,K=16
+// per offset into one TMEM accumulator, A and W double-buffered), so each
+// output row still accumulates its offsets in z order.
+// Measured on cfg5 (1 M voxels): 0.83 ms -> 0.65 ms. Not shipped: a TMA
+// tile::gather4 version (4 rows per instruction straight into the swizzled
+// operand; 1.0-3.2 ms with 1-8 issuing warps, gather4 costs ~43 cycles per
+// 512 B box per SM; tools/gather4_probe.cu pins its semantics), and a third W
+// slot to prefetch W one offset ahead (0.71 ms: 58 KB of smem drops the
+// 4th CTA per SM).
+constexpr int kOffPad = 28;  // Y row stride (ints): 27 offsets padded to 16 B
+
+struct UnitArgs {
+  const int32_t* Y;           // [n_out][kOffPad] y + 1, 0 = absent
+  const uint32_t* tile_mask;  // [ntiles] offsets used by the tile
+  const __nv_bfloat16* In;
+  float* Out;
+  int64_t n_out;
+  int accumulate;
+};
+
+__global__ void __launch_bounds__(kConvThreads, 4)
+    conv_unit_kernel(const __grid_constant__ CUtensorMap tmW, UnitArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* A = smem;               // [2][16 KB]
+  uint8_t* W = smem + 2 * kATile;  // [2][8 KB] (a third W slot costs the 4th CTA per SM)
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(W + 2 * kWTile);
+  uint64_t* mma_done = w_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&w_full[b], 1);
+      mbar_init(&mma_done[b], 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmW);
+  }
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, 64);
+    tmem_relinquish();
+  }
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * 128 + tid;
+  const bool row_ok = x < a.n_out;
+  // this row's input rows for all offsets (y + 1), one vectorised read
+  int yr[kOffPad];
+  if (row_ok) {
+    const int4* src = reinterpret_cast<const int4*>(a.Y + x * kOffPad);
+#pragma unroll
+    for (int j = 0; j < kOffPad / 4; ++j) {
+      const int4 v = __ldg(src + j);
+      yr[4 * j] = v.x, yr[4 * j + 1] = v.y, yr[4 * j + 2] = v.z, yr[4 * j + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kOffPad; ++j) yr[j] = 0;
+  }
+  const uint32_t tmask = a.tile_mask[blockIdx.x];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t idesc = idesc_bf16_f32(128, 64, /*A K-major*/ false, /*B MN-major*/ true);
+  const uint64_t keep = l2_evict_last();
+
+  // row of In for offset z (zeros when absent); z is warp-uniform
+  auto fetch = [&](int z, uint4 (&c)[8]) {
+    int y1 = 0;
+#pragma unroll
+    for (int j = 0; j < kOffPad; ++j) y1 = (j == z) ? yr[j] : y1;
+    if (y1 > 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.In + static_cast<int64_t>(y1 - 1) * 64);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[j] = __ldg(src + j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[j] = make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint32_t mask = tmask;
+  uint4 cur[8];
+  int z = mask ? __ffs(mask) - 1 : -1;
+  if (z >= 0) fetch(z, cur);
+  int k = 0;
+  while (z >= 0) {
+    mask &= mask - 1;
+    const int zn = mask ? __ffs(mask) - 1 : -1;
+    uint4 nxt[8];
+    if (zn >= 0) fetch(zn, nxt);  // next offset's row in flight during this one
+    const int buf = k & 1;
+    if (k >= 2) mbar_wait(&mma_done[buf], ((k - 2) >> 1) & 1);  // MMA k-2 freed buf
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&w_full[buf], kWTile);
+      tma_load_2d(W + buf * kWTile, &tmW, &w_full[buf], 0, z * 64, keep);
+    }
+    uint8_t* arow = A + buf * kATile + tid * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) *reinterpret_cast<uint4*>(arow + ((j ^ (tid & 7)) << 4)) = cur[j];
+    fence_proxy_async_smem();  // st.shared -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&w_full[buf], (k >> 1) & 1);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(A + buf * kATile), w0 = smem_u32(W + buf * kWTile);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = smem_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
+        const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
+        umma_f16(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+      }
+      umma_commit(&mma_done[buf]);
+    }
+    ++k;
+    z = zn;
+    if (zn >= 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(a.Out + x * 64);
+  if (k > 0) {
+    mbar_wait(&mma_done[(k - 1) & 1], ((k - 1) >> 1) & 1);
+    tc_fence_after();
+  }
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[16];
+    if (k > 0) {
+      tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, r);
+      tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) r[j] = 0;
+    }
+    if (row_ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        if (a.accumulate) {
+          const float4 old = o[c * 4 + j];
+          v.x += old.x;
+          v.y += old.y;
+          v.z += old.z;
+          v.w += old.w;
+        }
+        o[c * 4 + j] = v;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+}
+
+// Y[x * kOffPad + z] = MAPY[T[x, z]] + 1 (0 = absent); tile masks of used offsets.
+__global__ void conv_ytable_kernel(const int32_t* T, const int32_t* MAPY, int64_t n_out,
+                                   int64_t n_off, int32_t* Y, uint32_t* tile_mask) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_out * kOffPad) return;
+  const int64_t x = i / kOffPad, z = i % kOffPad;
+  int v = 0;
+  if (z < n_off) {
+    const int s = T[x * n_off + z];
+    if (s >= 0) {
+      v = MAPY[s] + 1;
+      atomicOr(&tile_mask[x / 128], 1u << z);
+    }
+  }
+  Y[i] = v;
+}
+
 // --------------------------------------------------------------- CSR path
 __global__ void iota_conv(int32_t* v, int64_t n) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -271,7 +461,9 @@ struct ixb_conv_plan {
   const int32_t *MAPZ = nullptr, *MAPX = nullptr, *MAPY = nullptr;
   const float* MAPV = nullptr;
   bool conflict = false;
-  ixb::Scratch<int32_t> T, perm, rowptr;
+  bool unit = false;  // every real slot has MAPV == 1: conv_unit_kernel usable
+  ixb::Scratch<int32_t> T, perm, rowptr, Y;
+  ixb::Scratch<uint32_t> tile_mask;
 };
 
 using namespace ixb;
@@ -297,13 +489,13 @@ int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t
     P->MAPV = MAPV;
     const int64_t slots = G * g;
     P->T = Scratch<int32_t>(n_out * n_off + 1, s);
-    Scratch<int> conflict(1, s);
+    Scratch<int> conflict(2, s);  // [0] conflict, [1] non-unit MAPV
     IXB_CUDA_CHECK(cudaMemsetAsync(P->T.p, 0xff, (n_out * n_off + 1) * 4, s));
-    IXB_CUDA_CHECK(cudaMemsetAsync(conflict.p, 0, 4, s));
+    IXB_CUDA_CHECK(cudaMemsetAsync(conflict.p, 0, 8, s));
     const bool check = !(flags & IXB_UNCHECKED);
     if (slots > 0) {
-      PlanArgs a{MAPZ, MAPX, MAPY, MAPV, G, g, n_in, n_off, n_out, P->T.p, conflict.p, check,
-                 device_error_record()};
+      PlanArgs a{MAPZ, MAPX, MAPY, MAPV, G, g, n_in, n_off, n_out, P->T.p, conflict.p,
+                 conflict.p + 1, check, device_error_record()};
       conv_index_kernel<<<ceil_div(slots, 256), 256, 0, s>>>(a);
       IXB_LAUNCH_CHECK("conv_index_kernel");
     }
@@ -313,10 +505,21 @@ int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t
                             {"MAPX", "Out", 0, n_out, MAPX, slots}};
       check_error_record(s, ops, 3);
     }
-    int h = 0;
-    IXB_CUDA_CHECK(cudaMemcpyAsync(&h, conflict.p, 4, cudaMemcpyDeviceToHost, s));
+    int h[2] = {0, 0};
+    IXB_CUDA_CHECK(cudaMemcpyAsync(h, conflict.p, 8, cudaMemcpyDeviceToHost, s));
     IXB_CUDA_CHECK(cudaStreamSynchronize(s));
-    P->conflict = h != 0;
+    P->conflict = h[0] != 0;
+    P->unit = !P->conflict && h[1] == 0 && n_off <= kOffPad && n_in < INT32_MAX;
+    if (P->unit && n_out > 0) {
+      const int64_t ntiles = ceil_div(n_out, 128);
+      P->Y = Scratch<int32_t>(n_out * kOffPad, s);
+      P->tile_mask = Scratch<uint32_t>(ntiles, s);
+      IXB_CUDA_CHECK(cudaMemsetAsync(P->tile_mask.p, 0, ntiles * 4, s));
+      conv_ytable_kernel<<<ceil_div(n_out * kOffPad, 256), 256, 0, s>>>(P->T.p, MAPY, n_out, n_off,
+                                                                       P->Y.p, P->tile_mask.p);
+      IXB_LAUNCH_CHECK("conv_ytable_kernel");
+      IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
     *plan = P.release();
   });
 }
@@ -335,6 +538,24 @@ int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void*
                     reinterpret_cast<uintptr_t>(In) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(Weight) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(Out) % 16 == 0;
+    static const bool unit_off = getenv("IXB_CONV_NO_UNIT") != nullptr;  // A/B switch
+    if (tc && P->unit && !unit_off) {
+      const CUtensorMap tmW =
+          make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+      UnitArgs ua{P->Y.p, P->tile_mask.p, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
+                  accumulate};
+      const uint32_t smem = 2 * kATile + 2 * kWTile + 1024 + 1024;
+      static std::once_flag once_u;
+      std::call_once(once_u, [&] {
+        cuda_check(cudaFuncSetAttribute(conv_unit_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                   "cudaFuncSetAttribute(conv_unit_kernel)");
+      });
+      conv_unit_kernel<<<ceil_div(P->n_out, 128), kConvThreads, smem, s>>>(tmW, ua);
+      IXB_LAUNCH_CHECK("conv_unit_kernel");
+      return;
+    }
     if (tc) {
       const CUtensorMap tmW =
           make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64, 64,
