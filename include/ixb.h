@@ -231,6 +231,21 @@ int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, const void*
                     float* Z, int accumulate, int flags, ixb_stream stream);
 void ixb_tp_plan_free(ixb_tp_plan* plan);
 
+/* Host-buffer forms of the SpMM evaluators (the shape of the reference's
+ * execute_mode: host Tensors in, host result out). All arrays are HOST
+ * memory (pinned for full overlap); the call returns with C written. The
+ * groups are cut into `nchunks` ranges at output-row boundaries: B is copied
+ * first, then chunk i's format H2D, its kernel and its C rows D2H run on
+ * three streams, so transfers overlap each other and the kernels. Results
+ * and errors are bit-identical to the device-buffer calls. */
+int ixb_spmm_blockgroupcoo_host(const int32_t* AM, const int32_t* AK, const void* AV, int64_t G,
+                                int64_t g, int64_t bm, int64_t bk, const void* B, int64_t KB,
+                                int64_t N, float* C, int64_t MB, int accumulate, int flags,
+                                int nchunks, ixb_stream stream);
+int ixb_spmm_groupcoo_host(const int32_t* AM, const int32_t* AK, const float* AV, int64_t G,
+                           int64_t g, const float* B, int64_t K, int64_t N, float* C, int64_t M,
+                           int accumulate, int flags, int nchunks, ixb_stream stream);
+
 /* ======================================================================
  * On-disk formats straight to/from the device.
  * ==================================================================== */

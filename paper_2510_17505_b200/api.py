@@ -307,6 +307,39 @@ def tp_grouped(CGL, CGI, CGJ, CGK, CGV, X, Y, W, Z, accumulate=True, flags=0, st
     return Z
 
 
+def _host(t, dtype=None):
+    if t.is_cuda:
+        raise ShapeError(4, "host-buffer calls take CPU tensors (pinned for full overlap)")
+    if dtype is not None and t.dtype != dtype:
+        raise ShapeError(4, f"expected {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def spmm_groupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=2, stream=None):
+    """K3 with HOST buffers in and out (execute_mode's shape, driver.cpp:235-265):
+    row-boundary chunks pipeline H2D, kernel and D2H on three streams; returns
+    with C_out written. Bit-identical to spmm_groupcoo."""
+    AM, AK, AV, B = _host(AM, torch.int32), _host(AK, torch.int32), _host(AV), _host(B)
+    AV2 = AV if AV.dim() == 2 else AV.reshape(-1, 1)
+    G, g = AV2.shape
+    check(lib().ixb_spmm_groupcoo_host(_ptr(AM), _ptr(AK), _ptr(AV2), G, g, _ptr(B), B.shape[0],
+                                       B.shape[1], _ptr(_host(C_out)), C_out.shape[0],
+                                       int(accumulate), flags, nchunks, _stream(stream)))
+    return C_out
+
+
+def spmm_blockgroupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=2,
+                            stream=None):
+    """K4 with HOST buffers in and out (see spmm_groupcoo_host)."""
+    AM, AK, AV, B = _host(AM, torch.int32), _host(AK, torch.int32), _host(AV), _host(B)
+    G, g, bm, bk = AV.shape
+    check(lib().ixb_spmm_blockgroupcoo_host(_ptr(AM), _ptr(AK), _ptr(AV), G, g, bm, bk, _ptr(B),
+                                            B.shape[0], B.shape[2], _ptr(_host(C_out)),
+                                            C_out.shape[0], int(accumulate), flags, nchunks,
+                                            _stream(stream)))
+    return C_out
+
+
 class TpPlan:
     """Inspector/executor form of K7: validates a grouped CG table and
     reshapes it (tensor-core job table / CUDA-core slot lists) once;

@@ -85,7 +85,20 @@ void check_error_record(cudaStream_t stream, const OperandInfo* ops, int nops) {
                             o.target_name + " (extent " + std::to_string(o.extent) + ")");
 }
 
+// Stream-ordered scratch from the device's default memory pool. The pool
+// keeps freed memory mapped (release threshold = max) so repeated calls do
+// not unmap and remap their temporaries at every synchronisation.
 void* scratch_alloc(size_t bytes, cudaStream_t stream) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  IXB_CUDA_CHECK(cudaGetDevice(&dev));
+  if (configured != dev) {
+    cudaMemPool_t pool;
+    IXB_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    IXB_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured = dev;
+  }
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
   IXB_CUDA_CHECK(cudaMallocAsync(&p, bytes, stream));

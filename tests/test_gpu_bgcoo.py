@@ -141,8 +141,8 @@ def test_tcgen05_long_rows_many_stages(P, ixo):
 
 
 def test_tcgen05_mixed_long_and_short_rows(P, ixo):
-    """Rows over the column-merge capacity (> 256 slots) keep slot order and
-    share a row-block (and its TMEM accumulators) with column-merged rows."""
+    """Long block-rows (> 256 slots, many pipeline stages and segment
+    queue entries) next to short and empty ones."""
     rng = ixo.Rng(21)
     a = ixo.synth_block_sparse_matrix(rng, 80, 6720, 16, 16, 0.7, 1)
     b = ixo.synth_dense(rng, (420, 16, 128), 1)
@@ -155,11 +155,12 @@ def test_tcgen05_mixed_long_and_short_rows(P, ixo):
     got = run(P, t, np.zeros((5, 16, 128)), flags=2)
     np.testing.assert_array_equal(got.astype(np.int64).reshape(80, 128), ref)
     rows = np.bincount(t["AM"], minlength=5) * t["AK"].shape[1]
-    assert rows.max() > 256  # the slot-order path ran
+    assert rows.max() > 256
 
 
 def test_tcgen05_more_items_than_sms(P, ixo):
-    """Many row-blocks x n tiles: persistent CTAs cycle both TMEM sets."""
+    """Far more work items than persistent CTAs: every CTA cycles its TMEM
+    accumulator buffers many times."""
     t, a, b = make16(ixo, 31, 3000, 12, 256, 0.2, 2)
     ref = (a.reshape(48000, 192).astype(np.int64) @ b.reshape(192, 256).astype(np.int64))
     got = run(P, t, np.zeros((3000, 16, 256)), accumulate=False, flags=2)
@@ -168,7 +169,7 @@ def test_tcgen05_more_items_than_sms(P, ixo):
 
 def test_tcgen05_deterministic_and_row_block_invariant(P, ixo):
     """Real values: repeated runs are bit-identical, and evaluating a row
-    slab alone (different row-block height R) gives the same bits."""
+    slab alone (a different chunk / work split) gives the same bits."""
     t, a, b = make16(ixo, 41, 64, 40, 512, 0.3, 4, kind=0)
     full1 = run(P, t, np.zeros((64, 16, 512)), flags=2)
     full2 = run(P, t, np.zeros((64, 16, 512)), flags=2)
@@ -234,3 +235,50 @@ def test_cfg2_full_size_slab_vs_oracle(P, ixo):
     got = C.double().sum(dim=2).cpu()
     rel = ((got - ref).abs() / torch.maximum(ref.abs(), torch.ones_like(ref))).max().item()
     assert rel <= 1e-3
+
+
+@pytest.mark.parametrize("nchunks", [1, 3, 8])
+def test_host_buffer_pipeline_bit_identical(P, ixo, nchunks):
+    """ixb_spmm_blockgroupcoo_host (host buffers, chunked H2D/kernel/D2H on
+    three streams) equals the device-buffer call bit for bit, for `=` and
+    `+=`, and reports index errors with the same message."""
+    t, a, b = make16(ixo, 51, 40, 30, 256, 0.3, 4, kind=0, empty_rows=(0, 7, 39))
+    AM = torch.from_numpy(t["AM"]).int()
+    AK = torch.from_numpy(t["AK"]).int()
+    AV, B = bf16(t["AV"]), bf16(t["B"])
+    ref = torch.zeros((40, 16, 256), device="cuda")
+    P.spmm_blockgroupcoo(AM.cuda(), AK.cuda(), AV.cuda(), B.cuda(), ref, accumulate=False)
+    out = torch.full((40, 16, 256), 7.0).pin_memory()
+    P.spmm_blockgroupcoo_host(AM.pin_memory(), AK.pin_memory(), AV.pin_memory(), B.pin_memory(),
+                              out, accumulate=False, nchunks=nchunks)
+    assert torch.equal(out, ref.cpu())
+    primed = torch.randn(40, 16, 256)
+    out = primed.clone().pin_memory()
+    P.spmm_blockgroupcoo_host(AM, AK, AV, B, out, accumulate=True, nchunks=nchunks)
+    ref2 = primed.cuda()
+    P.spmm_blockgroupcoo(AM.cuda(), AK.cuda(), AV.cuda(), B.cuda(), ref2, accumulate=True)
+    assert torch.equal(out, ref2.cpu())
+    bad = AK.clone()
+    bad.view(-1)[5] = 30
+    with pytest.raises(P.IndexRangeError) as e:
+        P.spmm_blockgroupcoo_host(AM, bad, AV, B, out, accumulate=False, nchunks=nchunks)
+    assert str(e.value) == ("index tensor AK value 30 at position [5] out of range for dim 0 "
+                            "of B (extent 30)")
+
+
+def test_host_buffer_pipeline_groupcoo_and_unsorted(P, ixo):
+    rng = ixo.Rng(8)
+    A = ixo.synth_sparse_matrix(rng, 300, 200, 0.05, 1)
+    Bn = ixo.synth_dense(rng, (200, 64), 1)
+    f = ixo.coo_to_groupcoo(300, 200, *ixo.dense_to_coo(A), 0, 4)
+    AM, AK = torch.from_numpy(f["AM"]).int(), torch.from_numpy(f["AK"]).int()
+    AV, B = torch.from_numpy(f["AV"]).float(), torch.from_numpy(Bn).float()
+    want = torch.from_numpy(A.astype(np.float32) @ Bn.astype(np.float32))
+    for nch in (1, 5):
+        out = torch.empty(300, 64)
+        P.spmm_groupcoo_host(AM, AK, AV, B, out, accumulate=False, nchunks=nch)
+        assert torch.equal(out, want)
+    perm = torch.from_numpy(np.random.default_rng(2).permutation(AM.numel()))
+    out = torch.empty(300, 64)
+    P.spmm_groupcoo_host(AM[perm], AK[perm], AV[perm], B, out, accumulate=False, nchunks=4)
+    assert torch.equal(out, want)
