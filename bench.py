@@ -205,6 +205,26 @@ class GroupCooWorkload:
     def roofline_bound(self):
         return "hbm"
 
+    # --sharded (strong scaling): row-group shards of ONE matrix
+    def shard(self, torch, P, dev, rank, ws):
+        from paper_2510_17505_b200 import distributed as D
+        sh = D.shard_plan(self.fmt.AM.cpu().numpy(), self.M, ws)
+        self.sh = sh[rank]
+        s = self.sh
+        self.sg = D.SlabGather(sh, rank, (self.N,), torch.float32, dev)
+        loc = [self.fmt.AM[s.g0:s.g1], self.fmt.AK[s.g0:s.g1], self.fmt.AV[s.g0:s.g1], self.B]
+        self.sh_h_in = [x.cpu().pin_memory() for x in loc]
+        self.sh_d_in = [x.clone() for x in loc]
+        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
+        return {"rows_owned": s.r1 - s.r0, "groups_owned": s.g1 - s.g0}
+
+    def sharded_step(self, P):
+        from paper_2510_17505_b200 import distributed as D
+        AM, AK, AV, B = self.sh_d_in
+        self.sg.local.zero_()
+        D.spmm_groupcoo_into(AM, AK, AV, self.g, B, self.sh, self.sg.local, flags=1 | 2)
+        return self.sg()
+
     # reference CPU path on a bounded slab of the same matrix
     def cpu_sample(self, ref, budget_rows=None):
         # ~40M reference iteration points (G*g*N), ~1-2 s per reference run
@@ -283,6 +303,25 @@ class BlockGroupCooWorkload:
 
     def roofline_bound(self):
         return "tensor"
+
+    def shard(self, torch, P, dev, rank, ws):
+        from paper_2510_17505_b200 import distributed as D
+        sh = D.shard_plan(self.fmt.AM.cpu().numpy(), self.M // self.b, ws)
+        self.sh = sh[rank]
+        s = self.sh
+        self.sg = D.SlabGather(sh, rank, (self.b, self.N), torch.float32, dev)
+        loc = [self.fmt.AM[s.g0:s.g1], self.fmt.AK[s.g0:s.g1], self.fmt.AV[s.g0:s.g1], self.B]
+        self.sh_h_in = [x.cpu().pin_memory() for x in loc]
+        self.sh_d_in = [x.clone() for x in loc]
+        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
+        return {"block_rows_owned": s.r1 - s.r0, "groups_owned": s.g1 - s.g0}
+
+    def sharded_step(self, P):
+        from paper_2510_17505_b200 import distributed as D
+        AM, AK, AV, B = self.sh_d_in
+        self.sg.local.zero_()
+        D.spmm_blockgroupcoo_into(AM, AK, AV, B, self.sh, self.sg.local, flags=1 | 2)
+        return self.sg()
 
     def cpu_sample(self, ref, budget_rows=None):
         import numpy as np
@@ -368,6 +407,24 @@ class TensorProductWorkload:
     def units_total(self):
         return self.batch
 
+    def shard(self, torch, P, dev, rank, ws):
+        from paper_2510_17505_b200 import distributed as D
+        sh = D.edge_blocks(self.batch, ws)
+        self.sh = sh[rank]
+        s = self.sh
+        self.sg = D.SlabGather(sh, rank, (16, 64), torch.float32, dev)
+        loc = [self.X[s.r0:s.r1], self.Y[s.r0:s.r1]]
+        self.sh_h_in = [x.cpu().pin_memory() for x in loc]
+        self.sh_d_in = [x.clone() for x in loc]
+        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
+        return {"edges_owned": s.r1 - s.r0}
+
+    def sharded_step(self, P):
+        if self.sh.r1 > self.sh.r0:
+            self.plan.run(self.sh_d_in[0], self.sh_d_in[1], self.W, self.sg.local,
+                          accumulate=False)
+        return self.sg()
+
     def cpu_sample(self, ref, budget_rows=None):
         import numpy as np
         from paper_2510_17505_b200 import synth as S
@@ -416,6 +473,7 @@ class SparseConvWorkload:
         gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], ones, 2, g, canonical=True)
         torch.cuda.synchronize()
         t1 = _t.perf_counter()
+        self.map, self.g = (mo, mi, mz), g
         self.MAPZ, (self.MAPX, self.MAPY), self.MAPV = gt.group_coord, gt.member_coords, gt.values
         self.plan = P.ConvPlan(self.MAPZ, self.MAPX, self.MAPY, self.MAPV, n, 27, n)
         torch.cuda.synchronize()
@@ -452,6 +510,30 @@ class SparseConvWorkload:
 
     def units_total(self):
         return getattr(self, "pairs_total", 9.12 * self.voxels)
+
+    def shard(self, torch, P, dev, rank, ws):
+        # point blocks: the map keeps only pairs whose output voxel is in the block
+        import time as _t
+        from paper_2510_17505_b200 import distributed as D
+        n = self.In.shape[0]
+        sh = D.point_blocks(n, ws)
+        self.sh = sh[rank]
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        self.sh_plan = D.conv_shard_plan(*self.map, n, self.sh, self.g)
+        torch.cuda.synchronize()
+        self.sg = D.SlabGather(sh, rank, (64,), torch.float32, dev)
+        self.sh_h_in = [self.In.cpu().pin_memory()]  # In is replicated
+        self.sh_d_in = [self.In.clone()]
+        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
+        return {"voxels_owned": self.sh.r1 - self.sh.r0,
+                "pairs_owned": int(self.sh_plan.keep_map.mask.sum().item()),
+                "shard_plan_ms": (_t.perf_counter() - t0) * 1e3}
+
+    def sharded_step(self, P):
+        if self.sh.r1 > self.sh.r0:
+            self.sh_plan.run(self.sh_d_in[0], self.Wt, self.sg.local, accumulate=False)
+        return self.sg()
 
     def cpu_sample(self, ref, budget_rows=None):
         import numpy as np
@@ -554,20 +636,56 @@ def run_b200(args, wl):
     from paper_2510_17505_b200 import synth as S
 
     ws, rank, local = dist_env()
+    # IXB_DIST_BACKEND=gloo lets several ranks share one GPU: a functional
+    # check of the sharded path on a 1-GPU box, never a timing
+    backend = os.environ.get("IXB_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     P.lib()
-    # weak scaling: every rank evaluates its own independent instance of the
-    # per-GPU workload (seed + rank); no data-path collective.
-    wl.setup(torch, P, S, dev, wl.seed + rank)
+    if args.sharded:
+        # strong scaling: every rank holds the SAME instance,
+        # evaluates its row / point-block / edge shard into its output slab,
+        # and the slabs are all-gathered over NCCL inside the timed step.
+        wl.setup(torch, P, S, dev, wl.seed)
+        shard_info = wl.shard(torch, P, dev, rank, ws)
+
+        def step():
+            wl.sharded_step(P)
+
+        def e2e_step():
+            for d, h in zip(wl.sh_d_in, wl.sh_h_in):
+                d.copy_(h, non_blocking=True)
+            wl.sh_h_out.copy_(wl.sharded_step(P), non_blocking=True)
+
+        def e2e_bytes():
+            return sum(x.numel() * x.element_size() for x in wl.sh_h_in), \
+                wl.sh_h_out.numel() * wl.sh_h_out.element_size()
+    else:
+        # weak scaling: every rank evaluates its own independent instance of the
+        # per-GPU workload (seed + rank); no data-path collective.
+        wl.setup(torch, P, S, dev, wl.seed + rank)
+        shard_info = None
+
+        def step():
+            wl.step(P)
+
+        def e2e_step():
+            wl.e2e_step(P)
+
+        e2e_bytes = wl.e2e_bytes
+    jobs = 1 if args.sharded else ws  # instances processed per step, whole job
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
     for _ in range(args.warmup):
         flush.zero_()
-        wl.step(P)
+        step()
     torch.cuda.synchronize()
     P.lib().ixb_check_errors(None)
 
@@ -583,7 +701,7 @@ def run_b200(args, wl):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        wl.step(P)
+        step()
         b.record(stream)
         evs.append((a, b))
     torch.cuda.synchronize()
@@ -601,11 +719,11 @@ def run_b200(args, wl):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = t.item()
     ms = total_ms / args.steps
-    value = wl.flops * ws / (ms * 1e-3) / 1e9
+    value = wl.flops * jobs / (ms * 1e-3) / 1e9
 
     # e2e through the public API with pinned host buffers
     for _ in range(2):
-        wl.e2e_step(P)
+        e2e_step()
     torch.cuda.synchronize()
     e_evs = []
     for _ in range(max(3, min(args.steps, 20))):
@@ -613,7 +731,7 @@ def run_b200(args, wl):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        wl.e2e_step(P)
+        e2e_step()
         b.record(stream)
         e_evs.append((a, b))
     torch.cuda.synchronize()
@@ -622,10 +740,10 @@ def run_b200(args, wl):
     if ws > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e_ms = et.item()
-    h2d, d2h = wl.e2e_bytes()
+    h2d, d2h = e2e_bytes()
 
     hbm, tc, tc_sus, peak_src = load_peaks()
-    kern_s = ms * 1e-3
+    kern_s = ms * 1e-3 * (ws if args.sharded else 1)  # per-GPU share of a sharded job
     if wl.roofline_bound() == "hbm":
         achieved = wl.alg_bytes / kern_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -653,18 +771,25 @@ def run_b200(args, wl):
     line = {"metric": metric, "value": ms if timelike else value,
             "unit": "ms" if timelike else "GFLOP/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": not timelike, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": not timelike,
+            "scaling": "strong" if args.sharded else "weak", "vs_baseline": None,
             "dtype": "bf16" if wl.roofline_bound() == "tensor" or timelike else "f32",
             "data": "synthetic (reference synth streams, seed 1 + rank)",
             "config": dict(wl.config(), l2="flushed between steps (256 MiB memset outside the "
-                                         "timed events)", parallelism=f"weak x{ws}", **wl.info),
+                                         "timed events)",
+                           parallelism=(f"sharded x{ws} + {backend if ws > 1 else 'no'} all-gather of output slabs"
+                                        if args.sharded else f"weak x{ws}"), **wl.info),
             "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
-            "e2e": {"value": e_ms if timelike else wl.flops * ws / (e_ms * 1e-3) / 1e9,
+            "e2e": {"value": e_ms if timelike else wl.flops * jobs / (e_ms * 1e-3) / 1e9,
                     "unit": "ms" if timelike else "GFLOP/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e_ms}}
     if timelike:
         line["config"]["useful_GFLOPs"] = value
+    if shard_info is not None:
+        line["config"]["shard_rank0"] = shard_info
+    if ws > 1:
+        line["config"]["dist_backend"] = backend
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference_time(wl)
@@ -686,6 +811,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="strong scaling: shard ONE instance across the ranks (row groups, "
+                         "point blocks or edges) and all-gather the output inside the step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]()

@@ -63,6 +63,34 @@ def gather_rows(local, shards, rank, group=None):
     return out.reshape((rows,) + tail)
 
 
+class SlabGather:
+    """Preallocated form of gather_rows for repeated steps: the rank writes
+    its slab straight into `local` (a view of the padded send buffer), and
+    __call__ runs one all_gather_into_tensor plus one index_select that drops
+    the padding into `out` (the full output, identical on every rank)."""
+
+    def __init__(self, shards, rank, tail, dtype, device, group=None):
+        self.group, self.world = group, len(shards)
+        self.maxrows = max(max(s.r1 - s.r0 for s in shards), 1)
+        s = shards[rank]
+        self.pad = torch.zeros((self.maxrows,) + tuple(tail), dtype=dtype, device=device)
+        self.local = self.pad[: s.r1 - s.r0]
+        self.buf = torch.empty((self.world * self.maxrows,) + tuple(tail), dtype=dtype,
+                               device=device)
+        idx = [torch.arange(r * self.maxrows, r * self.maxrows + (x.r1 - x.r0))
+               for r, x in enumerate(shards)]
+        self.idx = torch.cat(idx).to(device)
+        self.out = torch.empty((shards[-1].r1,) + tuple(tail), dtype=dtype, device=device)
+
+    def __call__(self):
+        import torch.distributed as dist
+        if self.world == 1:
+            return self.local
+        dist.all_gather_into_tensor(self.buf, self.pad, group=self.group)
+        torch.index_select(self.buf, 0, self.idx, out=self.out)
+        return self.out
+
+
 def _row_view_ptr(local, r0):
     """Device pointer of row 0 of the full output given the slab for rows [r0, ...)."""
     row_bytes = local[0].numel() * local.element_size() if local.shape[0] else 0
@@ -78,19 +106,118 @@ def sharded_spmm_groupcoo(fmt, B, shards, rank, group=None, flags=2, stream=None
 
 def spmm_groupcoo_slab(fmt, B, s, flags=2, stream=None):
     """K3 over one shard's groups into that shard's output slab [r1-r0, N]."""
+    local = torch.zeros((s.r1 - s.r0, B.shape[1]), dtype=torch.float32, device=B.device)
+    spmm_groupcoo_into(fmt.AM[s.g0:s.g1], fmt.AK[s.g0:s.g1], fmt.AV[s.g0:s.g1], fmt.group_size,
+                       B, s, local, flags, stream)
+    return local
+
+
+def spmm_groupcoo_into(AM, AK, AV, g, B, s, local, flags=2, stream=None):
+    """K3 over a shard's groups (AM/AK/AV already sliced to [g0, g1)) `+=`
+    into the ZEROED slab `local` = rows [s.r0, s.r1). No allocation: the C
+    pointer is offset by -r0 rows so absolute row ids land in the slab, and
+    `+=` means no zero-fill outside the rank's rows."""
     import ctypes as C
 
     from .abi import check, lib
-    N = B.shape[1]
-    local = torch.zeros((s.r1 - s.r0, N), dtype=torch.float32, device=B.device)
-    if s.g1 > s.g0:
-        AM, AK, AV = fmt.AM[s.g0:s.g1], fmt.AK[s.g0:s.g1], fmt.AV[s.g0:s.g1]
-        st = stream if stream is not None else torch.cuda.current_stream()
-        # `+=` into a zeroed slab: no zero-fill outside the rank's rows; the C
-        # pointer is offset so absolute row ids land inside the slab
-        check(lib().ixb_spmm_groupcoo(C.c_void_p(AM.data_ptr()), C.c_void_p(AK.data_ptr()),
-                                      C.c_void_p(AV.data_ptr()), s.g1 - s.g0, fmt.group_size,
-                                      C.c_void_p(B.data_ptr()), B.shape[0], N,
-                                      C.c_void_p(_row_view_ptr(local, s.r0)), s.r1, 1, flags,
-                                      C.c_void_p(st.cuda_stream)))
+    if AM.numel() == 0:
+        return local
+    st = stream if stream is not None else torch.cuda.current_stream()
+    check(lib().ixb_spmm_groupcoo(C.c_void_p(AM.data_ptr()), C.c_void_p(AK.data_ptr()),
+                                  C.c_void_p(AV.data_ptr()), AM.numel(), g,
+                                  C.c_void_p(B.data_ptr()), B.shape[0], B.shape[1],
+                                  C.c_void_p(_row_view_ptr(local, s.r0)), s.r1, 1, flags,
+                                  C.c_void_p(st.cuda_stream)))
     return local
+
+
+# ----------------------------------------------------------- BlockGroupCOO
+def sharded_spmm_blockgroupcoo(fmt, B, shards, rank, group=None, flags=2, stream=None):
+    """Block-row shards of C[AM[p],bm,n] = AV[p,q,bm,bk] * B[AK[p,q],bk,n]
+    (shard_plan over the block-row coordinate AM); all ranks gather C."""
+    local = spmm_blockgroupcoo_slab(fmt, B, shards[rank], flags, stream)
+    return gather_rows(local, shards, rank, group)
+
+
+def spmm_blockgroupcoo_slab(fmt, B, s, flags=2, stream=None):
+    """K4 over one shard's groups into that shard's block-row slab [r1-r0, bm, N]."""
+    local = torch.zeros((s.r1 - s.r0, fmt.AV.shape[2], B.shape[2]), dtype=torch.float32,
+                        device=B.device)
+    spmm_blockgroupcoo_into(fmt.AM[s.g0:s.g1], fmt.AK[s.g0:s.g1], fmt.AV[s.g0:s.g1], B, s, local,
+                            flags, stream)
+    return local
+
+
+def spmm_blockgroupcoo_into(AM, AK, AV, B, s, local, flags=2, stream=None):
+    """K4 `+=` into the zeroed block-row slab `local` (see spmm_groupcoo_into)."""
+    import ctypes as C
+
+    from .abi import check, lib
+    if AM.numel() == 0:
+        return local
+    G, g, bm, bk = AV.shape
+    st = stream if stream is not None else torch.cuda.current_stream()
+    check(lib().ixb_spmm_blockgroupcoo(
+        C.c_void_p(AM.data_ptr()), C.c_void_p(AK.data_ptr()), C.c_void_p(AV.data_ptr()), G, g,
+        bm, bk, C.c_void_p(B.data_ptr()), B.shape[0], B.shape[2],
+        C.c_void_p(_row_view_ptr(local, s.r0)), s.r1, 1, flags, C.c_void_p(st.cuda_stream)))
+    return local
+
+
+# ----------------------------------------------------------- sparse conv
+def point_blocks(n_out, world):
+    """Contiguous output-voxel blocks (voxels are in sorted order, so a block
+    is a spatially compact slab) as Shards (groups unused)."""
+    bounds = [(n_out * r) // world for r in range(world + 1)]
+    return [Shard(0, 0, bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def shard_map(mo, mi, mz, s):
+    """The pairs of a kernel map (numpy or torch, any order) whose output
+    voxel is in [s.r0, s.r1), output index rebased to the slab. Order is
+    kept, so a canonical (offset, out) map stays canonical."""
+    keep = (mo >= s.r0) & (mo < s.r1)
+    return mo[keep] - s.r0, mi[keep], mz[keep]
+
+
+def conv_shard_plan(mo, mi, mz, n_in, s, g, n_off=27):
+    """Point-block shard of a kernel map: keep the pairs whose
+    output voxel lies in [s.r0, s.r1), rebase their output index, and group
+    them by offset exactly as the full map (the canonical (z, x) order is
+    kept by the filter). In is replicated, so input indices stay global.
+    Returns a ConvPlan over the slab's n_out = s.r1 - s.r0 rows."""
+    mo_l, mi_l, mz_l = shard_map(mo, mi, mz, s)
+    n_local = s.r1 - s.r0
+    ones = torch.ones(mo_l.numel(), dtype=torch.float32, device=mo.device)
+    gt = api.group_coo_tensor([n_local, n_in, n_off], [mo_l, mi_l, mz_l], ones, 2, g,
+                              canonical=True)
+    plan = api.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values,
+                        n_in, n_off, n_local)
+    plan.keep_map = gt
+    return plan
+
+
+def sharded_conv(plan_local, In, Weight, shards, rank, group=None):
+    """Rank `rank` runs its point-block plan into its Out slab; all ranks
+    gather the full Out."""
+    s = shards[rank]
+    local = torch.empty((s.r1 - s.r0, Weight.shape[2]), dtype=torch.float32, device=In.device)
+    if s.r1 > s.r0:
+        plan_local.run(In, Weight, local, accumulate=False)
+    return gather_rows(local, shards, rank, group)
+
+
+# ----------------------------------------------------------- tensor product
+def edge_blocks(batch, world):
+    """Contiguous edge ranges (X, Y, Z are sharded; W is replicated)."""
+    return point_blocks(batch, world)
+
+
+def sharded_tp(plan, X, Y, W, shards, rank, group=None, gather=True):
+    """Rank `rank` evaluates Z for its edge range; the all-gather of Z is only
+    needed when every rank wants the full output."""
+    s = shards[rank]
+    local = torch.empty((s.r1 - s.r0, plan.ni, plan.Wd), dtype=torch.float32, device=X.device)
+    if s.r1 > s.r0:
+        plan.run(X[s.r0:s.r1], Y[s.r0:s.r1], W, local, accumulate=False)
+    return gather_rows(local, shards, rank, group) if gather else local

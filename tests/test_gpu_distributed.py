@@ -1,0 +1,189 @@
+"""SURVEY.md §4 'virtual ranks' for every sharded evaluator (§8e): each
+shard's slab is computed on one GPU by the sharded code path of
+paper_2510_17505_b200.distributed, the slabs are assembled, and the result
+must equal the unsharded evaluator bit for bit for world = 1, 2, 3, 4, 8
+(every output row has exactly one owner and keeps its summation order).
+The multi-process collective itself is covered by tests/test_distributed.py
+(gloo, world 2/3)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+WORLDS = [1, 2, 3, 4, 8]
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_17505_b200 as P
+    P.lib()
+    return P
+
+
+def bf16_dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("world", WORLDS)
+def test_blockgroupcoo_block_row_shards_bit_identical(P, ixo, world):
+    from paper_2510_17505_b200.distributed import shard_plan, spmm_blockgroupcoo_slab
+    rng = ixo.Rng(31)
+    a = ixo.synth_block_sparse_matrix(rng, 16 * 90, 16 * 70, 16, 16, 0.15)
+    b = ixo.synth_dense(rng, (70, 16, 256))
+    fmt = P.dense_to_blockgroupcoo(bf16_dev(a), 16, 16, 0)
+    B = bf16_dev(b)
+    full = torch.zeros((90, 16, 256), device="cuda")
+    P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, full, flags=2)
+    shards = shard_plan(fmt.AM.cpu().numpy(), 90, world)
+    assert shards[0].r0 == 0 and shards[-1].r1 == 90
+    out = torch.full_like(full, float("nan"))
+    for s in shards:
+        out[s.r0:s.r1] = spmm_blockgroupcoo_slab(fmt, B, s)
+    assert torch.equal(out, full)
+
+
+@pytest.mark.parametrize("world", WORLDS)
+def test_conv_point_block_shards_bit_identical(P, world):
+    from paper_2510_17505_b200.distributed import conv_shard_plan, point_blocks
+    g = np.random.default_rng(5)
+    pts = np.unique(g.integers(0, 24, (6000, 3)), axis=0).astype(np.int32)
+    n = len(pts)
+    mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+    ones = torch.ones(mo.numel(), device="cuda")
+    gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], ones, 2, 16, canonical=True)
+    In = bf16_dev(g.standard_normal((n, 64)))
+    W = bf16_dev(g.standard_normal((27, 64, 64)) * 0.1)
+    full = torch.zeros((n, 64), device="cuda")
+    P.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values, n, 27,
+               n).run(In, W, full, accumulate=False)
+    out = torch.full_like(full, float("nan"))
+    for s in point_blocks(n, world):
+        plan = conv_shard_plan(mo, mi, mz, n, s, 16)
+        local = torch.empty((s.r1 - s.r0, 64), device="cuda")
+        plan.run(In, W, local, accumulate=False)
+        out[s.r0:s.r1] = local
+    assert torch.equal(out, full)
+
+
+@pytest.mark.parametrize("world", WORLDS)
+def test_tp_edge_shards_bit_identical(P, ixo, world):
+    from paper_2510_17505_b200.distributed import edge_blocks
+    t = ixo.cg_table(3)
+    coords = [torch.from_numpy(np.ascontiguousarray(c, np.int32)).cuda()
+              for c in (t["i"], t["j"], t["k"], t["l"])]
+    nl = len(t["paths"])
+    gt = P.group_coo_tensor([16, 16, 16, nl], coords,
+                            torch.from_numpy(t["v"].astype(np.float32)).cuda(), 3, 4)
+    plan = P.TpPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1],
+                    gt.member_coords[2], gt.values, 16, 16, 16, nl)
+    g = np.random.default_rng(9)
+    Bt = 300
+    X = bf16_dev(g.standard_normal((Bt, 16, 64)))
+    Y = bf16_dev(g.standard_normal((Bt, 16)))
+    W = bf16_dev(g.standard_normal((nl, 64, 64)) * 0.1)
+    full = torch.zeros((Bt, 16, 64), device="cuda")
+    plan.run(X, Y, W, full, accumulate=False)
+    out = torch.full_like(full, float("nan"))
+    for s in edge_blocks(Bt, world):
+        if s.r1 > s.r0:
+            local = torch.empty((s.r1 - s.r0, 16, 64), device="cuda")
+            plan.run(X[s.r0:s.r1], Y[s.r0:s.r1], W, local, accumulate=False)
+            out[s.r0:s.r1] = local
+    assert torch.equal(out, full)
+
+
+def _two_rank_worker(rank, world, port, q):
+    import os
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_17505_b200 as P
+        from paper_2510_17505_b200 import distributed as D
+        from oracle import ixo
+        torch.cuda.set_device(0)
+        res = {}
+        # GroupCOO row shards through SlabGather
+        rng = ixo.Rng(41)
+        a = ixo.synth_sparse_matrix(rng, 2500, 1800, 0.01)
+        b = ixo.synth_dense(rng, (1800, 64))
+        fmt = P.dense_to_groupcoo(torch.from_numpy(a.astype(np.float32)).cuda(), g=0)
+        B = torch.from_numpy(b.astype(np.float32)).cuda()
+        sh = D.shard_plan(fmt.AM.cpu().numpy(), 2500, world)
+        s = sh[rank]
+        sg = D.SlabGather(sh, rank, (64,), torch.float32, "cuda")
+        sg.local.zero_()
+        D.spmm_groupcoo_into(fmt.AM[s.g0:s.g1], fmt.AK[s.g0:s.g1], fmt.AV[s.g0:s.g1],
+                             fmt.group_size, B, s, sg.local)
+        res["groupcoo"] = sg().cpu().numpy()
+        # BlockGroupCOO block-row shards
+        a = ixo.synth_block_sparse_matrix(rng, 16 * 40, 16 * 30, 16, 16, 0.2)
+        b = ixo.synth_dense(rng, (30, 16, 128))
+        f16 = P.dense_to_blockgroupcoo(bf16_dev(a), 16, 16, 0)
+        B16 = bf16_dev(b)
+        res["bgcoo"] = D.sharded_spmm_blockgroupcoo(
+            f16, B16, D.shard_plan(f16.AM.cpu().numpy(), 40, world), rank).cpu().numpy()
+        # conv point blocks
+        g = np.random.default_rng(2)
+        pts = np.unique(g.integers(0, 14, (2000, 3)), axis=0).astype(np.int32)
+        n = len(pts)
+        mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+        In, W = bf16_dev(g.standard_normal((n, 64))), bf16_dev(g.standard_normal((27, 64, 64)))
+        blocks = D.point_blocks(n, world)
+        plan = D.conv_shard_plan(mo, mi, mz, n, blocks[rank], 16)
+        res["conv"] = D.sharded_conv(plan, In, W, blocks, rank).cpu().numpy()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_share_gpu_sharded_gather(P, ixo):
+    """Two real ranks (gloo, both on cuda:0) run the sharded evaluators and
+    gather; every rank's result equals the single-call evaluator bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = ixo.Rng(41)
+    a = ixo.synth_sparse_matrix(rng, 2500, 1800, 0.01)
+    b = ixo.synth_dense(rng, (1800, 64))
+    fmt = P.dense_to_groupcoo(torch.from_numpy(a.astype(np.float32)).cuda(), g=0)
+    full = torch.zeros((2500, 64), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, torch.from_numpy(b.astype(np.float32)).cuda(), full)
+    a = ixo.synth_block_sparse_matrix(rng, 16 * 40, 16 * 30, 16, 16, 0.2)
+    b = ixo.synth_dense(rng, (30, 16, 128))
+    f16 = P.dense_to_blockgroupcoo(bf16_dev(a), 16, 16, 0)
+    full16 = torch.zeros((40, 16, 128), device="cuda")
+    P.spmm_blockgroupcoo(f16.AM, f16.AK, f16.AV, bf16_dev(b), full16)
+    g = np.random.default_rng(2)
+    pts = np.unique(g.integers(0, 14, (2000, 3)), axis=0).astype(np.int32)
+    n = len(pts)
+    mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+    In, W = bf16_dev(g.standard_normal((n, 64))), bf16_dev(g.standard_normal((27, 64, 64)))
+    gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], torch.ones(mo.numel(), device="cuda"), 2,
+                            16, canonical=True)
+    conv = torch.zeros((n, 64), device="cuda")
+    P.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values, n, 27,
+               n).run(In, W, conv, accumulate=False)
+    for rank, res in results:
+        np.testing.assert_array_equal(res["groupcoo"], full.cpu().numpy())
+        np.testing.assert_array_equal(res["bgcoo"], full16.cpu().numpy())
+        np.testing.assert_array_equal(res["conv"], conv.cpu().numpy())
