@@ -270,12 +270,13 @@ def tensor_hash(a):
 
 
 # ---- file formats (test fixtures and parity only)
-def ref_io(*args):
+def ref_io(*args, env=None):
     """Runs oracle/_ref/ref_io (the reference's file-format code in its own
     process); returns (exit code, stdout)."""
     import subprocess
     exe = os.path.join(ORACLE_DIR, "_ref", "ref_io")
-    r = subprocess.run([exe, *map(str, args)], capture_output=True, text=True)
+    r = subprocess.run([exe, *map(str, args)], capture_output=True, text=True,
+                       env=dict(os.environ, **env) if env else None)
     return r.returncode, r.stdout
 
 
@@ -294,10 +295,12 @@ def load_matrix_market(path):
             "col": np.asarray(d["col"], np.int64), "values": np.asarray(d["values"], dt)}
 
 
-def cmd_convert(inp, outdir, fmt, g=1, group_dim=0, block=None, prefix="A"):
-    """cmd_convert (driver.cpp:403-514) without --measure; returns the exit code."""
+def cmd_convert(inp, outdir, fmt, g=1, group_dim=0, block=None, prefix="A", measure=False):
+    """cmd_convert (driver.cpp:403-514); measure=True is `--measure` (candidates
+    scored by the wall clock of the reference SpMM). Returns the exit code."""
     bm, bk = block if block else (0, 0)
-    rc, _ = ref_io("convert", inp, outdir, fmt, g, group_dim, bm, bk, prefix)
+    rc, _ = ref_io("convert", inp, outdir, fmt, g, group_dim, bm, bk, prefix,
+                   env={"IXR_MEASURE": "1"} if measure else None)
     return rc
 
 

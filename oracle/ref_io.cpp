@@ -78,6 +78,7 @@ int main(int argc, char** argv) {
     cfg.group_dim = std::atoi(argv[6]);
     if (argc >= 9 && std::atoll(argv[7]) > 0) cfg.block = {std::atoll(argv[7]), std::atoll(argv[8])};
     if (argc >= 10) cfg.prefix = argv[9];
+    if (const char* m = std::getenv("IXR_MEASURE")) cfg.measure = std::atoi(m) != 0;  // --measure
     try {
       return ixsum::cmd_convert(cfg, std::cout, std::cerr);
     } catch (const std::exception& e) {

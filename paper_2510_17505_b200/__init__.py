@@ -25,7 +25,7 @@ from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupco
 from .executor import execute_mode, match_workload, WORKLOADS
 from . import io
 from .io import (ixt_info, load_ixt, save_ixt, load_matrix_market, read_matrix_market_host,
-                 save_format, load_format, convert, tune_report)
+                 save_format, load_format, convert, tune_report, tune_measured)
 
 __all__ = [
     "lib", "lib_path", "IxbError", "ParseError", "BindError", "ShapeError", "IndexRangeError",
@@ -36,5 +36,5 @@ __all__ = [
     "tp_grouped", "shard_groups", "ConvPlan", "TpPlan", "spmm_groupcoo_host",
     "spmm_blockgroupcoo_host", "count_accesses_model", "execute_mode", "match_workload",
     "WORKLOADS", "io", "ixt_info", "load_ixt", "save_ixt", "load_matrix_market",
-    "read_matrix_market_host", "save_format", "load_format", "convert", "tune_report",
+    "read_matrix_market_host", "save_format", "load_format", "convert", "tune_report", "tune_measured",
 ]

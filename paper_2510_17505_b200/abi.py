@@ -7,7 +7,8 @@ _lib = None
 
 
 def lib_path():
-    return os.path.join(_HERE, "libixb.so")
+    # IXB_LIB_PATH: load an alternative build of the same library (perf experiments)
+    return os.environ.get("IXB_LIB_PATH") or os.path.join(_HERE, "libixb.so")
 
 
 class IxbError(RuntimeError):

@@ -31,7 +31,7 @@ constexpr int kMathWarps = 16;                     // 64 edges x 8 u-slices
 constexpr int kMathThreads = kMathWarps * 32;
 constexpr int kTpThreads = kMathThreads + 64;      // + UMMA warp + TMA warp
 constexpr int kMaxJobs = 192;
-constexpr int kMaxEntries = 480;
+constexpr int kMaxJSteps = 512;
 constexpr int kMaxPathSeq = 64;
 constexpr int kNU = 2;                              // U ring (job operands, hi + lo)
 constexpr int kNW = 3;                              // W ring (one path each)
@@ -42,12 +42,20 @@ constexpr uint32_t kXTile = kEdges * 16 * 128;      // 64 edges x 16 irrep rows 
 
 // CG table reshaped for the tensor-core path, passed by value (constant bank:
 // every lane reads the same entry, which the constant cache broadcasts).
+// A job's entries are regrouped by input row j ("j-steps"): each X row is
+// loaded and converted once per job and feeds both components of the pair,
+// with coef_h(j) = sum_k v * Y[k] over the component's entries at that j.
 struct TpMeta {
   int njobs, npaths, ni, present;  // present: bit i = component i receives a job
   // job: {l | first-touch-of-cp << 8 | last-job-of-path << 9 | first-job-of-path << 10,
-  //       cp | path-seq << 8, e1 | n1 << 16, e2 | n2 << 16}
+  //       cp | path-seq << 8, first j-step | j-step count << 16, 0}
   int4 job[kMaxJobs];
-  int2 entry[kMaxEntries];  // {j | k << 8, float bits of v}
+  // j-step: {j | n0 << 4 | n1 << 6 | k00 << 8 | k01 << 12 | k10 << 16 | k11 << 20,
+  //          v00, v01, v10 (float bits)} and v11 in jv11: component 2cp has n0 <= 2
+  //          terms (k0t, v0t) at this j, component 2cp+1 has n1 <= 2 (a (component, j)
+  //          with more terms takes several steps)
+  int4 jstep[kMaxJSteps];
+  float jv11[kMaxJSteps];
   int path_l[kMaxPathSeq];  // W index of each path in job order
 };
 
@@ -87,8 +95,9 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     tp_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ TpMeta meta, TpArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // align by offset (not through an integer cast) so every derived pointer
+  // stays in the shared space: LDS/STS instead of generic loads
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* Xs = smem;                   // [64 edges * nj rows][128 B]
   uint8_t* Us = Xs + kXTile;            // [kNU][128 rows][128 B]  (SW128 K-major)
   uint8_t* Ws = Us + kNU * kUSlot;      // [kNW][64 rows][128 B]   (SW128 MN-major)
@@ -214,27 +223,43 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         // per component of the pair: U = hi + lo, both bf16 (the UMMA pair sees U
         // to ~2^-16 relative, so the only bf16 roundings are the operands X, Y, W)
         uint4 u[2], ul[2];
+        float2 a2[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a2[h][q] = make_float2(0.f, 0.f);
+        const int s0 = job.z & 0xFFFF, ns = job.z >> 16;
+#pragma unroll 2
+        for (int st = s0; st < s0 + ns; ++st) {
+          const int4 js = meta.jstep[st];
+          const int n0 = (js.x >> 4) & 3, n1 = (js.x >> 6) & 3;
+          const uint4 xv = *reinterpret_cast<const uint4*>(xrow + (js.x & 15) * 128);
+          float c0 = __int_as_float(js.y) * yrow[(js.x >> 8) & 15];
+          float c1 = __int_as_float(js.w) * yrow[(js.x >> 16) & 15];
+          if (n0 > 1) c0 = fmaf(__int_as_float(js.z), yrow[(js.x >> 12) & 15], c0);
+          if (n1 > 1) c1 = fmaf(meta.jv11[st], yrow[(js.x >> 20) & 15], c1);
+          const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
+          float2 xf[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) xf[q] = __bfloat1622float2(xh[q]);
+          if (n0) {  // uniform: every lane runs the same job
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a2[0][q] = ffma2(c0, xf[q], a2[0][q]);
+          }
+          if (n1) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a2[1][q] = ffma2(c1, xf[q], a2[1][q]);
+          }
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int e0 = h ? (job.w & 0xFFFF) : (job.z & 0xFFFF);
-          const int ne = h ? (job.w >> 16) : (job.z >> 16);
-          float2 a2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                          make_float2(0.f, 0.f)};
-          for (int e = e0; e < e0 + ne; ++e) {
-            const int2 en = meta.entry[e];
-            const float coef = __int_as_float(en.y) * yrow[(en.x >> 8) & 0xFF];
-            const uint4 xv = *reinterpret_cast<const uint4*>(xrow + (en.x & 0xFF) * 128);
-            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) a2[q] = ffma2(coef, __bfloat1622float2(xh[q]), a2[q]);
-          }
           __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&u[h]);
           __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&ul[h]);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            ph[q] = __floats2bfloat162_rn(a2[q].x, a2[q].y);
+            ph[q] = __floats2bfloat162_rn(a2[h][q].x, a2[h][q].y);
             const float2 back = __bfloat1622float2(ph[q]);
-            pl[q] = __floats2bfloat162_rn(a2[q].x - back.x, a2[q].y - back.y);
+            pl[q] = __floats2bfloat162_rn(a2[h][q].x - back.x, a2[h][q].y - back.y);
           }
         }
         const int64_t jc = jc0 + n;
@@ -419,29 +444,51 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
         if (hv[sl] == 0.f) continue;
         li[hl[sl / g]][hi[sl]].push_back(static_cast<int32_t>(sl));
       }
-      int njob = 0, ne = 0, nps = 0;
+      int njob = 0, nst = 0, nps = 0;
       std::vector<bool> touched((ni + 1) / 2, false);
       for (int l = 0; l < nl && tc; ++l) {
         const int first_job = njob;
         for (int cp = 0; cp < (ni + 1) / 2 && tc; ++cp) {
-          int e[2] = {0, 0}, n[2] = {0, 0};
-          for (int h = 0; h < 2 && tc; ++h) {
-            const int i = 2 * cp + h;
-            if (i >= ni) continue;
-            e[h] = ne;
-            for (int32_t sl : li[l][i]) {
-              if (ne >= kMaxEntries) {
+          // j-steps: distinct input rows j of the pair (ascending); per step the
+          // k-terms of component 2cp, then of 2cp+1, each in slot order
+          const std::vector<int32_t> none;
+          const std::vector<int32_t>& c0 = 2 * cp < ni ? li[l][2 * cp] : none;
+          const std::vector<int32_t>& c1 = 2 * cp + 1 < ni ? li[l][2 * cp + 1] : none;
+          if (c0.empty() && c1.empty()) continue;
+          if (!c0.empty()) meta.present |= 1 << (2 * cp);
+          if (!c1.empty()) meta.present |= 1 << (2 * cp + 1);
+          const int st0 = nst;
+          for (int j = 0; j < nj && tc; ++j) {
+            std::vector<int32_t> t[2];
+            for (int h = 0; h < 2; ++h)
+              for (int32_t sl : h ? c1 : c0)
+                if (hj[sl] == j) t[h].push_back(sl);
+            for (size_t r = 0; r < t[0].size() || r < t[1].size(); r += 2) {
+              if (nst >= kMaxJSteps) {
                 tc = false;
                 break;
               }
-              int vbits;
-              std::memcpy(&vbits, &hv[sl], sizeof vbits);
-              meta.entry[ne++] = make_int2(hj[sl] | (hk[sl] << 8), vbits);
+              int n[2], kk[2][2] = {{0, 0}, {0, 0}};
+              float vv[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+              for (int h = 0; h < 2; ++h) {
+                n[h] = static_cast<int>(std::min<size_t>(2, t[h].size() > r ? t[h].size() - r : 0));
+                for (int q = 0; q < n[h]; ++q) {
+                  kk[h][q] = hk[t[h][r + q]];
+                  vv[h][q] = hv[t[h][r + q]];
+                }
+              }
+              auto bits = [](float f) {
+                int b;
+                std::memcpy(&b, &f, sizeof b);
+                return b;
+              };
+              meta.jstep[nst] = make_int4(j | (n[0] << 4) | (n[1] << 6) | (kk[0][0] << 8) |
+                                              (kk[0][1] << 12) | (kk[1][0] << 16) | (kk[1][1] << 20),
+                                          bits(vv[0][0]), bits(vv[0][1]), bits(vv[1][0]));
+              meta.jv11[nst++] = vv[1][1];
             }
-            n[h] = ne - e[h];
-            if (n[h] > 0) meta.present |= 1 << i;
           }
-          if (!tc || n[0] + n[1] == 0) continue;
+          if (!tc) break;
           if (njob >= kMaxJobs || nps >= kMaxPathSeq) {
             tc = false;
             break;
@@ -450,7 +497,7 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
           touched[cp] = true;
           const int fp = njob == first_job ? 1 : 0;
           meta.job[njob] = make_int4(l | (ft << 8) | (fp << 10), cp | (nps << 8),
-                                     e[0] | (n[0] << 16), e[1] | (n[1] << 16));
+                                     st0 | ((nst - st0) << 16), 0);
           ++njob;
         }
         if (tc && njob > first_job) {

@@ -147,6 +147,48 @@ def tune_report(coord, extent, count_empty_rows=False, stream=None):
     return g.value, gs.value, [(cg[i], cs[i]) for i in range(n.value)]
 
 
+def tune_measured(coo, group_dim=0, count_empty_rows=False, repeats=3, bcols=8, stream=None):
+    """select with a measured evaluator (tuner.cpp:100-118; the `--measure`
+    path of cmd_convert, driver.cpp:434-460): every candidate g of the
+    occupancy profile is built on the device (coo_to_groupcoo) and scored
+    by the best of `repeats` CUDA-event timings of the GroupCOO SpMM
+    C[AM[p],n] += AV[p,q] * B[AK[p,q],n] (K3) against B = synth_dense(Rng(1),
+    [cols, bcols]); the first candidate wins a tie. Returns
+    (chosen g, g*, [(g, ms)]). Like the reference's evaluator the expression
+    is row-grouped, so group_dim must be 0."""
+    from . import synth as S
+    if group_dim != 0:
+        raise ValueError("measured tuning scores the row-grouped SpMM: group_dim must be 0")
+    _, gs, cands = tune_report(coo.row, coo.rows, count_empty_rows, stream)
+    dev = coo.row.device
+    B = S.synth_dense(S.Rng(1), (coo.cols, bcols), S.INT if coo.integer else S.REAL,
+                      torch.float32).to(dev)
+    C_out = torch.zeros((coo.rows, bcols), dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    scored = []
+    for g, _ in cands:
+        gc = api.coo_to_groupcoo(coo.rows, coo.cols, coo.row, coo.col,
+                                 coo.values.to(torch.float32), 0, g, canonical=False,
+                                 stream=stream)
+        best = None
+        for rep in range(max(1, repeats) + 1):  # +1: untimed first call
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            api.spmm_groupcoo(gc.AM, gc.AK, gc.AV, B, C_out, accumulate=True, stream=stream)
+            b.record(st)
+            b.synchronize()
+            if rep:
+                ms = a.elapsed_time(b)
+                best = ms if best is None else min(best, ms)
+        scored.append((g, best))
+    chosen, low = scored[0]
+    for g, ms in scored:
+        if ms < low:
+            chosen, low = g, ms
+    return chosen, gs, scored
+
+
 # ---------------------------------------------------------------- format directories
 def _value_dtype(integer, dtype):
     if dtype is not None:
@@ -208,13 +250,16 @@ def load_format(outdir, dtype=None, device=None, prefix="A"):
 
 
 def convert(input_path, outdir, format="coo", g=1, group_dim=0, block=None, prefix="A",
-            count_empty_rows=False, dtype=None, device=None, stream=None):
+            count_empty_rows=False, dtype=None, device=None, stream=None, measure=False,
+            measure_repeats=3, measure_bcols=8):
     """cmd_convert (driver.cpp:403-514) with the device builders: input .mtx
     (coordinate -> canonical COO; array -> dense_to_coo) or .ixt (dense);
     format coo | groupcoo | auto | blockgroupcoo. `auto` records the tuner's
-    report ("scoredBy": "costExact"; the reference's `--measure` timing mode
-    is not reproduced). Values stay in their file type (fp64 / int64) unless
-    `dtype` says otherwise, so the arrays match the reference bit for bit."""
+    report: "scoredBy": "costExact" (F(g) of the occupancy profile), or with
+    measure=True "measuredMs" (tune_measured: the candidates timed on the
+    device, driver.cpp:434-460). Values stay in their file type (fp64 /
+    int64) unless `dtype` says otherwise, so the arrays match the reference
+    bit for bit."""
     dev = _device(device)
     if input_path.endswith(".mtx"):
         m = _Mtx(input_path)
@@ -252,9 +297,13 @@ def convert(input_path, outdir, format="coo", g=1, group_dim=0, block=None, pref
         man["format"] = "groupcoo"
         if format == "auto":
             coord = coo.row if group_dim == 0 else coo.col
-            g, gs, cands = tune_report(coord, rows if group_dim == 0 else cols, count_empty_rows,
-                                       stream)
-            man["tuner"] = {"gStar": gs, "scoredBy": "costExact",
+            if measure:
+                g, gs, cands = tune_measured(coo, group_dim, count_empty_rows, measure_repeats,
+                                             measure_bcols, stream)
+            else:
+                g, gs, cands = tune_report(coord, rows if group_dim == 0 else cols,
+                                           count_empty_rows, stream)
+            man["tuner"] = {"gStar": gs, "scoredBy": "measuredMs" if measure else "costExact",
                             "candidates": [{"g": cg, "score": sc} for cg, sc in cands]}
         gc = _coo_to_groupcoo(coo, group_dim, g, stream)
         G = gc.num_groups()

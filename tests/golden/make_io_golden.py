@@ -179,5 +179,29 @@ def main():
     print("wrote", OUT)
 
 
+def measure_cases():
+    """`convert --measure` directories (driver.cpp:434-460): the scores are
+    wall-clock times, so tests compare the manifest's structure, gStar and
+    candidate list, not the scores or (timing-dependent) chosen g."""
+    import shutil
+    out = os.path.join(OUT, "convert_measure")
+    shutil.rmtree(out, ignore_errors=True)
+    os.makedirs(out)
+    cases = {"random_auto_measure": ("random_300x200.mtx", "auto", 1, 0, None),
+             "general_auto_measure": ("general_real.mtx", "auto", 1, 0, None)}
+    index = {}
+    for name, (inp, fmt, gg, gd, block) in cases.items():
+        rc = ref.cmd_convert(os.path.join(OUT, inp), os.path.join(out, name), fmt, gg, gd, block,
+                             measure=True)
+        assert rc == 0, (name, rc)
+        index[name] = {"input": inp, "format": fmt, "g": gg, "group_dim": gd, "block": block}
+    with open(os.path.join(out, "cases.json"), "w") as f:
+        json.dump(index, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--measure-only" in sys.argv:
+        measure_cases()
+    else:
+        main()
+        measure_cases()

@@ -137,3 +137,45 @@ def test_load_format_then_evaluate(P):
     assert ixo.max_rel_error(want, C.double().cpu().numpy()) <= 1e-5
     bg, man = P.load_format(os.path.join(GOLD, "convert", "general_bgcoo"))
     assert man["format"] == "blockgroupcoo" and list(bg.AV.shape[2:]) == man["block"]
+
+
+MEASURE = json.load(open(os.path.join(GOLD, "convert_measure", "cases.json")))
+
+
+@pytest.mark.parametrize("case", sorted(MEASURE))
+def test_convert_measure_like_reference(P, case, tmp_path):
+    """`convert --measure` (driver.cpp:434-460): candidates scored by measured
+    time on the device. The reference's directory pins the manifest layout,
+    g* and the candidate list; scores are timings, so the chosen g must be
+    the first minimum of OUR scores, and the arrays must equal a plain
+    `groupcoo` conversion at that g byte for byte."""
+    c = MEASURE[case]
+    want = json.load(open(os.path.join(GOLD, "convert_measure", case, "manifest.json")))
+    out = str(tmp_path / case)
+    man = P.convert(os.path.join(GOLD, c["input"]), out, c["format"], c["g"], c["group_dim"],
+                    c["block"], measure=True, measure_repeats=3)
+    assert list(man) == list(want)
+    assert list(man["tuner"]) == list(want["tuner"])
+    assert man["tuner"]["scoredBy"] == want["tuner"]["scoredBy"] == "measuredMs"
+    assert man["tuner"]["gStar"] == want["tuner"]["gStar"]
+    assert [x["g"] for x in man["tuner"]["candidates"]] == \
+        [x["g"] for x in want["tuner"]["candidates"]]
+    scores = [(x["g"], x["score"]) for x in man["tuner"]["candidates"]]
+    assert all(s > 0 for _, s in scores)
+    first_min = min(scores, key=lambda gs: gs[1])  # min() keeps the first on a tie
+    assert man["g"] == first_min[0]
+    plain = str(tmp_path / "plain")
+    P.convert(os.path.join(GOLD, c["input"]), plain, "groupcoo", man["g"], c["group_dim"])
+    for name, file in man["arrays"].items():
+        assert open(os.path.join(out, file), "rb").read() == \
+            open(os.path.join(plain, file), "rb").read(), name
+    if man["g"] == want["g"]:  # same choice as the reference run: same arrays
+        for name, file in want["arrays"].items():
+            assert open(os.path.join(out, file), "rb").read() == \
+                open(os.path.join(GOLD, "convert_measure", case, file), "rb").read(), name
+
+
+def test_tune_measured_rejects_column_grouping(P):
+    coo = P.load_matrix_market(os.path.join(GOLD, "random_300x200.mtx"), torch.float64)
+    with pytest.raises(ValueError):
+        P.tune_measured(coo, group_dim=1)
