@@ -29,7 +29,9 @@ using namespace sm100;
 constexpr int kEdges = 64;                         // edges per tile
 constexpr int kMathWarps = 16;                     // 64 edges x 8 u-slices
 constexpr int kMathThreads = kMathWarps * 32;
-constexpr int kTpThreads = kMathThreads + 64;      // + UMMA warp + TMA warp
+constexpr int kEpiWarps = 4;                        // one per TMEM lane quarter
+constexpr int kTpThreads = kMathThreads + 64 + kEpiWarps * 32;  // + UMMA, TMA, epilogue warps
+constexpr int kPairs = 8;                           // component pairs (16 components)
 constexpr int kMaxJobs = 192;
 constexpr int kMaxJSteps = 512;
 constexpr int kMaxPathSeq = 64;
@@ -47,8 +49,10 @@ constexpr uint32_t kXTile = kEdges * 16 * 128;      // 64 edges x 16 irrep rows 
 // with coef_h(j) = sum_k v * Y[k] over the component's entries at that j.
 struct TpMeta {
   int njobs, npaths, ni, present;  // present: bit i = component i receives a job
-  // job: {l | first-touch-of-cp << 8 | last-job-of-path << 9 | first-job-of-path << 10,
-  //       cp | path-seq << 8, first j-step | j-step count << 16, 0}
+  int ncp;                         // component pairs that receive a job
+  int cp_order[kPairs];            // drain order: the ncp pairs with jobs by their last job, then the rest
+  // job: {l | first-touch-of-cp << 8 | last-job-of-path << 9 | first-job-of-path << 10 |
+  //       last-touch-of-cp << 11, cp | path-seq << 8, first j-step | j-step count << 16, 0}
   int4 job[kMaxJobs];
   // j-step: {j | n0 << 4 | n1 << 6 | k00 << 8 | k01 << 12 | k10 << 16 | k11 << 20,
   //          v00, v01, v10 (float bits)} and v11 in jv11: component 2cp has n0 <= 2
@@ -89,8 +93,12 @@ struct TpArgs {
 // component 2cp+1): 8 pairs x 64 = all 512 columns.
 // Warps 0..15 compute U for job n into a kNU-deep ring (mbarrier handoff,
 // no block-wide barrier per job), warp 16 issues 4 UMMAs (K = 64) per job and
-// commits the slot back, warp 17 streams X tiles and W[l] (kNW ring) by TMA.
-// X of tile t+1 loads while the math warps drain tile t from TMEM.
+// commits the slot back, warp 17 streams X tiles and W[l] (kNW ring) by TMA,
+// warps 18..21 drain TMEM into Z. TMEM is handed over per component pair:
+// the issuer commits acc_full[cp] after the pair's last job of the tile and
+// waits on acc_empty[cp] before its first job of the next tile. Paths run
+// in order of their output irrep, so pairs complete one after another and
+// draining overlaps the remaining jobs and the next tile's start.
 __global__ void __launch_bounds__(kTpThreads, 1)
     tp_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ TpMeta meta, TpArgs a) {
@@ -108,9 +116,9 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   uint64_t* w_empty = w_full + kNW;
   uint64_t* u_full = w_empty + kNW;
   uint64_t* u_empty = u_full + kNU;
-  uint64_t* acc_full = u_empty + kNU;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* acc_full = u_empty + kNU;      // [kPairs]
+  uint64_t* acc_empty = acc_full + kPairs;  // [kPairs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kPairs);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -124,8 +132,10 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       mbar_init(&u_full[s], kMathWarps);
       mbar_init(&u_empty[s], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, kMathWarps);
+    for (int c = 0; c < kPairs; ++c) {
+      mbar_init(&acc_full[c], 1);
+      mbar_init(&acc_empty[c], kEpiWarps);
+    }
     fence_barrier_init();
   }
   if (warp == kMathWarps) {
@@ -169,8 +179,6 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       constexpr uint32_t idesc = idesc_bf16_f32(128, 64, /*A K-major*/ false, /*B MN-major*/ true);
       int tl = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-        mbar_wait(acc_empty, (tl & 1) ^ 1);  // previous tile drained from TMEM
-        tc_fence_after();
         const int64_t jc0 = static_cast<int64_t>(tl) * njobs;
         const int64_t wc0 = static_cast<int64_t>(tl) * npaths;
         for (int n = 0; n < njobs; ++n) {
@@ -186,6 +194,10 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           const uint32_t u0 = smem_u32(Us + us * kUSlot);
           const uint32_t w0 = smem_u32(Ws + wslot * kWTileTp);
           const bool first = (job.x >> 8) & 1;
+          if (first) {  // this pair's columns drained from the previous tile
+            mbar_wait(&acc_empty[cp], (tl & 1) ^ 1);
+            tc_fence_after();
+          }
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
@@ -196,11 +208,11 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           }
           umma_commit(&u_empty[us]);                         // U slot reusable
           if ((job.x >> 9) & 1) umma_commit(&w_empty[wslot]);  // last job of this path
+          if ((job.x >> 11) & 1) umma_commit(&acc_full[cp]);   // pair complete for this tile
         }
-        umma_commit(acc_full);
       }
     }
-  } else {
+  } else if (warp < kMathWarps) {
     // ---------------------------------------------------------- math warps
     const int b_loc = tid >> 3, slice = tid & 7;  // edge in tile, u slice [8*slice, +8)
     const uint32_t row1 = b_loc * 128 + ((slice ^ (b_loc & 7)) << 4);              // comp 2cp
@@ -276,17 +288,30 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(x_empty);  // X of this tile no longer read
-      // ---- epilogue: TMEM -> Z (lanes: quarter q -> comp parity q>>1, edges (q&1)*32+lane)
-      mbar_wait(acc_full, tl & 1);
-      tc_fence_after();
-      const int quarter = warp & 3, grp = warp >> 2;
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue warps
+    // TMEM lane quarter q = warp % 4: component parity q >> 1, edges (q & 1) * 32 + lane
+    const int quarter = warp & 3;
+    int tl = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
       const int64_t be = tile * kEdges + (quarter & 1) * 32 + lane;
 #pragma unroll 1
-      for (int cp = 2 * grp; cp < 2 * grp + 2; ++cp) {
+      for (int oc = 0; oc < kPairs; ++oc) {
+        const bool touched = oc < meta.ncp;
+        const int cp = meta.cp_order[oc];
         const int comp = 2 * cp + (quarter >> 1);
-        const bool has = comp < a.ni && ((meta.present >> comp) & 1);
+        if (2 * cp >= a.ni) continue;
         const bool row_ok = be < a.batch && comp < a.ni;
         float4* z = reinterpret_cast<float4*>(a.Z + (be * a.ni + comp) * 64);
+        if (!touched) {  // no job writes this pair: `=` stores zeros, `+=` leaves Z
+          if (row_ok && !a.accumulate)
+            for (int c = 0; c < 16; ++c) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          continue;
+        }
+        mbar_wait(&acc_full[cp], tl & 1);
+        tc_fence_after();
+        const bool has = comp < a.ni && ((meta.present >> comp) & 1);
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {  // 16 columns at a time keeps register pressure low
           uint32_t r[16];
@@ -311,10 +336,10 @@ __global__ void __launch_bounds__(kTpThreads, 1)
             }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[cp]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
     }
   }
   tc_fence_before();
@@ -446,7 +471,18 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
       }
       int njob = 0, nst = 0, nps = 0;
       std::vector<bool> touched((ni + 1) / 2, false);
-      for (int l = 0; l < nl && tc; ++l) {
+      // paths in order of the highest output component they write (stable):
+      // component pairs then complete one after another within a tile
+      std::vector<int> lorder(nl);
+      std::vector<int> top(nl, -1);
+      for (int l = 0; l < nl; ++l) {
+        lorder[l] = l;
+        for (int i = 0; i < ni; ++i)
+          if (!li[l][i].empty()) top[l] = i;
+      }
+      std::stable_sort(lorder.begin(), lorder.end(), [&](int x, int y) { return top[x] < top[y]; });
+      for (int lo = 0; lo < nl && tc; ++lo) {
+        const int l = lorder[lo];
         const int first_job = njob;
         for (int cp = 0; cp < (ni + 1) / 2 && tc; ++cp) {
           // j-steps: distinct input rows j of the pair (ascending); per step the
@@ -507,6 +543,21 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
       }
       meta.njobs = njob;
       meta.npaths = nps;
+      // last job of each pair -> commit flag; drain order = order of last jobs
+      int last[kPairs];
+      for (int c = 0; c < kPairs; ++c) last[c] = -1;
+      for (int n = 0; n < njob; ++n) last[meta.job[n].y & 0xFF] = n;
+      meta.ncp = 0;
+      for (int n = 0; n < njob; ++n) {
+        const int c = meta.job[n].y & 0xFF;
+        if (last[c] == n) {
+          meta.job[n].x |= 1 << 11;
+          meta.cp_order[meta.ncp++] = c;
+        }
+      }
+      int k = meta.ncp;
+      for (int c = 0; c < kPairs; ++c)
+        if (last[c] < 0) meta.cp_order[k++] = c;
     }
     plan->tc = tc;
     *out = plan.release();
