@@ -228,19 +228,26 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // group_coo_tensor produce) need no per-row scaling. The plan turns T into an
 // input-row table Y[x, z] = y + 1 (0 = absent; row stride kOffPad ints, 16 B
 // aligned) plus a bitmask of the offsets each 128-row tile uses. A thread
-// then reads its row's whole Y row in 7 vector loads, no per-offset
-// T -> MAPY dependence and no per-offset block vote remain, and the In row
-// for the next active offset is loaded while the current one is stored and
-// multiplied: one exposed global latency per tile instead of three per
-// offset. The tensor-core part is the kernel above (4 UMMAs M=128,N=64,K=16
-// per offset into one TMEM accumulator, A and W double-buffered), so each
-// output row still accumulates its offsets in z order.
-// Measured on cfg5 (1 M voxels): 0.83 ms -> 0.65 ms. Not shipped: a TMA
-// tile::gather4 version (4 rows per instruction straight into the swizzled
-// operand; 1.0-3.2 ms with 1-8 issuing warps, gather4 costs ~43 cycles per
-// 512 B box per SM; tools/gather4_probe.cu pins its semantics), and a third W
-// slot to prefetch W one offset ahead (0.71 ms: 58 KB of smem drops the
-// 4th CTA per SM).
+// reads its row's whole Y row in 7 vector loads, so no per-offset T -> MAPY
+// dependence and no per-offset block vote remain; the gathers of the next
+// two used offsets are in flight (cp.async) while the current one is
+// multiplied. The tensor-core part is the kernel above (4 UMMAs M=128,N=64,
+// K=16 per offset into one TMEM accumulator), so each output row still
+// accumulates its offsets in z order.
+// Measured on cfg5 (1 M voxels): 0.83 ms (conv_tc_kernel) -> 0.65 ms
+// (register prefetch, one row per thread) -> 0.567 ms (coalesced gather) ->
+// 0.513 ms (cp.async, 3-stage ring). Switching parts off: no gather
+// 0.512 ms, no MMA 0.413 ms, neither (nor W) 0.390 ms — the per-offset
+// __syncthreads + commit round trip of this one-tile-per-CTA structure is
+// the floor. Not shipped:
+// - a persistent warp-specialised kernel (8-stage ring, producer warps,
+//   MMA warp, epilogue warps with double-buffered TMEM): 0.60-0.92 ms; the
+//   producers' proxy fence waits for all of a thread's cp.async, which
+//   serialises stages per warp;
+// - deeper rings at this structure (s4d2 0.645 ms, s5d2 1.13 ms: fewer CTAs
+//   per SM);
+// - TMA tile::gather4 (1.0-3.2 ms; ~43 cycles per 512 B box per SM;
+//   tools/gather4_probe.cu pins its semantics).
 constexpr int kOffPad = 28;  // Y row stride (ints): 27 offsets padded to 16 B
 
 struct UnitArgs {
@@ -252,20 +259,29 @@ struct UnitArgs {
   int accumulate;
 };
 
-__global__ void __launch_bounds__(kConvThreads, 4)
+// Stage k of a tile = its k-th used offset z: the In rows of the 128 output
+// rows land in A[k % S] by cp.async (coalesced: 8 lanes share a 128 B row,
+// so a warp instruction covers 4 whole rows; the row's input index comes
+// from its owner lane by shuffle; absent rows are zero-filled) and W[z] in
+// W[k % S] by TMA, issued D = 2 stages ahead of the MMA. A ring of S = 3
+// (72 KB) keeps 3 CTAs per SM.
+constexpr int kUnitStages = 3;
+constexpr int kUnitDist = 2;
+constexpr uint32_t kUnitSmem = kUnitStages * (kATile + kWTile) + 1024 + 256;
+
+__global__ void __launch_bounds__(kConvThreads, 3)
     conv_unit_kernel(const __grid_constant__ CUtensorMap tmW, UnitArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint8_t* A = smem;               // [2][16 KB]
-  uint8_t* W = smem + 2 * kATile;  // [2][8 KB] (a third W slot costs the 4th CTA per SM)
-  uint64_t* w_full = reinterpret_cast<uint64_t*>(W + 2 * kWTile);
-  uint64_t* mma_done = w_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* A = smem;                         // [kUnitStages][16 KB]
+  uint8_t* W = smem + kUnitStages * kATile;  // [kUnitStages][8 KB]
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(W + kUnitStages * kWTile);
+  uint64_t* mma_done = w_full + kUnitStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + kUnitStages);
   const int tid = threadIdx.x, warp = tid >> 5;
 
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kUnitStages; ++b) {
       mbar_init(&w_full[b], 1);
       mbar_init(&mma_done[b], 1);
     }
@@ -292,6 +308,7 @@ __global__ void __launch_bounds__(kConvThreads, 4)
     for (int j = 0; j < kOffPad; ++j) yr[j] = 0;
   }
   const uint32_t tmask = a.tile_mask[blockIdx.x];
+  const int nk = __popc(tmask);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -299,65 +316,62 @@ __global__ void __launch_bounds__(kConvThreads, 4)
   constexpr uint32_t idesc = idesc_bf16_f32(128, 64, /*A K-major*/ false, /*B MN-major*/ true);
   const uint64_t keep = l2_evict_last();
 
-  // row of In for offset z (zeros when absent); z is warp-uniform
-  auto fetch = [&](int z, uint4 (&c)[8]) {
+  const int lane = tid & 31, chunk = lane & 7, sub = lane >> 3;
+  auto issue = [&](int k) {
+    const int z = __fns(tmask, 0, k + 1);  // k-th used offset (warp-uniform)
+    const int st = k % kUnitStages;
     int y1 = 0;
 #pragma unroll
     for (int j = 0; j < kOffPad; ++j) y1 = (j == z) ? yr[j] : y1;
-    if (y1 > 0) {
-      const uint4* src = reinterpret_cast<const uint4*>(a.In + static_cast<int64_t>(y1 - 1) * 64);
+    const uint32_t awarp = smem_u32(A + st * kATile + warp * 32 * 128);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) c[j] = __ldg(src + j);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) c[j] = make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < 8; ++i) {
+      const int r = sub + 4 * i;
+      const int yy = __shfl_sync(0xffffffffu, y1, r);
+      const __nv_bfloat16* src = a.In + static_cast<int64_t>(yy > 0 ? yy - 1 : 0) * 64 + chunk * 8;
+      cp_async_16(awarp + r * 128 + ((chunk ^ (r & 7)) << 4), src, yy > 0 ? 16u : 0u);
+    }
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&w_full[st], kWTile);
+      tma_load_2d(W + st * kWTile, &tmW, &w_full[st], 0, z * 64, keep);
     }
   };
-  uint32_t mask = tmask;
-  uint4 cur[8];
-  int z = mask ? __ffs(mask) - 1 : -1;
-  if (z >= 0) fetch(z, cur);
-  int k = 0;
-  while (z >= 0) {
-    mask &= mask - 1;
-    const int zn = mask ? __ffs(mask) - 1 : -1;
-    uint4 nxt[8];
-    if (zn >= 0) fetch(zn, nxt);  // next offset's row in flight during this one
-    const int buf = k & 1;
-    if (k >= 2) mbar_wait(&mma_done[buf], ((k - 2) >> 1) & 1);  // MMA k-2 freed buf
-    if (tid == 0) {
-      mbar_arrive_expect_tx(&w_full[buf], kWTile);
-      tma_load_2d(W + buf * kWTile, &tmW, &w_full[buf], 0, z * 64, keep);
-    }
-    uint8_t* arow = A + buf * kATile + tid * 128;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) *reinterpret_cast<uint4*>(arow + ((j ^ (tid & 7)) << 4)) = cur[j];
-    fence_proxy_async_smem();  // st.shared -> tensor core
+  for (int k = 0; k < kUnitDist; ++k) {
+    if (k < nk) issue(k);
+    cp_async_commit();
+  }
+  for (int k = 0; k < nk; ++k) {
+    const int st = k % kUnitStages;
+    cp_async_wait<kUnitDist - 1>();  // this thread's rows of stage k have landed
+    fence_proxy_async_smem();        // cp.async (generic proxy) -> tensor core
     __syncthreads();
     if (tid == 0) {
-      mbar_wait(&w_full[buf], (k >> 1) & 1);
+      mbar_wait(&w_full[st], (k / kUnitStages) & 1);
       tc_fence_after();
-      const uint32_t a0 = smem_u32(A + buf * kATile), w0 = smem_u32(W + buf * kWTile);
+      const uint32_t a0 = smem_u32(A + st * kATile), w0 = smem_u32(W + st * kWTile);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t ad = smem_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
         const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
         umma_f16(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
       }
-      umma_commit(&mma_done[buf]);
+      umma_commit(&mma_done[st]);
     }
-    ++k;
-    z = zn;
-    if (zn >= 0) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+    if (k + kUnitDist < nk) {
+      // stage k + D reuses the slot of stage k + D - S: wait for its MMAs
+      const int old = k + kUnitDist - kUnitStages;
+      if (old >= 0) mbar_wait(&mma_done[old % kUnitStages], (old / kUnitStages) & 1);
+      issue(k + kUnitDist);
     }
+    cp_async_commit();  // (possibly empty) group k + D keeps the wait count uniform
   }
-  float4* o = reinterpret_cast<float4*>(a.Out + x * 64);
-  if (k > 0) {
-    mbar_wait(&mma_done[(k - 1) & 1], ((k - 1) >> 1) & 1);
+  if (nk > 0) {
+    mbar_wait(&mma_done[(nk - 1) % kUnitStages], ((nk - 1) / kUnitStages) & 1);
     tc_fence_after();
   }
+  const int k = nk;
+  float4* o = reinterpret_cast<float4*>(a.Out + x * 64);
 #pragma unroll 1
   for (int c = 0; c < 4; ++c) {
     uint32_t r[16];
@@ -545,7 +559,7 @@ int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void*
                        CU_TENSOR_MAP_SWIZZLE_128B);
       UnitArgs ua{P->Y.p, P->tile_mask.p, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
                   accumulate};
-      const uint32_t smem = 2 * kATile + 2 * kWTile + 1024 + 1024;
+      const uint32_t smem = kUnitSmem;
       static std::once_flag once_u;
       std::call_once(once_u, [&] {
         cuda_check(cudaFuncSetAttribute(conv_unit_kernel,

@@ -103,6 +103,18 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
 
 // Orders this thread's generic-proxy shared-memory writes before later
 // async-proxy (TMA / tcgen05) accesses.
+// 16-byte global -> shared copy (LDGSTS, L2 only); src_size 0 zero-fills
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_size) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_size)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
