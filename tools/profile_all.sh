@@ -20,6 +20,6 @@ prof() {  # workload kernel-regex skip
 prof cfg2 bgcoo_tc
 prof cfg1 spmm_groupcoo
 prof cfg3_d0.30 spmm_groupcoo
-prof cfg5 conv_tc
+prof cfg5 conv_unit
 prof cfg4 tp_tc 1
 ls -la gpurun_out
