@@ -93,11 +93,21 @@ __device__ __forceinline__ void zero_rows(float* C, int64_t N, int64_t r0, int64
   }
 }
 
+// Residency over gathers in flight: T = 1 (N <= 128) runs 4 CTAs (32 warps)
+// per SM with 8 gathers per lane (cfg1 24.0 -> 20.9 us against 2 CTAs x 16);
+// wider passes run 3 CTAs per SM (cfg3 d0.02 349 -> 336 us) without spills.
+#ifndef IXB_K3_U1
+#define IXB_K3_U1 8
+#endif
+template <int T>
+constexpr int k3_min_blocks() {
+  return T == 1 ? 4 : 3;
+}
 template <int VEC, int T, bool PERM>
-__global__ void __launch_bounds__(kThreads, 2) spmm_groupcoo_kernel(SpmmArgs a) {
+__global__ void __launch_bounds__(kThreads, k3_min_blocks<T>()) spmm_groupcoo_kernel(SpmmArgs a) {
   using V = typename VecT<VEC>::T;
   constexpr int kColsPerPass = 32 * VEC * T;
-  constexpr int kUnroll = T >= 4 ? 4 : (T == 2 ? 8 : 16);  // 16 gathers in flight per lane
+  constexpr int kUnroll = T >= 4 ? 4 : (T == 2 ? 8 : IXB_K3_U1);  // gathers in flight per lane
   const int lane = lane_id();
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t base = warp * a.chunk;
