@@ -688,6 +688,24 @@ def run_b200(args, wl):
         step()
     torch.cuda.synchronize()
     P.lib().ixb_check_errors(None)
+    # One step captured in a CUDA graph and replayed per timed iteration, so
+    # the device time carries no host launch latency (the e2e leg below still
+    # goes through the public API call by call). Launches per step are
+    # counted at capture; eager launches if the step cannot be captured.
+    timed_step, timing, per_step = step, "eager launches", None
+    if not args.sharded and not args.no_graph:
+        try:
+            c0 = P.lib().ixb_launch_count()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            per_step = P.lib().ixb_launch_count() - c0
+            graph.replay()
+            torch.cuda.synchronize()
+            timed_step, timing = graph.replay, "CUDA-graph replay of one step"
+        except Exception as e:  # reported in config.timing, never fatal
+            timing = f"eager launches (graph capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
 
     clocks = Clocks(dev)
     if ws > 1:
@@ -701,13 +719,15 @@ def run_b200(args, wl):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        step()
+        timed_step()
         b.record(stream)
         evs.append((a, b))
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     launches = P.lib().ixb_launch_count() - launches0
+    if per_step is not None:
+        launches = per_step * args.steps
     clk = clocks.stop()
     rc = P.lib().ixb_check_errors(None)
     if rc != 0:
@@ -778,7 +798,8 @@ def run_b200(args, wl):
             "config": dict(wl.config(), l2="flushed between steps (256 MiB memset outside the "
                                          "timed events)",
                            parallelism=(f"sharded x{ws} + {backend if ws > 1 else 'no'} all-gather of output slabs"
-                                        if args.sharded else f"weak x{ws}"), **wl.info),
+                                        if args.sharded else f"weak x{ws}"), timing=timing,
+                           **wl.info),
             "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
             "e2e": {"value": e_ms if timelike else wl.flops * jobs / (e_ms * 1e-3) / 1e9,
                     "unit": "ms" if timelike else "GFLOP/s",
@@ -811,6 +832,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of a CUDA-graph replay of the step")
     ap.add_argument("--sharded", action="store_true",
                     help="strong scaling: shard ONE instance across the ranks (row groups, "
                          "point blocks or edges) and all-gather the output inside the step")
