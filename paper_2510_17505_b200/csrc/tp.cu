@@ -36,7 +36,12 @@ constexpr int kMaxJobs = 192;
 constexpr int kMaxJSteps = 512;
 constexpr int kMaxPathSeq = 64;
 constexpr int kNU = 2;                              // U ring (job operands, hi + lo)
-constexpr int kNW = 3;                              // W ring (one path each)
+constexpr int kNW = 2;                              // W ring (one path each)
+constexpr int kGroupWarps = kMathWarps / 2;         // math warps per job group
+#ifndef IXB_TP_JUNROLL
+#define IXB_TP_JUNROLL 1
+#endif
+constexpr int kJUnroll = IXB_TP_JUNROLL;            // j-step loop unroll
 constexpr uint32_t kUHalf = 128 * 128;              // 128 rows (2 comps x 64 edges) x 64 bf16
 constexpr uint32_t kUSlot = 2 * kUHalf;             // hi, lo
 constexpr uint32_t kWTileTp = 64 * 128;             // 64 u-rows x 64 bf16
@@ -109,8 +114,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   uint8_t* Xs = smem;                   // [64 edges * nj rows][128 B]
   uint8_t* Us = Xs + kXTile;            // [kNU][128 rows][128 B]  (SW128 K-major)
   uint8_t* Ws = Us + kNU * kUSlot;      // [kNW][64 rows][128 B]   (SW128 MN-major)
-  float* Ys = reinterpret_cast<float*>(Ws + kNW * kWTileTp);  // [64][16]
-  uint64_t* x_full = reinterpret_cast<uint64_t*>(Ys + kEdges * 16);
+  float* Ys = reinterpret_cast<float*>(Ws + kNW * kWTileTp);  // [2 groups][64][16]
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(Ys + 2 * kEdges * 16);
   uint64_t* x_empty = x_full + 1;
   uint64_t* w_full = x_empty + 1;
   uint64_t* w_empty = w_full + kNW;
@@ -129,7 +134,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       mbar_init(&w_empty[s], 1);
     }
     for (int s = 0; s < kNU; ++s) {
-      mbar_init(&u_full[s], kMathWarps);
+      mbar_init(&u_full[s], kGroupWarps);  // slot s is written by job group s
       mbar_init(&u_empty[s], 1);
     }
     for (int c = 0; c < kPairs; ++c) {
@@ -214,77 +219,96 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     }
   } else if (warp < kMathWarps) {
     // ---------------------------------------------------------- math warps
-    const int b_loc = tid >> 3, slice = tid & 7;  // edge in tile, u slice [8*slice, +8)
-    const uint32_t row1 = b_loc * 128 + ((slice ^ (b_loc & 7)) << 4);              // comp 2cp
-    const uint32_t row2 = (64 + b_loc) * 128 + ((slice ^ ((64 + b_loc) & 7)) << 4);  // comp 2cp+1
-    const uint8_t* xrow = Xs + b_loc * a.nj * 128 + slice * 16;
-    float* yrow = Ys + b_loc * 16;
+    // Two groups of 8 warps take alternate jobs (job jc -> group jc % 2 -> U
+    // slot jc % 2, the issuer's ring order): one group computes while the
+    // other group's slot is being consumed, so the handoff round trip hides
+    // behind math. A thread owns one edge and 16 u of both components.
+    const int grp = warp / kGroupWarps;
+    const int gt = tid - grp * kGroupWarps * 32;
+    const int b_loc = gt >> 2, slice = gt & 3;  // edge in tile, u slice [16*slice, +16)
+    uint32_t rowo[2][2];                        // [component][8-u chunk] in the SW128 U tile
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int r = h * 64 + b_loc, ch = 2 * slice + c;
+        rowo[h][c] = r * 128 + ((ch ^ (r & 7)) << 4);
+      }
+    const uint8_t* xrow = Xs + b_loc * a.nj * 128 + slice * 32;
+    float* yrow = Ys + (grp * kEdges + b_loc) * 16;
     int tl = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
       const int64_t b = tile * kEdges + b_loc;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int k = 2 * slice + q;
+      for (int q = 0; q < 4; ++q) {
+        const int k = 4 * slice + q;
         yrow[k] = (b < a.batch && k < a.nk) ? __bfloat162float(a.Y[b * a.nk + k]) : 0.f;
       }
-      __syncwarp();  // an edge's 8 threads share one warp
+      __syncwarp();  // an edge's 4 threads share one warp
       mbar_wait(x_full, tl & 1);
       const int64_t jc0 = static_cast<int64_t>(tl) * njobs;
       for (int n = 0; n < njobs; ++n) {
+        const int64_t jc = jc0 + n;
+        if (static_cast<int>(jc & 1) != grp) continue;
         const int4 job = meta.job[n];
-        // per component of the pair: U = hi + lo, both bf16 (the UMMA pair sees U
-        // to ~2^-16 relative, so the only bf16 roundings are the operands X, Y, W)
-        uint4 u[2], ul[2];
-        float2 a2[2][4];
+        float2 a2[2][8];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a2[h][q] = make_float2(0.f, 0.f);
+          for (int q = 0; q < 8; ++q) a2[h][q] = make_float2(0.f, 0.f);
         const int s0 = job.z & 0xFFFF, ns = job.z >> 16;
-#pragma unroll 2
+#pragma unroll kJUnroll
         for (int st = s0; st < s0 + ns; ++st) {
           const int4 js = meta.jstep[st];
           const int n0 = (js.x >> 4) & 3, n1 = (js.x >> 6) & 3;
-          const uint4 xv = *reinterpret_cast<const uint4*>(xrow + (js.x & 15) * 128);
+          const uint8_t* xp = xrow + (js.x & 15) * 128;
+          const uint4 xv0 = *reinterpret_cast<const uint4*>(xp);
+          const uint4 xv1 = *reinterpret_cast<const uint4*>(xp + 16);
           float c0 = __int_as_float(js.y) * yrow[(js.x >> 8) & 15];
           float c1 = __int_as_float(js.w) * yrow[(js.x >> 16) & 15];
           if (n0 > 1) c0 = fmaf(__int_as_float(js.z), yrow[(js.x >> 12) & 15], c0);
           if (n1 > 1) c1 = fmaf(meta.jv11[st], yrow[(js.x >> 20) & 15], c1);
-          const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
-          float2 xf[4];
+          float2 xf[8];
+          const __nv_bfloat162* xh0 = reinterpret_cast<const __nv_bfloat162*>(&xv0);
+          const __nv_bfloat162* xh1 = reinterpret_cast<const __nv_bfloat162*>(&xv1);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) xf[q] = __bfloat1622float2(xh[q]);
+          for (int q = 0; q < 4; ++q) {
+            xf[q] = __bfloat1622float2(xh0[q]);
+            xf[4 + q] = __bfloat1622float2(xh1[q]);
+          }
           if (n0) {  // uniform: every lane runs the same job
 #pragma unroll
-            for (int q = 0; q < 4; ++q) a2[0][q] = ffma2(c0, xf[q], a2[0][q]);
+            for (int q = 0; q < 8; ++q) a2[0][q] = ffma2(c0, xf[q], a2[0][q]);
           }
           if (n1) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) a2[1][q] = ffma2(c1, xf[q], a2[1][q]);
+            for (int q = 0; q < 8; ++q) a2[1][q] = ffma2(c1, xf[q], a2[1][q]);
           }
         }
+        // U = hi + lo, both bf16 (the UMMA pair sees U to ~2^-16 relative, so
+        // the only bf16 roundings are the operands X, Y, W)
+        mbar_wait(&u_empty[grp], static_cast<uint32_t>((jc >> 1) & 1) ^ 1);
+        uint8_t* U = Us + grp * kUSlot;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&u[h]);
-          __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&ul[h]);
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            ph[q] = __floats2bfloat162_rn(a2[h][q].x, a2[h][q].y);
-            const float2 back = __bfloat1622float2(ph[q]);
-            pl[q] = __floats2bfloat162_rn(a2[h][q].x - back.x, a2[h][q].y - back.y);
+          for (int c = 0; c < 2; ++c) {
+            uint4 hi, lo;
+            __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&hi);
+            __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&lo);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 v = a2[h][4 * c + q];
+              ph[q] = __floats2bfloat162_rn(v.x, v.y);
+              const float2 back = __bfloat1622float2(ph[q]);
+              pl[q] = __floats2bfloat162_rn(v.x - back.x, v.y - back.y);
+            }
+            *reinterpret_cast<uint4*>(U + rowo[h][c]) = hi;
+            *reinterpret_cast<uint4*>(U + kUHalf + rowo[h][c]) = lo;
           }
-        }
-        const int64_t jc = jc0 + n;
-        const int us = static_cast<int>(jc % kNU);
-        mbar_wait(&u_empty[us], ((jc / kNU) & 1) ^ 1);
-        uint8_t* U = Us + us * kUSlot;
-        *reinterpret_cast<uint4*>(U + row1) = u[0];
-        *reinterpret_cast<uint4*>(U + row2) = u[1];
-        *reinterpret_cast<uint4*>(U + kUHalf + row1) = ul[0];
-        *reinterpret_cast<uint4*>(U + kUHalf + row2) = ul[1];
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
-        if (lane == 0) mbar_arrive(&u_full[us]);
+        if (lane == 0) mbar_arrive(&u_full[grp]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(x_empty);  // X of this tile no longer read
@@ -584,7 +608,8 @@ extern "C" int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, 
                                            256, CU_TENSOR_MAP_SWIZZLE_NONE);
       TpArgs args{static_cast<const __nv_bfloat16*>(Y), Z, batch, static_cast<int>(p.nj),
                   static_cast<int>(p.nk), static_cast<int>(p.ni), accumulate};
-      const uint32_t smem = kXTile + kNU * kUSlot + kNW * kWTileTp + kEdges * 16 * 4 + 256 + 1024;
+      const uint32_t smem =
+          kXTile + kNU * kUSlot + kNW * kWTileTp + 2 * kEdges * 16 * 4 + 256 + 1024;
       static std::once_flag once;
       std::call_once(once, [&] {
         cuda_check(cudaFuncSetAttribute(tp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
