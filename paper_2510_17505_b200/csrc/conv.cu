@@ -241,9 +241,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // __syncthreads + commit round trip of this one-tile-per-CTA structure is
 // the floor. Not shipped:
 // - a persistent warp-specialised kernel (8-stage ring, producer warps,
-//   MMA warp, epilogue warps with double-buffered TMEM): 0.60-0.92 ms; the
-//   producers' proxy fence waits for all of a thread's cp.async, which
-//   serialises stages per warp;
+//   MMA warp, epilogue warps with double-buffered TMEM): 0.60-0.92 ms with
+//   producer-side wait + proxy fence (the fence waits for all of a thread's
+//   cp.async, serialising stages per warp), 0.78 ms with
+//   cp.async.mbarrier.arrive.noinc publishing (no producer waits, as
+//   CUTLASS's sm100 cp.async pipeline does) and the tile's Y rows in smem;
+//   one CTA per SM does not reach the 3-CTA kernel's throughput;
 // - deeper rings at this structure (s4d2 0.645 ms, s5d2 1.13 ms: fewer CTAs
 //   per SM);
 // - TMA tile::gather4 (1.0-3.2 ms; ~43 cycles per 512 B box per SM;
