@@ -187,3 +187,53 @@ def test_two_processes_share_gpu_sharded_gather(P, ixo):
         np.testing.assert_array_equal(res["groupcoo"], full.cpu().numpy())
         np.testing.assert_array_equal(res["bgcoo"], full16.cpu().numpy())
         np.testing.assert_array_equal(res["conv"], conv.cpu().numpy())
+
+
+def test_more_ranks_than_rows_empty_shards(P, ixo):
+    """world > output rows / voxels / edges: the empty shards build and
+    evaluate without error and the assembled outputs still equal one call."""
+    from paper_2510_17505_b200.distributed import (conv_shard_plan, edge_blocks, point_blocks,
+                                                   shard_plan, spmm_blockgroupcoo_slab,
+                                                   spmm_groupcoo_slab)
+    world = 8
+    rng = ixo.Rng(5)
+    a = ixo.synth_sparse_matrix(rng, 3, 40, 0.3)
+    b = ixo.synth_dense(rng, (40, 16))
+    fmt = P.dense_to_groupcoo(torch.from_numpy(a.astype(np.float32)).cuda(), g=0)
+    B = torch.from_numpy(b.astype(np.float32)).cuda()
+    full = torch.zeros((3, 16), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, B, full)
+    shards = shard_plan(fmt.AM.cpu().numpy(), 3, world)
+    assert sum(s.r1 - s.r0 for s in shards) == 3
+    out = torch.cat([spmm_groupcoo_slab(fmt, B, s) for s in shards])
+    assert torch.equal(out, full)
+
+    a16 = ixo.synth_block_sparse_matrix(rng, 32, 64, 16, 16, 0.5)
+    b16 = ixo.synth_dense(rng, (4, 16, 128))
+    f16 = P.dense_to_blockgroupcoo(bf16_dev(a16), 16, 16, 0)
+    full16 = torch.zeros((2, 16, 128), device="cuda")
+    P.spmm_blockgroupcoo(f16.AM, f16.AK, f16.AV, bf16_dev(b16), full16)
+    sh16 = shard_plan(f16.AM.cpu().numpy(), 2, world)
+    out16 = torch.cat([spmm_blockgroupcoo_slab(f16, bf16_dev(b16), s) for s in sh16])
+    assert torch.equal(out16, full16)
+
+    pts = np.array([[0, 0, 0], [0, 0, 1], [5, 5, 5]], np.int32)
+    mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+    g = np.random.default_rng(1)
+    In, W = bf16_dev(g.standard_normal((3, 64))), bf16_dev(g.standard_normal((27, 64, 64)))
+    gt = P.group_coo_tensor([3, 3, 27], [mo, mi, mz], torch.ones(mo.numel(), device="cuda"), 2, 4,
+                            canonical=True)
+    fullc = torch.zeros((3, 64), device="cuda")
+    P.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values, 3, 27,
+               3).run(In, W, fullc, accumulate=False)
+    parts = []
+    for s in point_blocks(3, world):
+        plan = conv_shard_plan(mo, mi, mz, 3, s, 4)
+        local = torch.zeros((s.r1 - s.r0, 64), device="cuda")
+        if s.r1 > s.r0:
+            plan.run(In, W, local, accumulate=False)
+        parts.append(local)
+    assert torch.equal(torch.cat(parts), fullc)
+
+    blocks = edge_blocks(5, world)
+    assert [s.r1 - s.r0 for s in blocks].count(0) == 3 and blocks[-1].r1 == 5
