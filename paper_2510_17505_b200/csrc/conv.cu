@@ -555,8 +555,7 @@ int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void*
                     reinterpret_cast<uintptr_t>(In) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(Weight) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(Out) % 16 == 0;
-    static const bool unit_off = getenv("IXB_CONV_NO_UNIT") != nullptr;  // A/B switch
-    if (tc && P->unit && !unit_off) {
+    if (tc && P->unit) {
       const CUtensorMap tmW =
           make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64, 64,
                        CU_TENSOR_MAP_SWIZZLE_128B);

@@ -530,8 +530,7 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
                                         CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tmAV = make_tmap_2d(AV, 16, G * g * 16, 32, 16, 16,
                                          CU_TENSOR_MAP_SWIZZLE_32B);
-    static const int sleep_ns = getenv("IXB_BG_SLEEP") ? atoi(getenv("IXB_BG_SLEEP")) : 256;
-    a.epi_sleep_ns = sleep_ns;
+    a.epi_sleep_ns = 256;  // back-off of the idle epilogue warps' barrier polls
     // 2 slots per stage, 4 stages: ~68 KB -> 3 CTAs (3 independent issue
     // streams) per SM; measured against 1, 4, 8, 12 slots per stage and
     // 1-5 CTAs/SM on cfg2 (profiles/k4_diag_r1.md)
