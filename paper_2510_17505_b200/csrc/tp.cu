@@ -165,14 +165,14 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       int64_t wc = 0;  // W loads issued
       int tl = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-        mbar_wait(x_empty, (tl & 1) ^ 1);  // previous tile's X fully consumed
+        mbar_wait_backoff(x_empty, (tl & 1) ^ 1, 128);  // previous tile's X fully consumed
         mbar_arrive_expect_tx(x_full, x_bytes);
         for (int r0 = 0; r0 < kEdges * a.nj; r0 += 256)
           tma_load_2d(Xs + r0 * 128, &tmX, x_full, 0,
                       static_cast<int32_t>(tile * kEdges * a.nj + r0), stream);
         for (int ps = 0; ps < npaths; ++ps, ++wc) {
           const int slot = static_cast<int>(wc % kNW);
-          mbar_wait(&w_empty[slot], ((wc / kNW) & 1) ^ 1);
+          mbar_wait_backoff(&w_empty[slot], ((wc / kNW) & 1) ^ 1, 64);
           mbar_arrive_expect_tx(&w_full[slot], kWTileTp);
           tma_load_2d(Ws + slot * kWTileTp, &tmW, &w_full[slot], 0, meta.path_l[ps] * 64, keep);
         }
@@ -225,16 +225,20 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     // behind math. A thread owns one edge and 16 u of both components.
     const int grp = warp / kGroupWarps;
     const int gt = tid - grp * kGroupWarps * 32;
-    const int b_loc = gt >> 2, slice = gt & 3;  // edge in tile, u slice [16*slice, +16)
-    uint32_t rowo[2][2];                        // [component][8-u chunk] in the SW128 U tile
+    const int b_loc = gt >> 2, slice = gt & 3;  // edge in tile, u chunks {slice, slice + 4}
+    // A thread owns the 8-u chunks cA, cB = {slice, slice + 4}, odd edges in
+    // swapped order: each X load of a warp (8 edges x 4 lanes, edge rows 2 KB
+    // apart) then covers both 64 B halves of the banks, conflict-free.
+    const int cA = slice + 4 * (b_loc & 1), cB = slice + 4 * (~b_loc & 1);
+    uint32_t rowo[2][2];  // [component][chunk A/B] in the SW128 U tile
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int r = h * 64 + b_loc, ch = 2 * slice + c;
+        const int r = h * 64 + b_loc, ch = c ? cB : cA;
         rowo[h][c] = r * 128 + ((ch ^ (r & 7)) << 4);
       }
-    const uint8_t* xrow = Xs + b_loc * a.nj * 128 + slice * 32;
+    const uint8_t* xrow = Xs + b_loc * a.nj * 128;
     float* yrow = Ys + (grp * kEdges + b_loc) * 16;
     int tl = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
@@ -257,13 +261,15 @@ __global__ void __launch_bounds__(kTpThreads, 1)
 #pragma unroll
           for (int q = 0; q < 8; ++q) a2[h][q] = make_float2(0.f, 0.f);
         const int s0 = job.z & 0xFFFF, ns = job.z >> 16;
+        int4 js_next = ns > 0 ? meta.jstep[s0] : make_int4(0, 0, 0, 0);
 #pragma unroll kJUnroll
         for (int st = s0; st < s0 + ns; ++st) {
-          const int4 js = meta.jstep[st];
+          const int4 js = js_next;
+          if (st + 1 < s0 + ns) js_next = meta.jstep[st + 1];  // next entry in flight
           const int n0 = (js.x >> 4) & 3, n1 = (js.x >> 6) & 3;
           const uint8_t* xp = xrow + (js.x & 15) * 128;
-          const uint4 xv0 = *reinterpret_cast<const uint4*>(xp);
-          const uint4 xv1 = *reinterpret_cast<const uint4*>(xp + 16);
+          const uint4 xv0 = *reinterpret_cast<const uint4*>(xp + cA * 16);
+          const uint4 xv1 = *reinterpret_cast<const uint4*>(xp + cB * 16);
           float c0 = __int_as_float(js.y) * yrow[(js.x >> 8) & 15];
           float c1 = __int_as_float(js.w) * yrow[(js.x >> 16) & 15];
           if (n0 > 1) c0 = fmaf(__int_as_float(js.z), yrow[(js.x >> 12) & 15], c0);
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
             for (int c = 0; c < 16; ++c) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
           continue;
         }
-        mbar_wait(&acc_full[cp], tl & 1);
+        mbar_wait_backoff(&acc_full[cp], tl & 1, 256);  // idle polls would steal math issue slots
         tc_fence_after();
         const bool has = comp < a.ni && ((meta.present >> comp) & 1);
 #pragma unroll 1
