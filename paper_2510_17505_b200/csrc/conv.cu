@@ -236,7 +236,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // accumulates its offsets in z order.
 // Measured on cfg5 (1 M voxels): 0.83 ms (conv_tc_kernel) -> 0.65 ms
 // (register prefetch, one row per thread) -> 0.567 ms (coalesced gather) ->
-// 0.513 ms (cp.async, 3-stage ring). Switching parts off: no gather
+// 0.513 ms (cp.async, 3-stage ring) -> 0.477 ms (2-stage ring, 4 CTAs/SM).
+// Switching parts off (3-stage ring): no gather
 // 0.512 ms, no MMA 0.413 ms, neither (nor W) 0.390 ms — the per-offset
 // __syncthreads + commit round trip of this one-tile-per-CTA structure is
 // the floor. Not shipped:
@@ -266,13 +267,20 @@ struct UnitArgs {
 // rows land in A[k % S] by cp.async (coalesced: 8 lanes share a 128 B row,
 // so a warp instruction covers 4 whole rows; the row's input index comes
 // from its owner lane by shuffle; absent rows are zero-filled) and W[z] in
-// W[k % S] by TMA, issued D = 2 stages ahead of the MMA. A ring of S = 3
-// (72 KB) keeps 3 CTAs per SM.
-constexpr int kUnitStages = 3;
-constexpr int kUnitDist = 2;
+// W[k % S] by TMA, issued D stages ahead of the MMA.
+// 2 stages issued 1 ahead (48 KB -> 4 CTAs per SM) beat 3 stages issued 2
+// ahead (72 KB -> 3 CTAs): 0.477 vs 0.510 ms on cfg5. More CTAs per SM
+// outweigh a deeper per-CTA ring here.
+#ifndef IXB_CONV_STAGES
+#define IXB_CONV_STAGES 2
+#define IXB_CONV_DIST 1
+#define IXB_CONV_MINB 4
+#endif
+constexpr int kUnitStages = IXB_CONV_STAGES;
+constexpr int kUnitDist = IXB_CONV_DIST;
 constexpr uint32_t kUnitSmem = kUnitStages * (kATile + kWTile) + 1024 + 256;
 
-__global__ void __launch_bounds__(kConvThreads, 3)
+__global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
     conv_unit_kernel(const __grid_constant__ CUtensorMap tmW, UnitArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
