@@ -779,9 +779,10 @@ def run_b200(args, wl):
                 "hbm_compulsory_frac": wl.alg_bytes / kern_s / 1e9 / hbm,
                 "l2_gather_GBps": wl.gather_bytes / kern_s / 1e9}
         if hasattr(wl, "mma_count"):
-            # measured tcgen05 cost of an M=128,K=16 MMA with N <= 64 (tools/umma_rate.cu,
-            # profiles/k4_diag_r1.md): the per-instruction floor, not flops, bounds 16-wide blocks
-            floor_s = wl.mma_count * 48.0 / (torch.cuda.get_device_properties(dev).multi_processor_count
+            # measured tensor-pipe occupancy of an M=128,N=16,K=16 MMA with >= 2 issuing CTAs
+            # per SM: 38.8 cycles (tools/umma_pair_rate.cu, profiles/k4_diag_r1.md §8); the
+            # per-instruction floor, not flops, bounds 16-wide blocks
+            floor_s = wl.mma_count * 38.8 / (torch.cuda.get_device_properties(dev).multi_processor_count
                                               * 1.965e9)
             roof["mma_issue_floor_us"] = floor_s * 1e6
             roof["frac_of_mma_issue_floor"] = floor_s / kern_s
