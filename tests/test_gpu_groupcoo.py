@@ -291,3 +291,60 @@ def test_virtual_rank_shards_bit_identical(P, ixo, world):
     for s in shards:
         out[s.r0:s.r1] = spmm_groupcoo_slab(fmt, B, s)
     assert torch.equal(out, full)
+
+
+@pytest.mark.parametrize("N", [128, 256])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_dense_rows_bit_exact(P, ixo, N, accumulate):
+    """Long rows (>= 1024 slots per row on average, the cfg3 d = 0.30 regime):
+    integer-valued data match the oracle exactly, for `=` and `+=`, with
+    empty rows."""
+    rng = ixo.Rng(17)
+    M, K = 70, 2100
+    a = ixo.synth_sparse_matrix(rng, M, K, 0.6, ixo.INT)
+    a[5] = 0
+    a[40:43] = 0
+    b = ixo.synth_dense(rng, (K, N), ixo.INT)
+    fmt = P.dense_to_groupcoo(torch.from_numpy(a).float().cuda(), g=8)
+    assert fmt.AK.numel() >= 1024 * M
+    c0 = ixo.synth_dense(rng, (M, N), ixo.INT)
+    C = torch.from_numpy(c0).float().cuda() if accumulate else torch.zeros((M, N), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, torch.from_numpy(b).float().cuda(), C,
+                    accumulate=accumulate)
+    r, c, v = ixo.dense_to_coo(a)
+    want_f = ixo.coo_to_groupcoo(M, K, r, c, v, 0, 8)
+    expr = "C[AM[p],n] += AV[p,q] * B[AK[p,q],n]"
+    want = ixo.einsum(expr if accumulate else expr.replace("+=", "="),
+                      {"AM": want_f["AM"], "AK": want_f["AK"], "AV": want_f["AV"], "B": b}, "C",
+                      c0.astype(np.int64) if accumulate else np.zeros((M, N), np.int64))
+    np.testing.assert_array_equal(C.cpu().numpy().astype(np.int64), want)
+
+
+def test_dense_rows_fp32_column_invariance_and_unsorted_members(P, ixo):
+    """fp32 long rows: N = 256 and N = 192 on the same columns give the same
+    bits (per-element summation order does not depend on N); a hand-built
+    format whose AK is not ascending within a row matches the oracle (fp32
+    sums of ~1200 terms per row: the sequential fp32 accumulation, not the
+    kernel, sets the 1e-4 bound)."""
+    rng = ixo.Rng(23)
+    M, K, N = 40, 1500, 256
+    a = ixo.synth_sparse_matrix(rng, M, K, 0.8)
+    b = ixo.synth_dense(rng, (K, N))
+    A = torch.from_numpy(a.astype(np.float32)).cuda()
+    B = torch.from_numpy(b.astype(np.float32)).cuda()
+    fmt = P.dense_to_groupcoo(A, g=16)
+    assert fmt.AK.numel() >= 1024 * M
+    C = torch.zeros((M, N), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, B, C)
+    C192 = torch.zeros((M, 192), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, B[:, :192].contiguous(), C192)
+    assert torch.equal(C[:, :192], C192)
+    # reverse the member order of every group: rows stay grouped, AK descends
+    AK = fmt.AK.flip(1).contiguous()
+    AV = fmt.AV.flip(1).contiguous()
+    C2 = torch.zeros((M, N), device="cuda")
+    P.spmm_groupcoo(fmt.AM, AK, AV, B, C2)
+    t = {"AM": fmt.AM.cpu().numpy().astype(np.int64), "AK": AK.cpu().numpy().astype(np.int64),
+         "AV": AV.double().cpu().numpy(), "B": b.astype(np.float32).astype(np.float64)}
+    want2 = ixo.einsum("C[AM[p],n] += AV[p,q] * B[AK[p,q],n]", t, "C", np.zeros((M, N)))
+    assert ixo.max_rel_error(want2, C2.double().cpu().numpy()) <= 1e-4
