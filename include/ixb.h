@@ -230,6 +230,14 @@ int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const int32_t* CG
 int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, const void* W, int64_t batch,
                     float* Z, int accumulate, int flags, ixb_stream stream);
 void ixb_tp_plan_free(ixb_tp_plan* plan);
+/* Host-buffer form of ixb_tp_plan_run: X [batch, nj, U] bf16, Y [batch, nk]
+ * bf16 and Z [batch, ni, Wd] fp32 are HOST arrays (pinned for overlap), W a
+ * device array. The batch is cut into `nchunks` runs of whole 64-edge tiles
+ * whose copy-in, evaluation and copy-out overlap on three streams; returns
+ * with Z written, bit-identical to the device-buffer call. */
+int ixb_tp_plan_run_host(ixb_tp_plan* plan, const void* X, const void* Y, const void* W,
+                         int64_t batch, float* Z, int accumulate, int flags, int nchunks,
+                         ixb_stream stream);
 
 /* Host-buffer forms of the SpMM evaluators (the shape of the reference's
  * execute_mode: host Tensors in, host result out). All arrays are HOST

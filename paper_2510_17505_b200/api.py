@@ -363,6 +363,17 @@ class TpPlan:
                                     int(accumulate), flags, _stream(stream)))
         return Z
 
+    def run_host(self, X, Y, W, Z, accumulate=True, flags=0, nchunks=8, stream=None):
+        """X, Y, Z: host tensors (pinned for overlap); W: device. Chunked
+        copy-in / evaluate / copy-out on three streams (ixb_tp_plan_run_host)."""
+        for t in (X, Y, Z):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("run_host takes contiguous host tensors for X, Y and Z")
+        check(lib().ixb_tp_plan_run_host(self.h, _ptr(X), _ptr(Y), _ptr(W), X.shape[0],
+                                         _ptr(Z), int(accumulate), flags, nchunks,
+                                         _stream(stream)))
+        return Z
+
     def __del__(self):
         if getattr(self, "h", None):
             self._free(self.h)

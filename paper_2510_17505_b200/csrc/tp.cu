@@ -638,6 +638,86 @@ extern "C" int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, 
   });
 }
 
+namespace {
+// Side streams and events for the host-buffer form, created once per thread
+// and device (as in pipeline.cpp).
+struct TpStreams {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int device = -1;
+  void ensure(size_t nev) {
+    int dev = 0;
+    IXB_CUDA_CHECK(cudaGetDevice(&dev));
+    if (device != dev) {
+      IXB_CUDA_CHECK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+      IXB_CUDA_CHECK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+      ev.clear();
+      device = dev;
+    }
+    while (ev.size() < nev) {
+      cudaEvent_t e;
+      IXB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+  }
+};
+thread_local TpStreams t_tp_streams;
+}  // namespace
+
+// Host-buffer form: X, Y and Z in host memory (pinned for overlap), W on the
+// device. Edges are independent, so the batch is cut into chunks of whole
+// 64-edge tiles; chunk i's X/Y copy in, its evaluation and its Z copy out
+// run on three streams, so both PCIe directions and the kernels overlap.
+// Each edge is evaluated exactly as by ixb_tp_plan_run (bit-identical).
+extern "C" int ixb_tp_plan_run_host(ixb_tp_plan* plan, const void* X, const void* Y,
+                                    const void* W, int64_t batch, float* Z, int accumulate,
+                                    int flags, int nchunks, ixb_stream stream) {
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (!plan) fail(IXB_SHAPE, "ixb_tp_plan_run: null plan");
+    if (batch < 0) fail(IXB_SHAPE, "ixb_tp_grouped: bad extents");
+    const ixb_tp_plan& p = *plan;
+    if (batch == 0 || p.ni == 0) return;
+    const int64_t xrow = p.nj * p.U * 2, yrow = p.nk * 2, zrow = p.ni * p.Wd * 4;
+    const int64_t wrow = p.w_per_batch ? p.nl * p.U * p.Wd * 2 : 0;  // per-edge W offset
+    if (nchunks < 1) nchunks = 1;
+    int64_t chunk = (batch + nchunks - 1) / nchunks;
+    chunk = (chunk + kEdges - 1) / kEdges * kEdges;
+    nchunks = static_cast<int>((batch + chunk - 1) / chunk);
+    Scratch<char> dX(batch * xrow, s), dY(batch * yrow, s), dZ(batch * zrow, s);
+    TpStreams& st = t_tp_streams;
+    st.ensure(2 + 2 * nchunks);
+    IXB_CUDA_CHECK(cudaEventRecord(st.ev[0], s));  // scratch allocated on s
+    IXB_CUDA_CHECK(cudaStreamWaitEvent(st.h2d, st.ev[0], 0));
+    for (int i = 0; i < nchunks; ++i) {
+      const int64_t b0 = i * chunk, n = batch - b0 < chunk ? batch - b0 : chunk;
+      cudaEvent_t in = st.ev[2 + 2 * i], out = st.ev[3 + 2 * i];
+      IXB_CUDA_CHECK(cudaMemcpyAsync(dX.p + b0 * xrow, static_cast<const char*>(X) + b0 * xrow,
+                                     n * xrow, cudaMemcpyHostToDevice, st.h2d));
+      IXB_CUDA_CHECK(cudaMemcpyAsync(dY.p + b0 * yrow, static_cast<const char*>(Y) + b0 * yrow,
+                                     n * yrow, cudaMemcpyHostToDevice, st.h2d));
+      if (accumulate)
+        IXB_CUDA_CHECK(cudaMemcpyAsync(dZ.p + b0 * zrow,
+                                       reinterpret_cast<const char*>(Z) + b0 * zrow, n * zrow,
+                                       cudaMemcpyHostToDevice, st.h2d));
+      IXB_CUDA_CHECK(cudaEventRecord(in, st.h2d));
+      IXB_CUDA_CHECK(cudaStreamWaitEvent(s, in, 0));
+      const int rc = ixb_tp_plan_run(plan, dX.p + b0 * xrow, dY.p + b0 * yrow,
+                                     static_cast<const char*>(W) + b0 * wrow, n,
+                                     reinterpret_cast<float*>(dZ.p + b0 * zrow), accumulate,
+                                     flags, stream);
+      if (rc != IXB_OK) fail(rc, ixb_last_error());
+      IXB_CUDA_CHECK(cudaEventRecord(out, s));
+      IXB_CUDA_CHECK(cudaStreamWaitEvent(st.d2h, out, 0));
+      IXB_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(Z) + b0 * zrow, dZ.p + b0 * zrow,
+                                     n * zrow, cudaMemcpyDeviceToHost, st.d2h));
+    }
+    IXB_CUDA_CHECK(cudaEventRecord(st.ev[1], st.d2h));
+    IXB_CUDA_CHECK(cudaStreamWaitEvent(s, st.ev[1], 0));
+    IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // Z is in host memory on return
+  });
+}
+
 extern "C" void ixb_tp_plan_free(ixb_tp_plan* plan) {
   if (!plan) return;
   cudaFree(plan->d_rowptr);  // synchronous: in-flight runs finish first

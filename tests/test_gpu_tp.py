@@ -171,3 +171,24 @@ def test_tp_plan_reuse_matches_one_shot(P, ixo):
         P.TpPlan(bad["CGL"], bad["CGI"], bad["CGJ"], bad["CGK"], bad["CGV"], ni, nj, nk, nl2, U,
                  Wd, w_per_batch=True)
     assert "index tensor CGK value 99 at position [1] out of range for dim 1 of Y" in str(e.value)
+
+
+@pytest.mark.parametrize("nchunks", [1, 3, 8])
+def test_tp_plan_run_host_matches_device(P, ixo, nchunks):
+    """The host-buffer pipelined form (chunks of whole 64-edge tiles) equals
+    the device call bit for bit, for `=` and `+=`, with a ragged last chunk."""
+    cg, nl = cg_grouped(P, ixo, 4)
+    dev = {k: cuda(v, torch.float32 if k == "CGV" else torch.int32) for k, v in cg.items()}
+    plan = P.TpPlan(dev["CGL"], dev["CGI"], dev["CGJ"], dev["CGK"], dev["CGV"], 16, 16, 16, nl)
+    rng = ixo.Rng(31)
+    B = 333
+    X = torch.from_numpy(bf16_round(ixo.synth_dense(rng, (B, 16, 64)))).to(torch.bfloat16)
+    Y = torch.from_numpy(bf16_round(ixo.synth_dense(rng, (B, 16)))).to(torch.bfloat16)
+    W = cuda(bf16_round(ixo.synth_dense(rng, (nl, 64, 64))), torch.bfloat16)
+    Z0 = torch.from_numpy(ixo.synth_dense(rng, (B, 16, 64))).float()
+    for acc in (False, True):
+        Zd = Z0.cuda() if acc else torch.zeros((B, 16, 64), device="cuda")
+        plan.run(X.cuda(), Y.cuda(), W, Zd, accumulate=acc)
+        Zh = Z0.clone().pin_memory() if acc else torch.zeros((B, 16, 64)).pin_memory()
+        plan.run_host(X.pin_memory(), Y.pin_memory(), W, Zh, accumulate=acc, nchunks=nchunks)
+        assert torch.equal(Zh, Zd.cpu())
