@@ -204,6 +204,15 @@ int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t
                          int64_t n_out, int flags, ixb_stream stream, ixb_conv_plan** plan);
 int ixb_conv_plan_run(ixb_conv_plan* plan, const void* In, int64_t Cin, const void* Weight,
                       int64_t Cout, float* Out, int accumulate, int flags, ixb_stream stream);
+/* Host-buffer form of ixb_conv_plan_run: In [n_in, Cin] bf16 and Out
+ * [n_out, Cout] fp32 are HOST arrays (pinned for overlap), Weight a device
+ * array. Builder-made (unit) maps run in `nchunks` groups of output tiles:
+ * In streams in row order and each group starts once the input rows it reads
+ * have landed, while earlier groups' Out rows copy back. Returns with Out
+ * written, bit-identical to the device-buffer call. */
+int ixb_conv_plan_run_host(ixb_conv_plan* plan, const void* In, int64_t Cin, const void* Weight,
+                           int64_t Cout, float* Out, int accumulate, int flags, int nchunks,
+                           ixb_stream stream);
 void ixb_conv_plan_free(ixb_conv_plan* plan);
 
 /* K7 — grouped Clebsch–Gordan tensor product,

@@ -85,6 +85,9 @@ _SIGS = {
                              [C.c_int, C.c_void_p, C.c_void_p]),
     "ixb_conv_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                     C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ixb_conv_plan_run_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                         C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                         C.c_void_p]),
     "ixb_conv_plan_free": (None, [C.c_void_p]),
     "ixb_conv_grouped": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,

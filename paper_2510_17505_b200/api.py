@@ -257,6 +257,17 @@ class ConvPlan:
                                       _stream(stream)))
         return Out
 
+    def run_host(self, In, Weight, Out, accumulate=True, flags=0, nchunks=8, stream=None):
+        """In, Out: host tensors (pinned for overlap); Weight: device. Output
+        tiles run in chunks as their input rows land (ixb_conv_plan_run_host)."""
+        for t in (In, Out):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("run_host takes contiguous host tensors for In and Out")
+        check(lib().ixb_conv_plan_run_host(self.h, _ptr(In), In.shape[1], _ptr(Weight),
+                                           Weight.shape[2], _ptr(Out), int(accumulate), flags,
+                                           nchunks, _stream(stream)))
+        return Out
+
     def __del__(self):
         if getattr(self, "h", None):
             self._free(self.h)

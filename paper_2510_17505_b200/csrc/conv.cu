@@ -25,7 +25,9 @@
 
 #include <cstdlib>
 #include <memory>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -261,6 +263,7 @@ struct UnitArgs {
   float* Out;
   int64_t n_out;
   int accumulate;
+  int64_t tile0;              // first 128-row tile of this launch (host pipeline chunks)
 };
 
 // Stage k of a tile = its k-th used offset z: the In rows of the 128 output
@@ -303,7 +306,8 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
     tmem_alloc(tmem_slot, 64);
     tmem_relinquish();
   }
-  const int64_t x = static_cast<int64_t>(blockIdx.x) * 128 + tid;
+  const int64_t tile = a.tile0 + blockIdx.x;
+  const int64_t x = tile * 128 + tid;
   const bool row_ok = x < a.n_out;
   // this row's input rows for all offsets (y + 1), one vectorised read
   int yr[kOffPad];
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
 #pragma unroll
     for (int j = 0; j < kOffPad; ++j) yr[j] = 0;
   }
-  const uint32_t tmask = a.tile_mask[blockIdx.x];
+  const uint32_t tmask = a.tile_mask[tile];
   const int nk = __popc(tmask);
   tc_fence_before();
   __syncthreads();
@@ -419,7 +423,8 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
 
 // Y[x * kOffPad + z] = MAPY[T[x, z]] + 1 (0 = absent); tile masks of used offsets.
 __global__ void conv_ytable_kernel(const int32_t* T, const int32_t* MAPY, int64_t n_out,
-                                   int64_t n_off, int32_t* Y, uint32_t* tile_mask) {
+                                   int64_t n_off, int32_t* Y, uint32_t* tile_mask,
+                                   int32_t* tile_need) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_out * kOffPad) return;
   const int64_t x = i / kOffPad, z = i % kOffPad;
@@ -429,6 +434,7 @@ __global__ void conv_ytable_kernel(const int32_t* T, const int32_t* MAPY, int64_
     if (s >= 0) {
       v = MAPY[s] + 1;
       atomicOr(&tile_mask[x / 128], 1u << z);
+      atomicMax(&tile_need[x / 128], v);  // input rows [0, v) hold this tile's inputs
     }
   }
   Y[i] = v;
@@ -489,9 +495,52 @@ struct ixb_conv_plan {
   bool unit = false;  // every real slot has MAPV == 1: conv_unit_kernel usable
   ixb::Scratch<int32_t> T, perm, rowptr, Y;
   ixb::Scratch<uint32_t> tile_mask;
+  std::vector<int32_t> tile_need;  // per 128-row tile: input rows [0, need) it reads
 };
 
 using namespace ixb;
+
+namespace {
+// conv_unit_kernel over the 128-row tiles [tile0, tile0 + ntiles)
+void launch_unit(const ixb_conv_plan* P, const void* In, const void* Weight, float* Out,
+                 int accumulate, int64_t tile0, int64_t ntiles, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  const CUtensorMap tmW = make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64,
+                                       64, CU_TENSOR_MAP_SWIZZLE_128B);
+  UnitArgs ua{P->Y.p, P->tile_mask.p, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
+              accumulate, tile0};
+  static std::once_flag once_u;
+  std::call_once(once_u, [&] {
+    cuda_check(cudaFuncSetAttribute(conv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kUnitSmem),
+               "cudaFuncSetAttribute(conv_unit_kernel)");
+  });
+  conv_unit_kernel<<<static_cast<unsigned>(ntiles), kConvThreads, kUnitSmem, s>>>(tmW, ua);
+  IXB_LAUNCH_CHECK("conv_unit_kernel");
+}
+
+struct ConvStreams {  // side streams + events of the host-buffer form, per thread and device
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int device = -1;
+  void ensure(size_t nev) {
+    int dev = 0;
+    IXB_CUDA_CHECK(cudaGetDevice(&dev));
+    if (device != dev) {
+      IXB_CUDA_CHECK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+      IXB_CUDA_CHECK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+      ev.clear();
+      device = dev;
+    }
+    while (ev.size() < nev) {
+      cudaEvent_t e;
+      IXB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+  }
+};
+thread_local ConvStreams t_conv_streams;
+}  // namespace
 
 extern "C" {
 
@@ -540,9 +589,14 @@ int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t
       P->Y = Scratch<int32_t>(n_out * kOffPad, s);
       P->tile_mask = Scratch<uint32_t>(ntiles, s);
       IXB_CUDA_CHECK(cudaMemsetAsync(P->tile_mask.p, 0, ntiles * 4, s));
-      conv_ytable_kernel<<<ceil_div(n_out * kOffPad, 256), 256, 0, s>>>(P->T.p, MAPY, n_out, n_off,
-                                                                       P->Y.p, P->tile_mask.p);
+      Scratch<int32_t> need(ntiles, s);
+      IXB_CUDA_CHECK(cudaMemsetAsync(need.p, 0, ntiles * 4, s));
+      conv_ytable_kernel<<<ceil_div(n_out * kOffPad, 256), 256, 0, s>>>(
+          P->T.p, MAPY, n_out, n_off, P->Y.p, P->tile_mask.p, need.p);
       IXB_LAUNCH_CHECK("conv_ytable_kernel");
+      P->tile_need.resize(ntiles);
+      IXB_CUDA_CHECK(cudaMemcpyAsync(P->tile_need.data(), need.p, ntiles * 4,
+                                     cudaMemcpyDeviceToHost, s));
       IXB_CUDA_CHECK(cudaStreamSynchronize(s));
     }
     *plan = P.release();
@@ -564,20 +618,7 @@ int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void*
                     reinterpret_cast<uintptr_t>(Weight) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(Out) % 16 == 0;
     if (tc && P->unit) {
-      const CUtensorMap tmW =
-          make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64, 64,
-                       CU_TENSOR_MAP_SWIZZLE_128B);
-      UnitArgs ua{P->Y.p, P->tile_mask.p, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
-                  accumulate};
-      const uint32_t smem = kUnitSmem;
-      static std::once_flag once_u;
-      std::call_once(once_u, [&] {
-        cuda_check(cudaFuncSetAttribute(conv_unit_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                   "cudaFuncSetAttribute(conv_unit_kernel)");
-      });
-      conv_unit_kernel<<<ceil_div(P->n_out, 128), kConvThreads, smem, s>>>(tmW, ua);
-      IXB_LAUNCH_CHECK("conv_unit_kernel");
+      launch_unit(P, In, Weight, Out, accumulate, 0, ceil_div(P->n_out, 128), s);
       return;
     }
     if (tc) {
@@ -636,6 +677,76 @@ int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void*
         static_cast<const __nv_bfloat16*>(In), Cin, static_cast<const __nv_bfloat16*>(Weight),
         Cout, Out, P->n_out, accumulate);
     IXB_LAUNCH_CHECK("conv_csr_kernel");
+  });
+}
+
+// Host-buffer form: In [n_in, Cin] bf16 and Out [n_out, Cout] fp32 in host
+// memory (pinned for overlap), Weight on the device. With the unit kernel the
+// output tiles run in `nchunks` groups: In is copied in row order, and each
+// group starts once the input rows its tiles read (recorded per tile by the
+// plan) have landed, while the previous group's Out rows copy back. Other
+// maps copy In, evaluate, and copy Out back in sequence. Results are
+// bit-identical to ixb_conv_plan_run.
+int ixb_conv_plan_run_host(ixb_conv_plan* P, const void* In, int64_t Cin, const void* Weight,
+                           int64_t Cout, float* Out, int accumulate, int flags, int nchunks,
+                           ixb_stream stream) {
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (!P) fail(IXB_FAILURE, "null conv plan");
+    if (Cin < 1 || Cout < 1) fail(IXB_SHAPE, "conv: channel counts must be >= 1");
+    if (P->n_out == 0) return;
+    const int64_t in_row = Cin * 2, out_row = Cout * 4;
+    Scratch<char> dIn(P->n_in * in_row, s), dOut(P->n_out * out_row, s);
+    const bool pipelined = !P->conflict && Cin == 64 && Cout == 64 && P->unit &&
+                           reinterpret_cast<uintptr_t>(Weight) % 16 == 0 && nchunks > 1;
+    if (!pipelined) {
+      IXB_CUDA_CHECK(cudaMemcpyAsync(dIn.p, In, P->n_in * in_row, cudaMemcpyHostToDevice, s));
+      if (accumulate)
+        IXB_CUDA_CHECK(cudaMemcpyAsync(dOut.p, Out, P->n_out * out_row, cudaMemcpyHostToDevice, s));
+      const int rc = ixb_conv_plan_run(P, dIn.p, Cin, Weight, Cout,
+                                       reinterpret_cast<float*>(dOut.p), accumulate, flags, stream);
+      if (rc != IXB_OK) fail(rc, ixb_last_error());
+      IXB_CUDA_CHECK(cudaMemcpyAsync(Out, dOut.p, P->n_out * out_row, cudaMemcpyDeviceToHost, s));
+      IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+      return;
+    }
+    const int64_t ntiles = ceil_div(P->n_out, 128);
+    if (nchunks > ntiles) nchunks = static_cast<int>(ntiles);
+    ConvStreams& st = t_conv_streams;
+    st.ensure(2 + 2 * nchunks);
+    IXB_CUDA_CHECK(cudaEventRecord(st.ev[0], s));  // scratch allocated on s
+    IXB_CUDA_CHECK(cudaStreamWaitEvent(st.h2d, st.ev[0], 0));
+    int64_t copied = 0;  // In rows [0, copied) are on their way
+    for (int i = 0; i < nchunks; ++i) {
+      const int64_t t0 = ntiles * i / nchunks, t1 = ntiles * (i + 1) / nchunks;
+      int64_t need = 0;
+      for (int64_t t = t0; t < t1; ++t) need = std::max<int64_t>(need, P->tile_need[t]);
+      if (i == nchunks - 1) need = P->n_in;  // the rest of In (unread rows are harmless)
+      if (need > copied) {
+        IXB_CUDA_CHECK(cudaMemcpyAsync(dIn.p + copied * in_row,
+                                       static_cast<const char*>(In) + copied * in_row,
+                                       (need - copied) * in_row, cudaMemcpyHostToDevice, st.h2d));
+        copied = need;
+      }
+      const int64_t r0 = t0 * 128, r1 = std::min<int64_t>(t1 * 128, P->n_out);
+      if (accumulate && r1 > r0)
+        IXB_CUDA_CHECK(cudaMemcpyAsync(dOut.p + r0 * out_row,
+                                       reinterpret_cast<const char*>(Out) + r0 * out_row,
+                                       (r1 - r0) * out_row, cudaMemcpyHostToDevice, st.h2d));
+      cudaEvent_t in_ev = st.ev[2 + 2 * i], out_ev = st.ev[3 + 2 * i];
+      IXB_CUDA_CHECK(cudaEventRecord(in_ev, st.h2d));
+      IXB_CUDA_CHECK(cudaStreamWaitEvent(s, in_ev, 0));
+      launch_unit(P, dIn.p, Weight, reinterpret_cast<float*>(dOut.p), accumulate, t0, t1 - t0, s);
+      IXB_CUDA_CHECK(cudaEventRecord(out_ev, s));
+      IXB_CUDA_CHECK(cudaStreamWaitEvent(st.d2h, out_ev, 0));
+      if (r1 > r0)
+        IXB_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(Out) + r0 * out_row,
+                                       dOut.p + r0 * out_row, (r1 - r0) * out_row,
+                                       cudaMemcpyDeviceToHost, st.d2h));
+    }
+    IXB_CUDA_CHECK(cudaEventRecord(st.ev[1], st.d2h));
+    IXB_CUDA_CHECK(cudaStreamWaitEvent(s, st.ev[1], 0));
+    IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // Out is in host memory on return
   });
 }
 

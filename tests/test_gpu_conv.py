@@ -182,3 +182,28 @@ def test_conv_index_errors(P, ixo):
     with pytest.raises(P.IndexRangeError) as e:
         run_conv(P, t, n, n, 27)
     assert "index tensor MAPX value -1 at position [2]" in str(e.value)
+
+
+@pytest.mark.parametrize("nchunks", [1, 2, 5])
+def test_conv_plan_run_host_matches_device(P, nchunks):
+    """Host-buffer form (output-tile chunks started as their input rows land)
+    equals the device call bit for bit, for `=` and `+=`."""
+    g = np.random.default_rng(4)
+    pts = np.unique(g.integers(0, 20, (3000, 3)), axis=0).astype(np.int32)
+    order = np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0]))  # sorted voxels: local windows
+    pts = pts[order]
+    n = len(pts)
+    mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+    gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], torch.ones(mo.numel(), device="cuda"), 2,
+                            16, canonical=True)
+    plan = P.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values, n, 27,
+                      n)
+    In = torch.from_numpy(g.standard_normal((n, 64))).to(torch.bfloat16)
+    W = torch.from_numpy(g.standard_normal((27, 64, 64)) * 0.1).to(torch.bfloat16).cuda()
+    O0 = torch.from_numpy(g.standard_normal((n, 64))).float()
+    for acc in (False, True):
+        Od = O0.cuda() if acc else torch.zeros((n, 64), device="cuda")
+        plan.run(In.cuda(), W, Od, accumulate=acc)
+        Oh = O0.clone().pin_memory() if acc else torch.zeros((n, 64)).pin_memory()
+        plan.run_host(In.pin_memory(), W, Oh, accumulate=acc, nchunks=nchunks)
+        assert torch.equal(Oh, Od.cpu())
