@@ -207,3 +207,23 @@ def test_conv_plan_run_host_matches_device(P, nchunks):
         Oh = O0.clone().pin_memory() if acc else torch.zeros((n, 64)).pin_memory()
         plan.run_host(In.pin_memory(), W, Oh, accumulate=acc, nchunks=nchunks)
         assert torch.equal(Oh, Od.cpu())
+
+
+def test_conv_plan_run_host_non_unit_map(P):
+    """Maps with MAPV != 1 take the host form's copy-all / run / copy-back
+    branch; it equals the device call bit for bit."""
+    g = np.random.default_rng(6)
+    pts = np.unique(g.integers(0, 12, (900, 3)), axis=0).astype(np.int32)
+    n = len(pts)
+    mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+    vals = torch.from_numpy(g.uniform(0.5, 1.5, mo.numel())).float().cuda()
+    gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], vals, 2, 8, canonical=True)
+    plan = P.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values, n, 27,
+                      n)
+    In = torch.from_numpy(g.standard_normal((n, 64))).to(torch.bfloat16)
+    W = torch.from_numpy(g.standard_normal((27, 64, 64)) * 0.1).to(torch.bfloat16).cuda()
+    Od = torch.zeros((n, 64), device="cuda")
+    plan.run(In.cuda(), W, Od, accumulate=False)
+    Oh = torch.zeros((n, 64)).pin_memory()
+    plan.run_host(In.pin_memory(), W, Oh, accumulate=False, nchunks=4)
+    assert torch.equal(Oh, Od.cpu())
