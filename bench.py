@@ -695,7 +695,9 @@ def run_b200(args, wl):
         try:
             c0 = P.lib().ixb_launch_count()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
+            # thread_local: CUDA calls from other threads (NCCL's) during the
+            # capture neither fail nor invalidate it
+            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
                 step()
             per_step = P.lib().ixb_launch_count() - c0
             graph.replay()
