@@ -192,3 +192,34 @@ def test_tp_plan_run_host_matches_device(P, ixo, nchunks):
         Zh = Z0.clone().pin_memory() if acc else torch.zeros((B, 16, 64)).pin_memory()
         plan.run_host(X.pin_memory(), Y.pin_memory(), W, Zh, accumulate=acc, nchunks=nchunks)
         assert torch.equal(Zh, Zd.cpu())
+
+
+def test_tp_plan_run_host_per_edge_w(P, ixo):
+    """Per-edge W[b,l,u,w] (the reference corpus form, CUDA-core kernel): the
+    host-buffer form offsets W per chunk and matches the oracle exactly on
+    integer data; pageable host buffers work too (no overlap, same result)."""
+    t, expr, on, out = instances.make(ixo, "grouped_tp", 1, 91)
+    d = {k: cuda(t[k], torch.float32 if k == "CGV" else torch.int32)
+         for k in ("CGL", "CGI", "CGJ", "CGK", "CGV")}
+    Bb, ni, Wd = out.shape
+    nj, nk, nl, U = t["X"].shape[1], t["Y"].shape[1], t["W"].shape[1], t["X"].shape[2]
+    plan = P.TpPlan(d["CGL"], d["CGI"], d["CGJ"], d["CGK"], d["CGV"], ni, nj, nk, nl, U, Wd,
+                    w_per_batch=True)
+    X = torch.from_numpy(t["X"]).to(torch.bfloat16)
+    Y = torch.from_numpy(t["Y"]).to(torch.bfloat16)
+    W = cuda(t["W"], torch.bfloat16)
+    Z = torch.from_numpy(out).float()  # `+=` into the instance's initial output
+    plan.run_host(X, Y, W, Z, accumulate=True, nchunks=3)
+    np.testing.assert_array_equal(Z.numpy().astype(np.int64), ixo.einsum(expr, t, on, out))
+    # 200 edges (4 tiles, 3 chunks): each chunk reads its own slice of the per-edge W
+    g = np.random.default_rng(5)
+    Bl = 200
+    t2 = dict(t, X=g.integers(-2, 3, (Bl, nj, U)).astype(np.int64),
+              Y=g.integers(-2, 3, (Bl, nk)).astype(np.int64),
+              W=g.integers(-2, 3, (Bl, nl, U, Wd)).astype(np.int64))  # integer kind, like t
+    Z2 = torch.zeros((Bl, ni, Wd))
+    plan.run_host(torch.from_numpy(t2["X"]).to(torch.bfloat16),
+                  torch.from_numpy(t2["Y"]).to(torch.bfloat16),
+                  cuda(t2["W"], torch.bfloat16), Z2, accumulate=False, nchunks=3)
+    want2 = ixo.einsum(expr, t2, on, np.zeros((Bl, ni, Wd), np.int64))
+    np.testing.assert_array_equal(Z2.numpy().astype(np.int64), want2)
