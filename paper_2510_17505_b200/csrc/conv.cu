@@ -509,12 +509,8 @@ void launch_unit(const ixb_conv_plan* P, const void* In, const void* Weight, flo
                                        64, CU_TENSOR_MAP_SWIZZLE_128B);
   UnitArgs ua{P->Y.p, P->tile_mask.p, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
               accumulate, tile0};
-  static std::once_flag once_u;
-  std::call_once(once_u, [&] {
-    cuda_check(cudaFuncSetAttribute(conv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kUnitSmem),
-               "cudaFuncSetAttribute(conv_unit_kernel)");
-  });
+  set_max_dynamic_smem(reinterpret_cast<const void*>(conv_unit_kernel), kUnitSmem,
+                       "cudaFuncSetAttribute(conv_unit_kernel)");
   conv_unit_kernel<<<static_cast<unsigned>(ntiles), kConvThreads, kUnitSmem, s>>>(tmW, ua);
   IXB_LAUNCH_CHECK("conv_unit_kernel");
 }
@@ -603,7 +599,15 @@ int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t
   });
 }
 
-void ixb_conv_plan_free(ixb_conv_plan* plan) { delete plan; }
+void ixb_conv_plan_free(ixb_conv_plan* plan) {
+  if (!plan) return;
+  // runs may be in flight on any stream: let them finish, then release the
+  // tables on the default stream (the creating stream may be gone)
+  cudaDeviceSynchronize();
+  plan->T.s = plan->perm.s = plan->rowptr.s = plan->Y.s = nullptr;
+  plan->tile_mask.s = nullptr;
+  delete plan;
+}
 
 int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void* Weight,
                       int64_t Cout, float* Out, int accumulate, int flags, ixb_stream stream) {
@@ -628,12 +632,8 @@ int ixb_conv_plan_run(ixb_conv_plan* P, const void* In, int64_t Cin, const void*
       RunArgs a{P->T.p, P->MAPY, P->MAPV, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
                 P->n_off, accumulate};
       const uint32_t smem = 2 * kATile + 2 * kWTile + 1024 + 1024;
-      static std::once_flag once;
-      std::call_once(once, [&] {
-        cuda_check(cudaFuncSetAttribute(conv_tc_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                   "cudaFuncSetAttribute(conv_tc_kernel)");
-      });
+      set_max_dynamic_smem(reinterpret_cast<const void*>(conv_tc_kernel), smem,
+                           "cudaFuncSetAttribute(conv_tc_kernel)");
       conv_tc_kernel<<<ceil_div(P->n_out, 128), kConvThreads, smem, s>>>(tmW, a);
       IXB_LAUNCH_CHECK("conv_tc_kernel");
       return;

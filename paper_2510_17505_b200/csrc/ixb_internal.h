@@ -36,6 +36,10 @@ void cuda_check(cudaError_t e, const char* what);
 
 void note_launch(int n = 1);
 int sm_count();
+// Opts `func` in to `bytes` of dynamic shared memory on the CURRENT device.
+// The attribute is per device/context, so the opt-in is tracked per
+// (device, function) and repeated on every device the process drives.
+void set_max_dynamic_smem(const void* func, int bytes, const char* name);
 
 // Per-device error record (lazily allocated, reset after each check).
 ErrorRecord* device_error_record();

@@ -18,6 +18,7 @@ std::atomic<int64_t> g_launches{0};
 struct DeviceCtx {
   ixb::ErrorRecord* rec = nullptr;
   int sms = 0;
+  std::vector<std::pair<const void*, int>> smem_optin;  // (kernel, bytes) opted in
 };
 std::mutex g_mu;
 std::vector<DeviceCtx> g_dev;
@@ -52,6 +53,23 @@ void cuda_check(cudaError_t e, const char* what) {
 void note_launch(int n) { g_launches += n; }
 
 int sm_count() { return ctx().sms; }
+
+void set_max_dynamic_smem(const void* func, int bytes, const char* name) {
+  DeviceCtx& c = ctx();
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (const auto& e : c.smem_optin)
+      if (e.first == func && e.second >= bytes) return;
+  }
+  cuda_check(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), name);
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& e : c.smem_optin)
+    if (e.first == func) {
+      if (bytes > e.second) e.second = bytes;
+      return;
+    }
+  c.smem_optin.emplace_back(func, bytes);
+}
 
 ErrorRecord* device_error_record() { return ctx().rec; }
 

@@ -616,12 +616,8 @@ extern "C" int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, 
                   static_cast<int>(p.nk), static_cast<int>(p.ni), accumulate};
       const uint32_t smem =
           kXTile + kNU * kUSlot + kNW * kWTileTp + 2 * kEdges * 16 * 4 + 256 + 1024;
-      static std::once_flag once;
-      std::call_once(once, [&] {
-        cuda_check(cudaFuncSetAttribute(tp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        smem),
-                   "cudaFuncSetAttribute(tp_tc_kernel)");
-      });
+      set_max_dynamic_smem(reinterpret_cast<const void*>(tp_tc_kernel), smem,
+                           "cudaFuncSetAttribute(tp_tc_kernel)");
       int64_t grid = ceil_div(batch, kEdges);
       if (grid > sm_count()) grid = sm_count();
       tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, smem, s>>>(tmW, tmX, p.meta, args);

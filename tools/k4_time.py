@@ -1,0 +1,82 @@
+"""K4 timing on cfg2 (perf experiment, not part of the library): the plan-reusing
+run (BgcooPlan.run), the one-shot call (plan + run + free) and plan creation,
+each as a CUDA-graph replay bracketed by events after an L2 flush.
+
+  python tools/k4_time.py [--reps 20] [--n 512]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def timed(torch, fn, reps, flush):
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        out.append(a.elapsed_time(b) * 1e3)
+    out.sort()
+    return out[len(out) // 2], out[0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--n", type=int, default=512)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2510_17505_b200 as P
+    from paper_2510_17505_b200 import synth as S
+    dev = torch.device("cuda", 0)
+    rng = S.Rng(1)
+    B = S.synth_dense(rng, (512, 16, args.n), S.REAL, torch.bfloat16).to(dev)
+    A = S.synth_block_sparse_matrix(rng, 8192, 8192, 16, 16, 0.10, S.REAL, torch.bfloat16)
+    fmt = P.dense_to_blockgroupcoo(A.to(dev), 16, 16, 0)
+    G, g = fmt.num_groups(), fmt.group_size
+    C = torch.empty((512, 16, args.n), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = P.BgcooPlan(fmt.AM, fmt.AK, G, g, 512, 512)
+    torch.cuda.synchronize()
+    create_ms = (time.perf_counter() - t0) * 1e3
+    res = {"G": G, "g": g, "blocks": fmt.num_blocks, "plan_create_host_ms": create_ms}
+    res["run_us"] = timed(torch, lambda: plan.run(fmt.AV, B, C, accumulate=False), args.reps, flush)
+    ref = C.clone()
+    res["oneshot_us"] = timed(torch, lambda: P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C,
+                                                                  accumulate=False, flags=1 | 2),
+                              args.reps, flush)
+    res["oneshot_equal_run"] = bool(torch.equal(C, ref))
+    os.environ["IXB_BG_LEGACY"] = "1"
+    P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C, accumulate=False, flags=1 | 2)
+    torch.cuda.synchronize()
+    res["legacy_max_abs_diff"] = float((C - ref).abs().max())
+    res["legacy_us"] = timed(torch, lambda: P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C,
+                                                                 accumulate=False, flags=1 | 2),
+                             args.reps, flush)
+    del os.environ["IXB_BG_LEGACY"]
+    flops = 2.0 * fmt.num_blocks * 256 * args.n
+    res["run_TFLOPs"] = flops / (res["run_us"][0] * 1e-6) / 1e12
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
