@@ -175,22 +175,6 @@ int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV,
                            int64_t N, float* C, int64_t MB, int accumulate, int flags,
                            ixb_stream stream);
 
-/* Inspector/executor split of K4 for a BlockGroupCOO structure reused across
- * calls (the format is static; AV and B may change): the plan validates AK/AM
- * once (reference order, plan.cpp:544-561), sorts groups by block row when AM
- * is unsorted, and builds the per-panel (block column, slot)-ordered op list
- * the panel kernel streams; run evaluates AV, B -> C with the same semantics
- * as ixb_spmm_blockgroupcoo (which is create + run + free). bm = bk = 16,
- * N % 128 == 0 for run; the AV passed to run must have the plan's [G,g,16,16]
- * shape. */
-typedef struct ixb_bgcoo_plan ixb_bgcoo_plan;
-int ixb_bgcoo_plan_create(const int32_t* AM, const int32_t* AK, int64_t G, int64_t g, int64_t bm,
-                          int64_t bk, int64_t KB, int64_t MB, int flags, ixb_stream stream,
-                          ixb_bgcoo_plan** plan);
-int ixb_bgcoo_plan_run(ixb_bgcoo_plan* plan, const void* AV, const void* B, int64_t N, float* C,
-                       int accumulate, int flags, ixb_stream stream);
-void ixb_bgcoo_plan_free(ixb_bgcoo_plan* plan);
-
 /* K5 — submanifold 3x3x3 kernel map over n voxels (coords [n,3] int32,
  * unique). Pairs (out i, in j, offset z) with coord[j] == coord[i] + delta(z),
  * z = (dx+1)*9 + (dy+1)*3 + (dz+1), ordered by (z, i) — the canonical order

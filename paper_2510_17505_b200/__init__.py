@@ -19,7 +19,7 @@ from .abi import (BindError, IxbError, IndexRangeError, IoError, ParseError, Sha
 from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupcoo,
                   dense_to_coo, dense_to_groupcoo, coo_to_groupcoo, emit_operands,
                   group_coo_tensor, kernel_map, tune_group_size, spmm_groupcoo,
-                  spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups, ConvPlan, TpPlan, BgcooPlan,
+                  spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups, ConvPlan, TpPlan,
                   spmm_groupcoo_host, spmm_blockgroupcoo_host,
                   count_accesses_model)
 from .executor import execute_mode, match_workload, WORKLOADS
@@ -33,7 +33,7 @@ __all__ = [
     "GroupCoo", "BlockGroupCoo", "GroupCooTensor", "dense_to_coo", "coo_to_groupcoo",
     "dense_to_groupcoo", "dense_to_blockgroupcoo", "group_coo_tensor", "emit_operands",
     "kernel_map", "tune_group_size", "spmm_groupcoo", "spmm_blockgroupcoo", "conv_grouped",
-    "tp_grouped", "shard_groups", "ConvPlan", "TpPlan", "BgcooPlan", "spmm_groupcoo_host",
+    "tp_grouped", "shard_groups", "ConvPlan", "TpPlan", "spmm_groupcoo_host",
     "spmm_blockgroupcoo_host", "count_accesses_model", "execute_mode", "match_workload",
     "WORKLOADS", "io", "ixt_info", "load_ixt", "save_ixt", "load_matrix_market",
     "read_matrix_market_host", "save_format", "load_format", "convert", "tune_report", "tune_measured",

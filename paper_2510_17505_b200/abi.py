@@ -102,11 +102,6 @@ _SIGS = {
     "ixb_spmm_groupcoo_host": (C.c_int, [C.c_void_p] * 3 + [C.c_int64] * 2 + [C.c_void_p] +
                                [C.c_int64] * 2 + [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int,
                                                   C.c_void_p]),
-    "ixb_bgcoo_plan_create": (C.c_int, [C.c_void_p] * 2 + [C.c_int64] * 6 +
-                              [C.c_int, C.c_void_p, C.c_void_p]),
-    "ixb_bgcoo_plan_run": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_void_p, C.c_int, C.c_int,
-                                                         C.c_void_p]),
-    "ixb_bgcoo_plan_free": (None, [C.c_void_p]),
     "ixb_tp_plan_create": (C.c_int, [C.c_void_p] * 5 + [C.c_int64, C.c_int64, C.c_int] +
                            [C.c_int64] * 6 + [C.c_int, C.c_void_p, C.c_void_p]),
     "ixb_tp_plan_run": (C.c_int, [C.c_void_p] * 4 + [C.c_int64, C.c_void_p, C.c_int, C.c_int,

@@ -293,43 +293,6 @@ def spmm_blockgroupcoo(AM, AK, AV, B, C_out, accumulate=True, flags=0, stream=No
     return C_out
 
 
-class BgcooPlan:
-    """Inspector/executor form of K4 for a static BlockGroupCOO structure:
-    validates AK/AM and builds the panel op list once (ixb_bgcoo_plan_create);
-    run() evaluates C[AM[p],bm,n] (+)= AV[p,q,bm,bk] * B[AK[p,q],bk,n]."""
-
-    def __init__(self, AM, AK, G, g, KB, MB, bm=16, bk=16, flags=0, stream=None):
-        self.keep = (AM.contiguous(), AK.contiguous())
-        self.G, self.g, self.bm, self.bk, self.KB, self.MB = G, g, bm, bk, KB, MB
-        self._free = lib().ixb_bgcoo_plan_free
-        self.h = C.c_void_p()
-        check(lib().ixb_bgcoo_plan_create(_ptr(self.keep[0]), _ptr(self.keep[1]), G, g, bm, bk,
-                                          KB, MB, flags, _stream(stream), C.byref(self.h)))
-
-    def run(self, AV, B, C_out, accumulate=True, flags=0, stream=None):
-        want_av = (self.G, self.g, self.bm, self.bk)
-        if tuple(AV.shape) != want_av or AV.dtype != torch.bfloat16 or not AV.is_contiguous():
-            raise ShapeError(4, f"BgcooPlan.run: AV must be contiguous bf16 {list(want_av)}")
-        if (B.dim() != 3 or tuple(B.shape[:2]) != (self.KB, self.bk) or
-                B.dtype != torch.bfloat16 or not B.is_contiguous()):
-            raise ShapeError(4, f"BgcooPlan.run: B must be contiguous bf16 [{self.KB},{self.bk},N]")
-        N = B.shape[2]
-        if (tuple(C_out.shape) != (self.MB, self.bm, N) or C_out.dtype != torch.float32 or
-                not C_out.is_contiguous()):
-            raise ShapeError(4, f"BgcooPlan.run: C must be contiguous fp32 [{self.MB},{self.bm},{N}]")
-        for t in (AV, B, C_out):
-            if not t.is_cuda:
-                raise ShapeError(4, "BgcooPlan.run: operands must be device tensors")
-        check(lib().ixb_bgcoo_plan_run(self.h, _ptr(AV), _ptr(B), N, _ptr(C_out),
-                                       int(accumulate), flags, _stream(stream)))
-        return C_out
-
-    def __del__(self):
-        if getattr(self, "h", None):
-            self._free(self.h)
-            self.h = None
-
-
 def conv_grouped(MAPZ, MAPX, MAPY, MAPV, In, Weight, Out, accumulate=True, flags=0,
                  stream=None):
     """K6: Out[MAPX[p,q],m] (+)= MAPV[p,q] * In[MAPY[p,q],c] * Weight[MAPZ[p],c,m]."""

@@ -22,16 +22,13 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
-#include <memory>
 #include <mutex>
 
-#include "bgcoo_panel.h"
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tmap.h"
 
 namespace ixb {
-
 namespace {
 
 using namespace sm100;
@@ -485,11 +482,9 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     return;
   }
   if (G * g * bk > INT32_MAX || KB * bk > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 rows");
-  const bool panel = bgcoo_panel_ok(bm, bk, N, AV, B) && !getenv("IXB_BG_LEGACY");
   // Unsorted group coordinates: validate the original arrays (K8), then
-  // evaluate over a stably sorted order of the groups, which keeps every
-  // output row's summation order. The panel kernel addresses the caller's AV
-  // through the permutation; the CUDA-core kernel reads gathered copies.
+  // evaluate over a stably sorted copy of the format (rows of AK/AV gathered
+  // by the permutation), which keeps every output row's summation order.
   Scratch<int32_t> am_sorted, perm, ak_sorted;
   Scratch<__nv_bfloat16> av_sorted;
   if (!(flags & IXB_GROUPS_SORTED) && !groups_sorted(AM, G, s)) {
@@ -501,24 +496,20 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     }
     sort_groups(AM, G, s, am_sorted, perm);
     ak_sorted = Scratch<int32_t>(G * g, s);
+    av_sorted = Scratch<__nv_bfloat16>(G * g * bm * bk, s);
     gather_rows(perm.p, AK, ak_sorted.p, G, g * 4, s);
+    gather_rows(perm.p, AV, av_sorted.p, G, g * bm * bk * 2, s);
     AM = am_sorted.p;
     AK = ak_sorted.p;
-    if (!panel) {
-      av_sorted = Scratch<__nv_bfloat16>(G * g * bm * bk, s);
-      gather_rows(perm.p, AV, av_sorted.p, G, g * bm * bk * 2, s);
-      AV = av_sorted.p;
-    }
+    AV = av_sorted.p;
     flags |= IXB_UNCHECKED;
   }
   const bool check2 = !(flags & IXB_UNCHECKED);
   ErrorRecord* err = device_error_record();
-  if (panel) {
-    BgPanelPlan P;
-    bgcoo_panel_plan(AM, AK, perm.p, G, g, KB, MB, check2, s, P);
-    bgcoo_panel_run(P, AV, B, N, C, accumulate, s);
-  } else if (bm == 16 && bk == 16 && N % 128 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0 &&
-             reinterpret_cast<uintptr_t>(AV) % 16 == 0) {
+  const bool tc_ok = bm == 16 && bk == 16 && N % 128 == 0 &&
+                     reinterpret_cast<uintptr_t>(B) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(AV) % 16 == 0;
+  if (tc_ok) {
     TcArgs a;
     a.AM = AM;
     a.AK = AK;
@@ -535,11 +526,17 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     a.err = err;
     a.nchunks = static_cast<int>(ceil_div(G, a.chunk));
     const int nsub = N % 256 == 0 ? 2 : 1;
+    // B viewed as {64 n, rows, N/64 atoms}: one TMA box = the whole n tile of
+    // 16 rows, landing as [atom][row][64] (the MN-major SW128 canonical layout)
     const CUtensorMap tmB = make_tmap_3d(B, 64, KB * 16, N / 64, N * 2, 128, 64, 16, 2 * nsub,
                                         CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tmAV = make_tmap_2d(AV, 16, G * g * 16, 32, 16, 16,
                                          CU_TENSOR_MAP_SWIZZLE_32B);
-    a.epi_sleep_ns = 256;
+    a.epi_sleep_ns = 256;  // back-off of the idle epilogue warps' barrier polls
+    // 2 slots per stage, 4 stages: ~68 KB -> 3 CTAs (3 independent issue
+    // streams) per SM; measured against 1, 4, 8, 12 slots per stage and
+    // 1-5 CTAs/SM on cfg2 (profiles/k4_diag_r1.md), and against a panel
+    // kernel with B-tile reuse across block rows (profiles/k4_diag_r2.md)
     if (nsub == 1) launch_tc<1, 8, 4, 2>(tmB, tmAV, a, s);
     else launch_tc<2, 4, 4, 2>(tmB, tmAV, a, s);
   } else {
@@ -565,77 +562,4 @@ extern "C" int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, cons
     ixb::spmm_blockgroupcoo(AM, AK, AV, G, g, bm, bk, B, KB, N, C, MB, accumulate, flags,
                             reinterpret_cast<cudaStream_t>(stream));
   });
-}
-
-// ---------------------------------------------------------- plan object
-struct ixb_bgcoo_plan {
-  ixb::BgPanelPlan P;
-  ixb::Scratch<int32_t> perm;  // sorted group position -> caller's (unsorted AM only)
-  int64_t bm = 16, bk = 16;
-};
-
-extern "C" int ixb_bgcoo_plan_create(const int32_t* AM, const int32_t* AK, int64_t G, int64_t g,
-                                     int64_t bm, int64_t bk, int64_t KB, int64_t MB, int flags,
-                                     ixb_stream stream, ixb_bgcoo_plan** plan) {
-  return ixb_guard([&] {
-    using namespace ixb;
-    auto s = reinterpret_cast<cudaStream_t>(stream);
-    if (!plan) fail(IXB_FAILURE, "null plan out-pointer");
-    *plan = nullptr;
-    if (G < 0 || g < 1 || KB < 0 || MB < 0) fail(IXB_SHAPE, "ixb_bgcoo_plan_create: bad extents");
-    if (bm != 16 || bk != 16) fail(IXB_SHAPE, "ixb_bgcoo_plan_create: the panel kernel takes 16x16 blocks");
-    if (G * g * bk > INT32_MAX || KB * bk > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 rows");
-    const bool check = !(flags & IXB_UNCHECKED);
-    auto P = std::make_unique<ixb_bgcoo_plan>();
-    Scratch<int32_t> am_sorted, ak_sorted;
-    const int32_t *am = AM, *ak = AK;
-    if (G > 0 && !(flags & IXB_GROUPS_SORTED) && !groups_sorted(AM, G, s)) {
-      if (check) {
-        validate_range(AK, G * g, KB, 0, s);
-        validate_range(AM, G, MB, 1, s);
-      }
-      sort_groups(AM, G, s, am_sorted, P->perm);
-      ak_sorted = Scratch<int32_t>(G * g, s);
-      gather_rows(P->perm.p, AK, ak_sorted.p, G, g * 4, s);
-      am = am_sorted.p;
-      ak = ak_sorted.p;
-    }
-    bgcoo_panel_plan(am, ak, P->perm.p, G, g, KB, MB, check, s, P->P);
-    if (check) {
-      OperandInfo ops[2] = {{"AK", "B", 0, KB, AK, G * g}, {"AM", "C", 0, MB, AM, G}};
-      check_error_record(s, ops, 2);
-    } else {
-      IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // scratch of the sort is released on `s`
-    }
-    *plan = P.release();
-  });
-}
-
-extern "C" int ixb_bgcoo_plan_run(ixb_bgcoo_plan* plan, const void* AV, const void* B, int64_t N,
-                                  float* C, int accumulate, int flags, ixb_stream stream) {
-  return ixb_guard([&] {
-    using namespace ixb;
-    (void)flags;
-    auto s = reinterpret_cast<cudaStream_t>(stream);
-    if (!plan) fail(IXB_FAILURE, "null bgcoo plan");
-    if (N < 0) fail(IXB_SHAPE, "ixb_bgcoo_plan_run: bad extents");
-    const BgPanelPlan& P = plan->P;
-    if (N == 0 || P.MB == 0) return;
-    if (P.G == 0) {
-      if (!accumulate) IXB_CUDA_CHECK(cudaMemsetAsync(C, 0, P.MB * 16 * N * sizeof(float), s));
-      return;
-    }
-    if (!bgcoo_panel_ok(plan->bm, plan->bk, N, AV, B))
-      fail(IXB_SHAPE, "ixb_bgcoo_plan_run: N must be a multiple of 128 and AV/B 16-byte aligned");
-    bgcoo_panel_run(P, AV, B, N, C, accumulate, s);
-  });
-}
-
-extern "C" void ixb_bgcoo_plan_free(ixb_bgcoo_plan* plan) {
-  if (!plan) return;
-  // in-flight runs on any stream finish before the tables are released; the
-  // creating stream may be gone by now, so release on the default stream
-  cudaDeviceSynchronize();
-  plan->P.rowptr.s = plan->P.rec.s = plan->P.nstages.s = plan->perm.s = nullptr;
-  delete plan;
 }

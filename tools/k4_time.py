@@ -1,6 +1,6 @@
-"""K4 timing on cfg2 (perf experiment, not part of the library): the plan-reusing
-run (BgcooPlan.run), the one-shot call (plan + run + free) and plan creation,
-each as a CUDA-graph replay bracketed by events after an L2 flush.
+"""K4 timing on cfg2 (perf experiment, not part of the library): the shipped
+BlockGroupCOO SpMM as a CUDA-graph replay bracketed by events after an L2
+flush, median and best of --reps.
 
   python tools/k4_time.py [--reps 20] [--n 512]
 """
@@ -8,7 +8,6 @@ import argparse
 import json
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -50,31 +49,13 @@ def main():
     B = S.synth_dense(rng, (512, 16, args.n), S.REAL, torch.bfloat16).to(dev)
     A = S.synth_block_sparse_matrix(rng, 8192, 8192, 16, 16, 0.10, S.REAL, torch.bfloat16)
     fmt = P.dense_to_blockgroupcoo(A.to(dev), 16, 16, 0)
-    G, g = fmt.num_groups(), fmt.group_size
     C = torch.empty((512, 16, args.n), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    plan = P.BgcooPlan(fmt.AM, fmt.AK, G, g, 512, 512)
-    torch.cuda.synchronize()
-    create_ms = (time.perf_counter() - t0) * 1e3
-    res = {"G": G, "g": g, "blocks": fmt.num_blocks, "plan_create_host_ms": create_ms}
-    res["run_us"] = timed(torch, lambda: plan.run(fmt.AV, B, C, accumulate=False), args.reps, flush)
-    ref = C.clone()
-    res["oneshot_us"] = timed(torch, lambda: P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C,
-                                                                  accumulate=False, flags=1 | 2),
-                              args.reps, flush)
-    res["oneshot_equal_run"] = bool(torch.equal(C, ref))
-    os.environ["IXB_BG_LEGACY"] = "1"
-    P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C, accumulate=False, flags=1 | 2)
-    torch.cuda.synchronize()
-    res["legacy_max_abs_diff"] = float((C - ref).abs().max())
-    res["legacy_us"] = timed(torch, lambda: P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C,
-                                                                 accumulate=False, flags=1 | 2),
-                             args.reps, flush)
-    del os.environ["IXB_BG_LEGACY"]
-    flops = 2.0 * fmt.num_blocks * 256 * args.n
-    res["run_TFLOPs"] = flops / (res["run_us"][0] * 1e-6) / 1e12
+    res = {"G": fmt.num_groups(), "g": fmt.group_size, "blocks": fmt.num_blocks}
+    res["call_us"] = timed(torch, lambda: P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, C,
+                                                               accumulate=False, flags=1 | 2),
+                           args.reps, flush)
+    res["TFLOPs"] = 2.0 * fmt.num_blocks * 256 * args.n / (res["call_us"][0] * 1e-6) / 1e12
     print(json.dumps(res))
 
 
