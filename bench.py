@@ -32,6 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DEFAULT_WORKLOAD = "cfg2"
+# L2 -> SM read bandwidth measured on this pool's B200s (tools/l2_rate.cu:
+# 16-byte gathers of an L2-resident buffer, all SMs; profiles/l2_rate_r2.json)
+L2_PEAK_GBPS = 21300.0
+L2_PEAK_SOURCE = "measured tools/l2_rate.cu (profiles/l2_rate_r2.json)"
 
 
 # --------------------------------------------------------------- helpers
@@ -151,6 +155,23 @@ def dist_env():
 
 
 # ------------------------------------------------------------- workloads
+def time_builder(torch, fn, reps=2):
+    """Wall time of a format-builder call (its plan phase syncs the host for
+    the output sizes, so CUDA events would miss nothing but the host part):
+    one warm call, then the best of `reps` synchronised calls. Returns
+    (result, ms)."""
+    out = fn()
+    best = None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t0) * 1e3
+        best = ms if best is None else min(best, ms)
+    return out, best
+
+
 class GroupCooWorkload:
     """configs[0] / configs[2]: unstructured GroupCOO SpMM, fp32 (K3)."""
     expr = "C[AM[p],n] = AV[p,q] * B[AK[p,q],n]"
@@ -171,17 +192,32 @@ class GroupCooWorkload:
         B = S.synth_dense(rng, (self.K, self.N), S.REAL, torch.float32)
         A = S.synth_sparse_matrix(rng, self.M, self.K, self.density, S.REAL, torch.float32)
         self.B = B.to(dev)
-        fmt = P.dense_to_groupcoo(A.to(dev), g=0)  # format: auto (tuner)
+        Ad = A.to(dev)
         del A
+        # K1 dense -> GroupCOO builder (format: auto, tuner on device), timed warm
+        fmt, build_ms = time_builder(torch, lambda: P.dense_to_groupcoo(Ad, g=0))
         self.fmt = fmt
         self.G, self.g = fmt.num_groups(), fmt.group_size
         self.nnz = int(fmt.mask.sum().item())
         self.rows_nz = int(torch.unique(fmt.AM).numel())
+        slots = self.G * self.g
+        # builder: dense read (compulsory once; the kernels read it twice: count + pack)
+        # + format written (AM, AK, AV, mask)
+        self.builder = {"name": "K1 dense_to_groupcoo (+tuner)", "ms": build_ms,
+                        "compulsory_bytes": self.M * self.K * 4 + self.G * 4 + slots * 9,
+                        "passes_over_dense": 2}
+        del Ad
         self.C = torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
         self.flops = 2.0 * self.nnz * self.N
-        # gather model: B row per stored nonzero + format once + C rows once
-        self.alg_bytes = (self.nnz * self.N * 4 + self.G * self.g * (4 + 4) + self.G * 4 +
+        # gather model (BASELINE §3): B row per stored nonzero + format
+        # once + non-empty C rows once. It counts L2-served B rows as HBM bytes.
+        self.alg_bytes = (self.nnz * self.N * 4 + slots * (4 + 4) + self.G * 4 +
                           self.rows_nz * self.N * 4)
+        # compulsory DRAM: format once, B once, every C row written once (`=`)
+        self.dram_bytes = self.G * 4 + slots * 8 + self.K * self.N * 4 + self.M * self.N * 4
+        # L2 -> SM as the kernel moves it: one B row per slot (pads included) + format + C
+        self.l2_bytes = self.G * 4 + slots * 8 + slots * self.N * 4 + self.M * self.N * 4
+        self.tc_flops = None
         self.info = {"nnz": self.nnz, "G": self.G, "g": self.g, "nonempty_rows": self.rows_nz}
         # pinned host copies for e2e
         self.h_in = [fmt.AM.cpu().pin_memory(), fmt.AK.cpu().pin_memory(),
@@ -266,8 +302,11 @@ class BlockGroupCooWorkload:
         A = S.synth_block_sparse_matrix(rng, self.M, self.K, b, b, self.bdens, S.REAL,
                                         torch.bfloat16)
         self.B = B.to(dev)
-        fmt = P.dense_to_blockgroupcoo(A.to(dev), b, b, 0)  # g by the tuner on block occupancy
+        Ad = A.to(dev)
         del A
+        # K2 dense -> BlockGroupCOO builder (g by the tuner on block occupancy), timed warm
+        fmt, build_ms = time_builder(torch, lambda: P.dense_to_blockgroupcoo(Ad, b, b, 0))
+        del Ad
         self.fmt = fmt
         self.G, self.g = fmt.num_groups(), fmt.group_size
         self.nblk = fmt.num_blocks
@@ -278,7 +317,19 @@ class BlockGroupCooWorkload:
         # compulsory bytes: format once, dense operand once, C written once
         self.alg_bytes = (slots * b * b * 2 + slots * 4 + self.G * 4 + self.K * self.N * 2 +
                           self.rows_nz * b * self.N * 4)
+        self.dram_bytes = slots * b * b * 2 + slots * 4 + self.G * 4 + self.K * self.N * 2 + \
+            self.M * self.N * 4
         self.gather_bytes = slots * b * self.N * 2
+        # L2 -> SM as the kernel moves it: a 16-row B tile per slot and 256-wide n
+        # tile, AV block + AK per slot and n tile, AM, C written once
+        ntile = max(self.N // 256, 1)
+        self.l2_bytes = self.gather_bytes + slots * (b * b * 2 + 4) * ntile + self.G * 4 + \
+            self.M * self.N * 4
+        self.tc_flops = 2.0 * self.nblk * b * b * self.N
+        # builder: dense read once + present blocks re-read + format written
+        self.builder = {"name": "K2 dense_to_blockgroupcoo (+tuner)", "ms": build_ms,
+                        "compulsory_bytes": self.M * self.K * 2 + self.nblk * b * b * 2 +
+                        slots * (b * b * 2 + 4 + 1) + self.G * 4, "passes_over_dense": 1}
         self.mma_count = slots * (self.N // 128)  # one M=128 (n) x N=16 (bm) UMMA per slot per n tile
         self.info = {"blocks": self.nblk, "G": self.G, "g": self.g,
                      "nonempty_block_rows": self.rows_nz,
@@ -380,6 +431,10 @@ class TensorProductWorkload:
         self.Z = torch.empty((B, 16, 64), dtype=torch.float32, device=dev)
         self.flops = 2.0 * 99 * 64 * 64 * B  # factorised form (sum over paths of 2*l3+1 = 99)
         self.alg_bytes = B * (16 * 64 * 2 + 16 * 2 + 16 * 64 * 4) + nl * 64 * 64 * 2
+        self.dram_bytes = self.alg_bytes
+        # L2 -> SM: X/Y/Z once + W[l] (8 KB) per (path, component-pair) job per 64-edge tile
+        self.l2_bytes = self.alg_bytes + math.ceil(B / 64) * 61 * 64 * 64 * 2
+        self.tc_flops = self.flops
         self.info = {"paths": nl, "cg_nnz": int(cg["v"].numel()), "G": gt.num_groups(), "g": g,
                      "plan_ms": plan_ms,
                      "formulation": "output-side factorised: 99 (path, component) products per "
@@ -464,19 +519,21 @@ class SparseConvWorkload:
         import time as _t
         coords = S.synth_voxel_shells(self.voxels).to(dev)
         n = coords.shape[0]
-        torch.cuda.synchronize()
-        t0 = _t.perf_counter()
-        mo, mi, mz = P.kernel_map(coords)
-        g, _ = P.tune_group_size(mz, 27)
-        ones = torch.ones(mo.numel(), dtype=torch.float32, device=dev)
-        gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], ones, 2, g, canonical=True)
-        torch.cuda.synchronize()
-        t1 = _t.perf_counter()
+        def build():
+            mo, mi, mz = P.kernel_map(coords)
+            g, _ = P.tune_group_size(mz, 27)
+            ones = torch.ones(mo.numel(), dtype=torch.float32, device=dev)
+            return mo, mi, mz, g, P.group_coo_tensor([n, n, 27], [mo, mi, mz], ones, 2, g,
+                                                     canonical=True)
+        # K5 kernel map + tuner + group_coo_tensor, timed warm
+        (mo, mi, mz, g, gt), build_ms = time_builder(torch, build)
         self.map, self.g = (mo, mi, mz), g
         self.MAPZ, (self.MAPX, self.MAPY), self.MAPV = gt.group_coord, gt.member_coords, gt.values
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
         self.plan = P.ConvPlan(self.MAPZ, self.MAPX, self.MAPY, self.MAPV, n, 27, n)
         torch.cuda.synchronize()
-        t2 = _t.perf_counter()
+        plan_ms = (_t.perf_counter() - t0) * 1e3
         rng = S.Rng(seed)
         self.In = S.synth_dense(rng, (n, 64), S.REAL, torch.bfloat16).to(dev)
         self.Wt = S.synth_dense(rng, (27, 64, 64), S.REAL, torch.bfloat16).to(dev)
@@ -487,8 +544,20 @@ class SparseConvWorkload:
         G = gt.num_groups()
         # gather model: In row gathered + Out row updated per pair, map once
         self.alg_bytes = pairs * 64 * (2 + 4) + G * g * (4 + 2 * 4) + G * 4
+        # compulsory DRAM: In once, Out once, the plan's input-row table Y[n, 28] int32
+        self.dram_bytes = n * 64 * 2 + n * 64 * 4 + n * 28 * 4
+        # L2 -> SM: an In row (128 B) per map pair, Weight[z] (8 KB) per used
+        # (128-row tile, offset), the Y table, Out once
+        tile_off = int(torch.unique((mo // 128).long() * 27 + mz.long()).numel())
+        self.l2_bytes = pairs * 128 + tile_off * 64 * 64 * 2 + n * 28 * 4 + n * 64 * 4
+        self.tc_flops = self.flops
+        self.builder = {"name": "K5 kernel_map + tuner + group_coo_tensor", "ms": build_ms,
+                        # coords read + hash table (2 x 8 B per slot) + pairs written (3 x 4 B)
+                        # + grouped map written (MAPZ, MAPX, MAPY, MAPV)
+                        "compulsory_bytes": n * 12 + 2 * n * 8 + pairs * 12 + G * 4 +
+                        G * g * 12, "passes_over_dense": None}
         self.info = {"voxels": n, "pairs": pairs, "kappa": pairs / n, "G": G, "g": g,
-                     "kernel_map_and_group_ms": (t1 - t0) * 1e3, "plan_ms": (t2 - t1) * 1e3}
+                     "kernel_map_and_group_ms": build_ms, "plan_ms": plan_ms}
         self.h_in = [self.In.cpu().pin_memory()]
         self.h_out = torch.empty_like(self.Out, device="cpu").pin_memory()
         self.d_in = [torch.empty_like(self.In)]
@@ -626,6 +695,199 @@ def load_ncu_traffic(name):
         return None
 
 
+def roofline(wl, kern_s, torch, dev):
+    """Three fractions of the step's dominant kernel:
+    compulsory DRAM bytes vs measured HBM, the kernel's L2->SM bytes vs the
+    measured L2 read bandwidth, and tensor-core flops vs measured bf16 peak
+    (tensor-core kernels only). `bound` is the binding level: the one whose
+    floor (bytes or flops / peak) is longest, i.e. the largest fraction."""
+    hbm, tc, _, peak_src = load_peaks()
+    fr = {"hbm": wl.dram_bytes / kern_s / 1e9 / hbm,
+          "l2": wl.l2_bytes / kern_s / 1e9 / L2_PEAK_GBPS}
+    if wl.tc_flops:
+        fr["tensor"] = wl.tc_flops / kern_s / 1e12 / tc
+    bound = max(fr, key=fr.get)
+    if bound == "tensor":
+        achieved, peak, unit = wl.tc_flops / kern_s / 1e12, tc, "TFLOP/s"
+        src = f"{peak_src} MEASURED_PEAKS.json bf16_tflops (burst)"
+    elif bound == "hbm":
+        achieved, peak, unit = wl.dram_bytes / kern_s / 1e9, hbm, "GB/s"
+        src = f"{peak_src} MEASURED_PEAKS.json hbm_gbs"
+    else:
+        achieved, peak, unit = wl.l2_bytes / kern_s / 1e9, L2_PEAK_GBPS, "GB/s"
+        src = L2_PEAK_SOURCE
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": load_ncu_traffic(wl.name),
+            "traffic_source": f"profiles/ncu_{wl.name}.json (ncu --set full, dram__bytes "
+                              "read+write per launch)",
+            "fracs": fr, "peak_source": src,
+            "bytes": {"dram_compulsory": wl.dram_bytes, "l2_to_sm": wl.l2_bytes},
+            "tc_flops": wl.tc_flops,
+            "peaks": {"hbm_GBps": hbm, "l2_GBps": L2_PEAK_GBPS, "bf16_TFLOPs": tc}}
+    if hasattr(wl, "alg_bytes") and wl.roofline_bound() == "hbm":
+        # BASELINE §3's gather model (B rows counted as if from HBM)
+        roof["gather_model_frac"] = wl.alg_bytes / kern_s / 1e9 / hbm
+    if hasattr(wl, "mma_count"):
+        # measured tensor-pipe occupancy of an M=128,N=16,K=16 MMA with >= 2 issuing CTAs
+        # per SM: 38.8 cycles (tools/umma_pair_rate.cu, profiles/k4_diag_r1.md §8 and
+        # k4_diag_r2.md §1); the per-instruction floor, not flops, bounds 16-wide blocks
+        floor_s = wl.mma_count * 38.8 / (torch.cuda.get_device_properties(dev).multi_processor_count
+                                          * 1.965e9)
+        roof["mma_issue_floor_us"] = floor_s * 1e6
+        roof["frac_of_mma_issue_floor"] = floor_s / kern_s
+    return roof
+
+
+def measure(torch, P, step, e2e_step, steps, warmup, e2e_reps, flush, stream, graph=True,
+            ws=1, dist=None):
+    """W warm-up steps, then `steps` timed steps (CUDA-graph replay of one
+    step unless graph=False), each bracketed by events on `stream` after an
+    L2 flush outside the events; clocks sampled during the timed region;
+    max over ranks. Then the e2e leg through the public API."""
+    dev = flush.device
+    for _ in range(warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    P.lib().ixb_check_errors(None)
+    timed_step, timing, per_step = step, "eager launches", None
+    if graph:
+        try:
+            c0 = P.lib().ixb_launch_count()
+            g = torch.cuda.CUDAGraph()
+            # thread_local: CUDA calls from other threads (NCCL's) during the
+            # capture neither fail nor invalidate it
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                step()
+            per_step = P.lib().ixb_launch_count() - c0
+            g.replay()
+            torch.cuda.synchronize()
+            timed_step, timing = g.replay, "CUDA-graph replay of one step"
+        except Exception as e:  # reported in config.timing, never fatal
+            timing = f"eager launches (graph capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
+    clocks = Clocks(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = P.lib().ixb_launch_count()
+    evs = []
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        timed_step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = P.lib().ixb_launch_count() - launches0
+    if per_step is not None:
+        launches = per_step * steps
+    clk = clocks.stop()
+    rc = P.lib().ixb_check_errors(None)
+    if rc != 0:
+        raise RuntimeError("index error during bench: " + P.lib().ixb_last_error().decode())
+    total = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([total], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item() / steps
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_evs = []
+    for _ in range(e2e_reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        e_evs.append((a, b))
+    torch.cuda.synchronize()
+    e_ms = statistics.mean(a.elapsed_time(b) for a, b in e_evs)
+    et = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    return {"ms": ms, "e2e_ms": et.item(), "launches": int(launches), "timing": timing,
+            "clocks": clk}
+
+
+def workload_record(wl, m, torch, dev, jobs=1, kern_scale=1.0):
+    """The JSON fields of one workload measured by `measure`."""
+    metric = getattr(wl, "metric", METRIC)
+    timelike = metric != METRIC
+    ms = m["ms"]
+    value = wl.flops * jobs / (ms * 1e-3) / 1e9
+    h2d, d2h = wl.e2e_bytes() if hasattr(wl, "e2e_bytes") else (None, None)
+    rec = {"metric": metric, "value": ms if timelike else value,
+           "unit": "ms" if timelike else "GFLOP/s", "ms_per_step": ms,
+           "higher_is_better": not timelike,
+           "dtype": "bf16" if wl.tc_flops or timelike else "f32",
+           "config": dict(wl.config(), timing=m["timing"], **wl.info),
+           "roofline": roofline(wl, ms * 1e-3 * kern_scale, torch, dev),
+           "clocks": m["clocks"], "gpu_launches": m["launches"],
+           "e2e": {"value": m["e2e_ms"] if timelike else wl.flops * jobs / (m["e2e_ms"] * 1e-3) / 1e9,
+                   "unit": "ms" if timelike else "GFLOP/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": m["e2e_ms"]}}
+    if timelike:
+        rec["config"]["useful_GFLOPs"] = value
+    return rec
+
+
+def builder_record(wl):
+    """Format-builder timing recorded by the workload's setup (warm call)."""
+    hbm, _, _, _ = load_peaks()
+    b = dict(wl.builder)
+    gbps = b["compulsory_bytes"] / (b["ms"] * 1e-3) / 1e9
+    b.update({"workload": wl.name, "achieved_GBps": gbps, "hbm_frac": gbps / hbm,
+              "timing": "wall time of the API call (warm, best of 2; its plan phase syncs "
+                        "the host for the output sizes)"})
+    return b
+
+
+def cpu_builder_baseline(name):
+    """The reference's own builders on the same full-size input (cfg1: dense_to_coo +
+    tune + coo_to_groupcoo; cfg2: dense_to_blockgroupcoo), oracle/_ref, one core."""
+    import numpy as np
+    from oracle import ref
+    if not ref.available():
+        return None
+    if name == "cfg1":
+        rng = ref.Rng(1)
+        ref.synth_dense(rng, (4096, 128), 0)
+        A = ref.synth_sparse_matrix(rng, 4096, 4096, 0.01, 0)
+        t0 = time.perf_counter()
+        r, c, v = ref.dense_to_coo(A)
+        g = ref.tune(np.bincount(r, minlength=4096))["chosen"]
+        ref.coo_to_groupcoo(4096, 4096, r, c, v, 0, g)
+        ms = (time.perf_counter() - t0) * 1e3
+        return {"ms": ms, "cores": 1, "kind": "reference",
+                "sample": "full cfg1 matrix: dense_to_coo + tuner + coo_to_groupcoo"}
+    if name == "cfg2":
+        rng = ref.Rng(1)
+        ref.synth_dense(rng, (512, 16, 512), 0)
+        A = ref.synth_block_sparse_matrix(rng, 8192, 8192, 16, 16, 0.10, 0)
+        t0 = time.perf_counter()
+        ref.dense_to_blockgroupcoo(A, 16, 16, 8, 0)
+        ms = (time.perf_counter() - t0) * 1e3
+        return {"ms": ms, "cores": 1, "kind": "reference",
+                "sample": "full cfg2 matrix: dense_to_blockgroupcoo (g=8, the tuner's choice)"}
+    return None
+
+
+SECONDARY = ["cfg1", "cfg3_d0.30", "cfg3_d0.20", "cfg3_d0.10", "cfg3_d0.05", "cfg3_d0.02",
+             "cfg4", "cfg5"]
+# bounded reference samples for the secondary workloads (a few seconds each)
+SECONDARY_BUDGET = {"cfg1": 1000, "cfg4": 2, "cfg5": 800}
+for _d in (0.30, 0.20, 0.10, 0.05, 0.02):  # ~2e7 reference iteration points per run
+    SECONDARY_BUDGET[f"cfg3_d{_d:.2f}"] = max(1, int(2.0e7 / (16384 * _d * 256)))
+
+
 def run_b200(args, wl):
     import torch
     import torch.distributed as dist
@@ -664,6 +926,7 @@ def run_b200(args, wl):
         def e2e_bytes():
             return sum(x.numel() * x.element_size() for x in wl.sh_h_in), \
                 wl.sh_h_out.numel() * wl.sh_h_out.element_size()
+        wl.e2e_bytes = e2e_bytes
     else:
         # weak scaling: every rank evaluates its own independent instance of the
         # per-GPU workload (seed + rank); no data-path collective.
@@ -675,154 +938,79 @@ def run_b200(args, wl):
 
         def e2e_step():
             wl.e2e_step(P)
-
-        e2e_bytes = wl.e2e_bytes
     jobs = 1 if args.sharded else ws  # instances processed per step, whole job
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
-
-    for _ in range(args.warmup):
-        flush.zero_()
-        step()
-    torch.cuda.synchronize()
-    P.lib().ixb_check_errors(None)
-    # One step captured in a CUDA graph and replayed per timed iteration, so
-    # the device time carries no host launch latency (the e2e leg below still
-    # goes through the public API call by call). Launches per step are
-    # counted at capture; eager launches if the step cannot be captured.
-    timed_step, timing, per_step = step, "eager launches", None
-    if not args.sharded and not args.no_graph:
-        try:
-            c0 = P.lib().ixb_launch_count()
-            graph = torch.cuda.CUDAGraph()
-            # thread_local: CUDA calls from other threads (NCCL's) during the
-            # capture neither fail nor invalidate it
-            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
-                step()
-            per_step = P.lib().ixb_launch_count() - c0
-            graph.replay()
-            torch.cuda.synchronize()
-            timed_step, timing = graph.replay, "CUDA-graph replay of one step"
-        except Exception as e:  # reported in config.timing, never fatal
-            timing = f"eager launches (graph capture failed: {type(e).__name__})"
-            torch.cuda.synchronize()
-
-    clocks = Clocks(dev)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    launches0 = P.lib().ixb_launch_count()
-    evs = []
-    for _ in range(args.steps):
-        flush.zero_()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        timed_step()
-        b.record(stream)
-        evs.append((a, b))
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    launches = P.lib().ixb_launch_count() - launches0
-    if per_step is not None:
-        launches = per_step * args.steps
-    clk = clocks.stop()
-    rc = P.lib().ixb_check_errors(None)
-    if rc != 0:
-        raise RuntimeError("index error during bench: " + P.lib().ixb_last_error().decode())
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = t.item()
-    ms = total_ms / args.steps
-    value = wl.flops * jobs / (ms * 1e-3) / 1e9
-
-    # e2e through the public API with pinned host buffers
-    for _ in range(2):
-        e2e_step()
-    torch.cuda.synchronize()
-    e_evs = []
-    for _ in range(max(3, min(args.steps, 20))):
-        flush.zero_()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        e2e_step()
-        b.record(stream)
-        e_evs.append((a, b))
-    torch.cuda.synchronize()
-    e_ms = statistics.mean(a.elapsed_time(b) for a, b in e_evs)
-    et = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-    if ws > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e_ms = et.item()
-    h2d, d2h = e2e_bytes()
-
-    hbm, tc, tc_sus, peak_src = load_peaks()
-    kern_s = ms * 1e-3 * (ws if args.sharded else 1)  # per-GPU share of a sharded job
-    if wl.roofline_bound() == "hbm":
-        achieved = wl.alg_bytes / kern_s / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": load_ncu_traffic(wl.name),
-                "algorithmic_bytes_per_launch": wl.alg_bytes,
-                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
-    else:
-        achieved = wl.flops / kern_s / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
-                "frac": achieved / tc, "traffic": load_ncu_traffic(wl.name),
-                "algorithmic_flops_per_launch": wl.flops,
-                "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops (burst)",
-                "hbm_compulsory_frac": wl.alg_bytes / kern_s / 1e9 / hbm,
-                "l2_gather_GBps": wl.gather_bytes / kern_s / 1e9}
-        if hasattr(wl, "mma_count"):
-            # measured tensor-pipe occupancy of an M=128,N=16,K=16 MMA with >= 2 issuing CTAs
-            # per SM: 38.8 cycles (tools/umma_pair_rate.cu, profiles/k4_diag_r1.md §8); the
-            # per-instruction floor, not flops, bounds 16-wide blocks
-            floor_s = wl.mma_count * 38.8 / (torch.cuda.get_device_properties(dev).multi_processor_count
-                                              * 1.965e9)
-            roof["mma_issue_floor_us"] = floor_s * 1e6
-            roof["frac_of_mma_issue_floor"] = floor_s / kern_s
-
-    metric = getattr(wl, "metric", METRIC)
-    timelike = metric != METRIC
-    line = {"metric": metric, "value": ms if timelike else value,
-            "unit": "ms" if timelike else "GFLOP/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": not timelike,
+    m = measure(torch, P, step, e2e_step, args.steps, args.warmup, max(3, min(args.steps, 20)),
+                flush, stream, graph=not args.sharded and not args.no_graph, ws=ws, dist=dist)
+    rec = workload_record(wl, m, torch, dev, jobs=jobs,
+                          kern_scale=ws if args.sharded else 1)
+    line = {"metric": rec["metric"], "value": rec["value"], "unit": rec["unit"], "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
+            "higher_is_better": rec["higher_is_better"],
             "scaling": "strong" if args.sharded else "weak", "vs_baseline": None,
-            "dtype": "bf16" if wl.roofline_bound() == "tensor" or timelike else "f32",
-            "data": "synthetic (reference synth streams, seed 1 + rank)",
-            "config": dict(wl.config(), l2="flushed between steps (256 MiB memset outside the "
-                                         "timed events)",
-                           parallelism=(f"sharded x{ws} + {backend if ws > 1 else 'no'} all-gather of output slabs"
-                                        if args.sharded else f"weak x{ws}"), timing=timing,
-                           **wl.info),
-            "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
-            "e2e": {"value": e_ms if timelike else wl.flops * jobs / (e_ms * 1e-3) / 1e9,
-                    "unit": "ms" if timelike else "GFLOP/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e_ms}}
-    if timelike:
-        line["config"]["useful_GFLOPs"] = value
+            "dtype": rec["dtype"], "data": "synthetic (reference synth streams, seed 1 + rank)",
+            "config": dict(rec["config"], l2="flushed between steps (256 MiB memset outside "
+                                             "the timed events)",
+                           parallelism=(f"sharded x{ws} + {backend if ws > 1 else 'no'} "
+                                        "all-gather of output slabs"
+                                        if args.sharded else f"weak x{ws}")),
+            "roofline": rec["roofline"], "clocks": rec["clocks"],
+            "gpu_launches": rec["gpu_launches"], "e2e": rec["e2e"]}
     if shard_info is not None:
         line["config"]["shard_rank0"] = shard_info
     if ws > 1:
         line["config"]["dist_backend"] = backend
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        try:
-            r = cpu_reference_time(wl)
-            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        except Exception as e:  # reported, never fatal
-            line["cpu_baseline"] = {"value": None, "unit": "GFLOP/s", "cores": None,
-                                    "kind": "reference", "sample": f"unavailable: {e}"}
+        line["cpu_baseline"] = cpu_line(wl)
+    builders = {}
+    if getattr(wl, "builder", None) and not args.sharded:
+        builders[wl.name] = builder_record(wl)
+    if ws == 1 and not args.sharded and args.workloads != "none":
+        # every other BASELINE config, measured the same way in this invocation
+        names = SECONDARY if args.workloads == "all" else args.workloads.split(",")
+        line["workloads"] = {}
+        del wl
+        for name in names:
+            if name == args.workload:
+                continue
+            w2 = WORKLOADS[name]()
+            try:
+                w2.setup(torch, P, S, dev, w2.seed)
+                m2 = measure(torch, P, lambda: w2.step(P), lambda: w2.e2e_step(P),
+                             args.sub_steps, 3, 3, flush, stream, graph=not args.no_graph)
+                r2 = workload_record(w2, m2, torch, dev)
+                r2["steps"], r2["warmup"] = args.sub_steps, 3
+                if not args.no_cpu_baseline:
+                    r2["cpu_baseline"] = cpu_line(w2, SECONDARY_BUDGET.get(name), steps=1)
+                if getattr(w2, "builder", None):
+                    builders[name] = builder_record(w2)
+                line["workloads"][name] = r2
+            except Exception as e:  # reported per workload, never fatal to the headline
+                line["workloads"][name] = {"error": f"{type(e).__name__}: {e}"}
+            del w2
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    if builders:
+        if not args.no_cpu_baseline:
+            for name, b in builders.items():
+                cb = cpu_builder_baseline(name)
+                if cb:
+                    b["cpu_baseline"] = cb
+        line["builders"] = builders
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def cpu_line(wl, budget=None, steps=1):
+    try:
+        r = cpu_reference_time(wl, steps=steps, budget_rows=budget)
+        return {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    except Exception as e:  # reported, never fatal
+        return {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "reference",
+                "sample": f"unavailable: {e}"}
 
 
 def main():
@@ -835,6 +1023,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of a CUDA-graph replay of the step")
+    ap.add_argument("--workloads", default="all",
+                    help="other BASELINE configs timed in the same invocation (N=1 only): "
+                         "'all', 'none' or a comma list")
+    ap.add_argument("--sub-steps", type=int, default=10,
+                    help="timed steps per secondary workload")
     ap.add_argument("--sharded", action="store_true",
                     help="strong scaling: shard ONE instance across the ranks (row groups, "
                          "point blocks or edges) and all-gather the output inside the step")

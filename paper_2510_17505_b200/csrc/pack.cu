@@ -36,6 +36,10 @@ namespace {
 
 constexpr int kTB = 256;
 
+// One pass over the occupancy counts: S, non-empty rows, max, and
+// sum_r ceil(occ_r / 2^i) for every i (all candidate F(g) at once). Each
+// thread reduces its rows in registers, warps reduce by shuffles, one smem
+// atomic per warp per statistic, one global atomic per CTA per statistic.
 __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
   __shared__ unsigned long long sh[35];
   for (int i = threadIdx.x; i < 35; i += blockDim.x) sh[i] = 0;
@@ -50,19 +54,31 @@ __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) grp[i] += (o + (1ull << i) - 1) >> i;
   }
-  atomicAdd(&sh[0], S);
-  atomicAdd(&sh[1], nz);
-  atomicMax(&sh[2], mx);
-  for (int i = 0; i < 32; ++i) {
-    if (grp[i]) atomicAdd(&sh[3 + i], grp[i]);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    S += __shfl_xor_sync(0xffffffffu, S, off);
+    nz += __shfl_xor_sync(0xffffffffu, nz, off);
+    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = m2 > mx ? m2 : mx;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) grp[i] += __shfl_xor_sync(0xffffffffu, grp[i], off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&sh[0], S);
+    atomicAdd(&sh[1], nz);
+    atomicMax(&sh[2], mx);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (grp[i]) atomicAdd(&sh[3 + i], grp[i]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    atomicAdd(&out->S, sh[0]);
-    atomicAdd(&out->nonzero, sh[1]);
+    if (sh[0]) atomicAdd(&out->S, sh[0]);
+    if (sh[1]) atomicAdd(&out->nonzero, sh[1]);
     atomicMax(&out->maxocc, sh[2]);
   }
-  if (threadIdx.x < 32 && sh[3 + threadIdx.x]) atomicAdd(&out->groups_pow2[threadIdx.x], sh[3 + threadIdx.x]);
+  if (threadIdx.x < 32 && sh[3 + threadIdx.x])
+    atomicAdd(&out->groups_pow2[threadIdx.x], sh[3 + threadIdx.x]);
 }
 
 }  // namespace
@@ -74,8 +90,9 @@ int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_e
   Scratch<OccStats> d(1, s);
   IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
   if (n > 0) {
-    int64_t grid = ceil_div(n, kTB);
-    if (grid > 4 * sm_count()) grid = 4 * sm_count();
+    // ~8 rows per thread, at most one CTA per SM: few global atomics per CTA
+    int64_t grid = ceil_div(n, 8 * kTB);
+    if (grid > sm_count()) grid = sm_count();
     occ_stats_kernel<<<grid, kTB, 0, s>>>(occ, n, d.p);
     IXB_LAUNCH_CHECK("occ_stats_kernel");
   }
@@ -379,13 +396,54 @@ __global__ void block_flags_kernel(const T* __restrict__ dense, int64_t rows, in
   flags[b] = any ? 1 : 0;
 }
 
-// 16x16 bf16/f32 fast path: one warp per block row-stripe element group.
+// Vectorised block flags: a warp covers one block row and 32 16-byte column
+// chunks (32 * 16 / (bk * sizeof(T)) consecutive blocks), walking the block's
+// bm rows with coalesced 512-byte loads; the lanes of one block OR their
+// "any nonzero" bits by shuffles. Needs bk * sizeof(T) to divide 512 and 16-byte
+// aligned rows (the shape check is on the host); ragged edges are masked.
+template <typename T>
+__global__ void block_flags_vec_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
+                                       int64_t bm, int64_t bk, int64_t gr, int64_t gcn,
+                                       uint8_t* flags) {
+  constexpr int V = 16 / sizeof(T);  // elements per chunk
+  const int lane = lane_id();
+  const int cpb = static_cast<int>(bk / V);  // chunks per block row segment
+  const int bpw = 32 / cpb;                  // blocks per warp
+  const int64_t warps_per_row = (gcn + bpw - 1) / bpw;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w >= gr * warps_per_row) return;
+  const int64_t br = w / warps_per_row;
+  const int64_t bc = (w % warps_per_row) * bpw + lane / cpb;
+  const int64_t c0 = bc * bk + static_cast<int64_t>(lane % cpb) * V;
+  const bool in = bc < gcn && c0 < cols;
+  const int64_t ie = (br + 1) * bm < rows ? (br + 1) * bm : rows;
+  bool any = false;
+  if (in) {
+    if (c0 + V <= cols) {
+      for (int64_t i = br * bm; i < ie; ++i) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(dense + i * cols + c0));
+        const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+        for (int j = 0; j < V; ++j) any |= nz<T>(e[j]);
+      }
+    } else {
+      for (int64_t i = br * bm; i < ie; ++i)
+        for (int64_t j = c0; j < cols; ++j) any |= nz<T>(dense[i * cols + j]);
+    }
+  }
+  unsigned m = __ballot_sync(0xffffffffu, any);
+  const int first = (lane / cpb) * cpb;
+  const unsigned mine = (m >> first) & ((cpb == 32 ? 0u : (1u << cpb)) - 1u);
+  if (in && lane % cpb == 0) flags[br * gcn + bc] = (cpb == 32 ? m : mine) ? 1 : 0;
+}
+
+// Block copy: one warp per slot, 16-byte chunks (bk * sizeof(T) a multiple of
+// 16, 16-byte aligned rows); pad slots and ragged edges are zero-filled.
 template <typename T>
 __global__ void block_copy_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
                                   int64_t bm, int64_t bk, int group_dim, const int32_t* AM,
                                   const int32_t* AK, const uint8_t* mask, int64_t slots, int64_t g,
-                                  T* AV) {
-  // one warp per slot; lanes stride the bm*bk elements
+                                  T* AV, int vec) {
   const int64_t slot = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (slot >= slots) return;
   const int lane = lane_id();
@@ -394,6 +452,26 @@ __global__ void block_copy_kernel(const T* __restrict__ dense, int64_t rows, int
   const int64_t p = slot / g;
   const int64_t rb = group_dim == 0 ? AM[p] : AK[slot];
   const int64_t cb = group_dim == 0 ? AK[slot] : AM[p];
+  if (vec) {
+    constexpr int V = 16 / sizeof(T);
+    const int64_t cpr = bk / V;  // chunks per block row
+    for (int64_t e = lane; e < bm * cpr; e += 32) {
+      const int64_t i = e / cpr, j = (e % cpr) * V;
+      const int64_t si = rb * bm + i, sj = cb * bk + j;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (real && si < rows) {
+        if (sj + V <= cols) {
+          v = __ldg(reinterpret_cast<const uint4*>(dense + si * cols + sj));
+        } else {
+          T* t = reinterpret_cast<T*>(&v);
+          for (int k = 0; k < V; ++k)
+            if (sj + k < cols) t[k] = dense[si * cols + sj + k];
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + i * bk + j) = v;
+    }
+    return;
+  }
   for (int64_t e = lane; e < bm * bk; e += 32) {
     const int64_t i = e / bk, j = e % bk;
     const int64_t si = rb * bm + i, sj = cb * bk + j;
@@ -785,8 +863,19 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
     if (nb) {
       dispatch_dense(dtype, [&](auto tag) {
         using T = decltype(tag);
-        block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
-            static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
+        const int64_t rowb = bk * static_cast<int64_t>(sizeof(T));
+        const bool vec = rowb % 16 == 0 && 512 % rowb == 0 &&
+                         (cols * static_cast<int64_t>(sizeof(T))) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(dense) % 16 == 0;
+        if (vec) {
+          const int64_t bpw = 512 / rowb;
+          const int64_t warps = P->gr * ceil_div(P->gcn, bpw);
+          block_flags_vec_kernel<<<ceil_div(warps * 32, kTB), kTB, 0, P->s>>>(
+              static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
+        } else {
+          block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
+              static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
+        }
       });
       IXB_LAUNCH_CHECK("block_flags_kernel");
     }
@@ -849,9 +938,13 @@ int ixb_blockgroupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint
       const int64_t grid = ceil_div(slots * 32, kTB);
       dispatch_dense(P->dtype, [&](auto tag) {
         using T = decltype(tag);
+        const int vec = (P->bk * static_cast<int64_t>(sizeof(T))) % 16 == 0 &&
+                        (P->cols * static_cast<int64_t>(sizeof(T))) % 16 == 0 &&
+                        reinterpret_cast<uintptr_t>(P->dense) % 16 == 0 &&
+                        reinterpret_cast<uintptr_t>(AV) % 16 == 0;
         block_copy_kernel<<<grid, kTB, 0, P->s>>>(static_cast<const T*>(P->dense), P->rows,
                                                  P->cols, P->bm, P->bk, P->group_dim, AM, AK, m,
-                                                 slots, P->g, static_cast<T*>(AV));
+                                                 slots, P->g, static_cast<T*>(AV), vec);
       });
       IXB_LAUNCH_CHECK("block_copy_kernel");
     }
