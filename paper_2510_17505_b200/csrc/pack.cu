@@ -86,19 +86,22 @@ __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
 // select() of tuner.cpp:100-118 over device occupancy counts.
 int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_empty_rows,
                       cudaStream_t s, double* gstar_out, int64_t* cand_g = nullptr,
-                      double* cand_score = nullptr, int* ncand = nullptr) {
+                      double* cand_score = nullptr, int* ncand = nullptr,
+                      int64_t* total_out = nullptr) {
   Scratch<OccStats> d(1, s);
   IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
   if (n > 0) {
-    // ~8 rows per thread, at most one CTA per SM: few global atomics per CTA
-    int64_t grid = ceil_div(n, 8 * kTB);
-    if (grid > sm_count()) grid = sm_count();
+    // one row per thread up to two CTAs per SM (latency-bound for short
+    // profiles), grid-stride beyond; one global atomic per statistic per CTA
+    int64_t grid = ceil_div(n, kTB);
+    if (grid > 2 * sm_count()) grid = 2 * sm_count();
     occ_stats_kernel<<<grid, kTB, 0, s>>>(occ, n, d.p);
     IXB_LAUNCH_CHECK("occ_stats_kernel");
   }
   OccStats h;
   IXB_CUDA_CHECK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
   IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (total_out) *total_out = static_cast<int64_t>(h.S);
   // g_star (tuner.cpp:60-65)
   double gs = 1.0;
   if (h.S > 0) {
@@ -279,9 +282,39 @@ __global__ void row_pack_kernel(const T* __restrict__ dense, int64_t rows, int64
   }
 }
 
+// occupancy() (formats.cpp:96-103): histogram of a coordinate array. Small
+// extents (the 27 kernel offsets of a conv map, the paths of a CG table) are
+// counted in a per-CTA shared-memory histogram, grid-stride, and merged with
+// one global atomic per non-empty bin per CTA; large extents (matrix rows)
+// have little contention and count straight into global memory.
+constexpr int kOccSmemBins = 8192;
 __global__ void occupancy_kernel(const int32_t* c, int64_t n, int64_t ext, int32_t* o) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n && c[i] >= 0 && c[i] < ext) atomicAdd(o + c[i], 1);
+  __shared__ int32_t h[kOccSmemBins];
+  const bool small = ext <= kOccSmemBins;
+  if (small) {
+    for (int64_t b = threadIdx.x; b < ext; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+  }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = c[i];
+    if (v >= 0 && v < ext) {
+      if (small) atomicAdd(h + v, 1);
+      else atomicAdd(o + v, 1);
+    }
+  }
+  if (small) {
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < ext; b += blockDim.x)
+      if (h[b]) atomicAdd(o + b, h[b]);
+  }
+}
+void launch_occupancy(const int32_t* coord, int64_t nnz, int64_t extent, int32_t* occ,
+                      cudaStream_t s) {
+  int64_t grid = ceil_div(nnz, kTB);
+  if (extent <= kOccSmemBins && grid > 2 * sm_count()) grid = 2 * sm_count();
+  occupancy_kernel<<<static_cast<unsigned>(grid), kTB, 0, s>>>(coord, nnz, extent, occ);
+  IXB_LAUNCH_CHECK("occupancy_kernel");
 }
 
 __global__ void groups_per_run_kernel(const int32_t* occ, int64_t n, int64_t g, int32_t* ng) {
@@ -538,21 +571,36 @@ void launch_row_pack(const T* d, int64_t rows, int64_t cols, const int32_t* occ,
 }
 
 // Exclusive scan of n int32 into out[0..n] (out[n] = total); returns total (sync).
-int64_t exclusive_scan_total(const int32_t* in, int64_t n, int32_t* out, cudaStream_t s) {
-  if (n == 0) return 0;
+__global__ void scan_total_kernel(const int32_t* in, int64_t n, int32_t* out) {
+  out[n] = in[n - 1] + out[n - 1];
+}
+
+// Exclusive scan of n counts into out[0..n), with the total in out[n], all on
+// the device (no host round trip).
+void exclusive_scan_dev(const int32_t* in, int64_t n, int32_t* out, cudaStream_t s) {
+  if (n == 0) {
+    IXB_CUDA_CHECK(cudaMemsetAsync(out, 0, 4, s));
+    return;
+  }
   size_t tb = 0;
   IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int>(n), s));
   Scratch<char> tmp(tb, s);
   IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, static_cast<int>(n), s));
   note_launch();
-  int32_t last_in = 0, last_out = 0;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&last_out, out + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  scan_total_kernel<<<1, 1, 0, s>>>(in, n, out);
+  IXB_LAUNCH_CHECK("scan_total_kernel");
+}
+
+// exclusive_scan_dev + the total read back (one host sync): the caller sizes
+// its output buffers from it.
+int64_t exclusive_scan_total(const int32_t* in, int64_t n, int32_t* out, cudaStream_t s) {
+  if (n == 0) return 0;
+  exclusive_scan_dev(in, n, out, s);
+  int32_t total = 0;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&total, out + n, 4, cudaMemcpyDeviceToHost, s));
   IXB_CUDA_CHECK(cudaStreamSynchronize(s));
-  const int64_t total = static_cast<int64_t>(last_in) + last_out;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(out + n, &total, 4, cudaMemcpyHostToDevice, s));
-  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
-  if (total > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 entries");
+  // counts are non-negative, so a negative int32 total means it wrapped past 2^31
+  if (total < 0) fail(IXB_SHAPE, "format exceeds 2^31 entries");
   return total;
 }
 
@@ -567,10 +615,16 @@ void count_rows(ixb_pack* P) {
 // Dense-row grouping plan (group_dim 0): occ -> tuner -> groups per row -> gofs.
 void plan_dense_rows(ixb_pack* P, int64_t g_req, int64_t* g_out) {
   count_rows(P);
-  Scratch<int32_t> tmp(P->rows + 1, P->s);
-  P->nnz = exclusive_scan_total(P->occ.p, P->rows, tmp.p, P->s);
   int64_t g = g_req;
-  if (g == 0) g = tune_from_occ(P->occ.p, P->rows, P->rows, 0, P->s, nullptr);
+  if (g == 0) {
+    // the tuner's one read-back also returns S = nnz
+    g = tune_from_occ(P->occ.p, P->rows, P->rows, 0, P->s, nullptr, nullptr, nullptr, nullptr,
+                      &P->nnz);
+    if (P->nnz > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 entries");
+  } else {
+    Scratch<int32_t> tmp(P->rows + 1, P->s);
+    P->nnz = exclusive_scan_total(P->occ.p, P->rows, tmp.p, P->s);
+  }
   P->g = g;
   if (g_out) *g_out = g;
   Scratch<int32_t> ng(P->rows + 1, P->s);
@@ -991,8 +1045,7 @@ int ixb_tune_report(const int32_t* coord, int64_t nnz, int64_t extent, int count
     Scratch<int32_t> occ(extent + 1, s);
     IXB_CUDA_CHECK(cudaMemsetAsync(occ.p, 0, (extent + 1) * 4, s));
     if (nnz) {
-      occupancy_kernel<<<ceil_div(nnz, kTB), kTB, 0, s>>>(coord, nnz, extent, occ.p);
-      IXB_LAUNCH_CHECK("occupancy_kernel");
+      launch_occupancy(coord, nnz, extent, occ.p, s);
     }
     *g_out = tune_from_occ(occ.p, extent, extent, count_empty_rows, s, gstar_out, cand_g,
                            cand_score, ncand);
@@ -1007,8 +1060,7 @@ int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int c
     Scratch<int32_t> occ(extent + 1, s);
     IXB_CUDA_CHECK(cudaMemsetAsync(occ.p, 0, (extent + 1) * 4, s));
     if (nnz) {
-      occupancy_kernel<<<ceil_div(nnz, kTB), kTB, 0, s>>>(coord, nnz, extent, occ.p);
-      IXB_LAUNCH_CHECK("occupancy_kernel");
+      launch_occupancy(coord, nnz, extent, occ.p, s);
     }
     *g_out = tune_from_occ(occ.p, extent, extent, count_empty_rows, s, gstar_out);
   });
