@@ -147,6 +147,11 @@ int ixb_group_coo_tensor_pack(ixb_pack* plan, const void* values, int dtype,
 int ixb_tune_report(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
                     ixb_stream stream, int64_t* g, double* gstar, int64_t* cand_g,
                     double* cand_score, int* ncand);
+/* brute_force_optimal (tuner.cpp:86-97), the TuneReport's brute_optimal:
+ * argmin over g in [1, max occ] of cost_exact (ties -> smaller g). *g = 0 for an
+ * empty profile (the reference's nullopt). */
+int ixb_tune_brute(const int32_t* coord, int64_t nnz, int64_t extent, ixb_stream stream,
+                   int64_t* g, int64_t* cost);
 int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
                         ixb_stream stream, int64_t* g_out, double* gstar_out);
 

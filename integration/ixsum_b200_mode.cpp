@@ -5,12 +5,15 @@
 // A maintainer adds one branch to execute_mode:
 //     } else if (mode == "b200") { return ixsum::b200::execute(problem); }
 // This file is that branch's implementation: it matches the inferred
-// EinsumStmt to one of the hot-path workloads, moves the BoundProblem's
-// Tensors to the device in the device formats (int32 indices; fp32 for the
-// GroupCOO SpMM, bf16 operands with fp32 accumulation elsewhere), calls the
-// sm_100a evaluator and returns a ModeResult with the analytic access
-// counters (count_accesses_model, plan.cpp:607-631). Errors come back as the
-// reference's exception types with the reference's message content.
+// EinsumStmt structurally (roles AND variable identity, like
+// paper_2510_17505_b200/executor.py match_workload) to one of the hot-path
+// workloads, moves the BoundProblem's Tensors to the device in the device
+// formats (int32 indices; fp32 for the GroupCOO SpMM, bf16 operands with fp32
+// accumulation elsewhere), calls the sm_100a evaluator and returns a
+// ModeResult with the analytic access counters (count_accesses_model,
+// plan.cpp:607-631). Statements outside the hot path are rejected, never
+// computed as something else. Errors come back as the reference's exception
+// types with the reference's message content.
 #include "ixsum_b200_mode.hpp"
 
 #include <cuda_bf16.h>
@@ -18,78 +21,222 @@
 
 #include <chrono>
 #include <cmath>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "b200_util.hpp"
 #include "ixb.h"
 
 namespace ixsum::b200 {
 namespace {
 
-struct DevBuf {
-  void* p = nullptr;
-  explicit DevBuf(size_t bytes) {
-    if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) throw std::runtime_error("cudaMalloc");
-  }
-  ~DevBuf() { cudaFree(p); }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-};
+using detail::check;
+using detail::DevBuf;
 
-void rethrow(int code, const EinsumStmt& stmt) {
-  (void)stmt;
-  const std::string msg = ixb_last_error();
-  switch (code) {
-    case IXB_OK: return;
-    case IXB_PARSE: throw ParseError(msg, 0);
-    case IXB_BIND: throw BindError(msg);
-    case IXB_SHAPE: throw ShapeError(msg);
-    case IXB_INDEX_RANGE: throw IndexRangeError(msg);
-    default: throw std::runtime_error(msg);
+// ------------------------------------------------------ statement structure
+bool direct(const IndexExpr& e) { return std::holds_alternative<DirectIndex>(e); }
+const std::string& dvar(const IndexExpr& e) { return std::get<DirectIndex>(e).var; }
+const IndirectIndex& ind(const IndexExpr& e) { return std::get<IndirectIndex>(e); }
+
+std::vector<std::string> vars_of(const TensorAccess& a) {  // all direct, else empty
+  std::vector<std::string> v;
+  for (const auto& i : a.indices) {
+    if (!direct(i)) return {};
+    v.push_back(dvar(i));
   }
+  return v;
 }
 
-std::unique_ptr<DevBuf> up_index(const Tensor& t) {
+enum class Workload { GroupCooSpmm, CooSpmm, BlockGroupCooSpmm, GroupedConv, Conv, TpPerEdge, TpShared };
+
+// Role -> tensor name of a matched statement.
+struct Match {
+  Workload wl;
+  std::map<std::string, std::string> t;
+};
+
+// The four frozen hot-path expressions and their degenerate
+// forms, recognised by structure and variable identity.
+std::optional<Match> match(const EinsumStmt& st) {
+  const auto& o = st.output;
+  const auto& in = st.inputs;
+  // C[AM[p],n] += AV[p,q] * B[AK[p,q],n]   (COO form: AV[p], AK[p])
+  if (in.size() == 2 && o.indices.size() == 2 && !direct(o.indices[0]) && direct(o.indices[1])) {
+    const auto& v = in[0];
+    const auto& b = in[1];
+    const auto& pm = ind(o.indices[0]).args;
+    const std::string& n = dvar(o.indices[1]);
+    const auto vv = vars_of(v);
+    if (pm.size() == 1 && !vv.empty() && b.indices.size() == 2 && !direct(b.indices[0]) &&
+        direct(b.indices[1]) && dvar(b.indices[1]) == n && ind(b.indices[0]).args == vv &&
+        vv[0] == pm[0] && (vv.size() == 1 || vv.size() == 2) && n != pm[0] &&
+        (vv.size() == 1 || (vv[1] != n && vv[1] != pm[0]))) {
+      return Match{vv.size() == 2 ? Workload::GroupCooSpmm : Workload::CooSpmm,
+                   {{"C", o.tensor}, {"AM", ind(o.indices[0]).tensor}, {"AV", v.tensor},
+                    {"B", b.tensor}, {"AK", ind(b.indices[0]).tensor}}};
+    }
+  }
+  // C[AM[p],bm,n] += AV[p,q,bm,bk] * B[AK[p,q],bk,n]
+  if (in.size() == 2 && o.indices.size() == 3 && !direct(o.indices[0]) && direct(o.indices[1]) &&
+      direct(o.indices[2])) {
+    const auto& v = in[0];
+    const auto& b = in[1];
+    const auto& pm = ind(o.indices[0]).args;
+    const auto vv = vars_of(v);
+    if (pm.size() == 1 && vv.size() == 4 && vv[0] == pm[0] && vv[2] == dvar(o.indices[1]) &&
+        b.indices.size() == 3 && !direct(b.indices[0]) &&
+        ind(b.indices[0]).args == std::vector<std::string>{vv[0], vv[1]} &&
+        direct(b.indices[1]) && dvar(b.indices[1]) == vv[3] && direct(b.indices[2]) &&
+        dvar(b.indices[2]) == dvar(o.indices[2])) {
+      return Match{Workload::BlockGroupCooSpmm,
+                   {{"C", o.tensor}, {"AM", ind(o.indices[0]).tensor}, {"AV", v.tensor},
+                    {"B", b.tensor}, {"AK", ind(b.indices[0]).tensor}}};
+    }
+  }
+  // Out[MAPX[p,q],m] += MAPV[p,q] * In[MAPY[p,q],c] * Weight[MAPZ[p],c,m]  (COO form: [p])
+  if (in.size() == 3 && o.indices.size() == 2 && !direct(o.indices[0]) && direct(o.indices[1])) {
+    const auto& v = in[0];
+    const auto& x = in[1];
+    const auto& w = in[2];
+    const auto& pq = ind(o.indices[0]).args;
+    const std::string& m = dvar(o.indices[1]);
+    if (vars_of(v) == pq && (pq.size() == 1 || pq.size() == 2) && x.indices.size() == 2 &&
+        !direct(x.indices[0]) && ind(x.indices[0]).args == pq && direct(x.indices[1]) &&
+        w.indices.size() == 3 && !direct(w.indices[0]) &&
+        ind(w.indices[0]).args == std::vector<std::string>{pq[0]} && direct(w.indices[1]) &&
+        dvar(w.indices[1]) == dvar(x.indices[1]) && direct(w.indices[2]) &&
+        dvar(w.indices[2]) == m) {
+      return Match{pq.size() == 2 ? Workload::GroupedConv : Workload::Conv,
+                   {{"Out", o.tensor}, {"MAPX", ind(o.indices[0]).tensor}, {"MAPV", v.tensor},
+                    {"In", x.tensor}, {"MAPY", ind(x.indices[0]).tensor}, {"Weight", w.tensor},
+                    {"MAPZ", ind(w.indices[0]).tensor}}};
+    }
+  }
+  // Z[b,CGI[p,q],w] += CGV[p,q] * X[b,CGJ[p,q],u] * Y[b,CGK[p,q]] * W[(b,)CGL[p],u,w]
+  if (in.size() == 4 && o.indices.size() == 3 && direct(o.indices[0]) && !direct(o.indices[1]) &&
+      direct(o.indices[2])) {
+    const auto& v = in[0];
+    const auto& x = in[1];
+    const auto& y = in[2];
+    const auto& w = in[3];
+    const std::string& b = dvar(o.indices[0]);
+    const auto& pq = ind(o.indices[1]).args;
+    const std::string& wv = dvar(o.indices[2]);
+    const bool ok = pq.size() == 2 && vars_of(v) == pq && x.indices.size() == 3 &&
+                    direct(x.indices[0]) && dvar(x.indices[0]) == b && !direct(x.indices[1]) &&
+                    ind(x.indices[1]).args == pq && direct(x.indices[2]) &&
+                    y.indices.size() == 2 && direct(y.indices[0]) && dvar(y.indices[0]) == b &&
+                    !direct(y.indices[1]) && ind(y.indices[1]).args == pq;
+    if (ok) {
+      const std::string& u = dvar(x.indices[2]);
+      const std::vector<std::string> p1{pq[0]};
+      std::map<std::string, std::string> t{{"Z", o.tensor},
+                                           {"CGI", ind(o.indices[1]).tensor},
+                                           {"CGV", v.tensor},
+                                           {"X", x.tensor},
+                                           {"CGJ", ind(x.indices[1]).tensor},
+                                           {"Y", y.tensor},
+                                           {"CGK", ind(y.indices[1]).tensor},
+                                           {"W", w.tensor}};
+      if (w.indices.size() == 4 && direct(w.indices[0]) && dvar(w.indices[0]) == b &&
+          !direct(w.indices[1]) && ind(w.indices[1]).args == p1 && direct(w.indices[2]) &&
+          dvar(w.indices[2]) == u && direct(w.indices[3]) && dvar(w.indices[3]) == wv) {
+        t["CGL"] = ind(w.indices[1]).tensor;
+        return Match{Workload::TpPerEdge, t};
+      }
+      if (w.indices.size() == 3 && !direct(w.indices[0]) && ind(w.indices[0]).args == p1 &&
+          direct(w.indices[1]) && dvar(w.indices[1]) == u && direct(w.indices[2]) &&
+          dvar(w.indices[2]) == wv) {
+        t["CGL"] = ind(w.indices[0]).tensor;
+        return Match{Workload::TpShared, t};
+      }
+    }
+  }
+  return std::nullopt;
+}
+
+// ---------------------------------------------------------- operand moves
+// int64 index tensor -> device int32. A value that does not fit int32 is out
+// of range for any device extent; it is reported by the caller's host check
+// in the reference's order instead of being wrapped.
+std::unique_ptr<DevBuf> up_index(const Tensor& t, bool& unrepresentable) {
   std::vector<int32_t> h(static_cast<size_t>(t.numel()));
-  for (int64_t i = 0; i < t.numel(); ++i) h[i] = static_cast<int32_t>(t.int_at(i));
+  for (int64_t i = 0; i < t.numel(); ++i) {
+    const int64_t v = t.int_at(i);
+    if (v < INT32_MIN || v > INT32_MAX) unrepresentable = true;
+    // in-range values (negative ones included) go through unchanged: the
+    // device check reports them with their own value
+    h[static_cast<size_t>(i)] =
+        static_cast<int32_t>(v < INT32_MIN ? INT32_MIN : (v > INT32_MAX ? INT32_MAX : v));
+  }
   auto d = std::make_unique<DevBuf>(h.size() * 4);
-  cudaMemcpy(d->p, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  detail::cuda_ok(cudaMemcpy(d->p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "H2D");
   return d;
 }
 
 std::unique_ptr<DevBuf> up_f32(const Tensor& t) {
   std::vector<float> h(static_cast<size_t>(t.numel()));
-  for (int64_t i = 0; i < t.numel(); ++i) h[i] = static_cast<float>(t.as_real(i));
+  for (int64_t i = 0; i < t.numel(); ++i) h[static_cast<size_t>(i)] = static_cast<float>(t.as_real(i));
   auto d = std::make_unique<DevBuf>(h.size() * 4);
-  cudaMemcpy(d->p, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  detail::cuda_ok(cudaMemcpy(d->p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "H2D");
   return d;
 }
 
 std::unique_ptr<DevBuf> up_bf16(const Tensor& t) {
   std::vector<__nv_bfloat16> h(static_cast<size_t>(t.numel()));
-  for (int64_t i = 0; i < t.numel(); ++i) h[i] = __float2bfloat16_rn(static_cast<float>(t.as_real(i)));
+  for (int64_t i = 0; i < t.numel(); ++i)
+    h[static_cast<size_t>(i)] = __float2bfloat16_rn(static_cast<float>(t.as_real(i)));
   auto d = std::make_unique<DevBuf>(h.size() * 2);
-  cudaMemcpy(d->p, h.data(), h.size() * 2, cudaMemcpyHostToDevice);
+  detail::cuda_ok(cudaMemcpy(d->p, h.data(), h.size() * 2, cudaMemcpyHostToDevice), "H2D");
   return d;
 }
 
 Tensor down(const DevBuf& d, const Tensor& like) {
   std::vector<float> h(static_cast<size_t>(like.numel()));
-  cudaMemcpy(h.data(), d.p, h.size() * 4, cudaMemcpyDeviceToHost);
+  detail::cuda_ok(cudaMemcpy(h.data(), d.p, h.size() * 4, cudaMemcpyDeviceToHost), "D2H");
   Tensor out = Tensor::zeros(like.kind(), like.shape());
   for (int64_t i = 0; i < like.numel(); ++i) {
-    if (out.is_int()) out.int_at(i) = std::llround(h[i]);
-    else out.real_at(i) = h[i];
+    if (out.is_int()) out.int_at(i) = std::llround(h[static_cast<size_t>(i)]);
+    else out.real_at(i) = h[static_cast<size_t>(i)];
   }
   return out;
 }
 
-const std::string& dvar(const IndexExpr& e) { return std::get<DirectIndex>(e).var; }
-bool direct(const IndexExpr& e) { return std::holds_alternative<DirectIndex>(e); }
-const IndirectIndex& ind(const IndexExpr& e) { return std::get<IndirectIndex>(e); }
+// One indirect access of an index tensor into a target dimension, in the
+// reference's checking order (gathers = inputs in order, then the scatter).
+struct IndexUse {
+  std::string index, target;
+  int dim;
+  int64_t extent;
+};
+
+// checked_index (plan.cpp:249-259) on the host, for statements whose index
+// values do not fit the device's int32: same first offender, same message.
+void host_check(const TensorMap& T, const std::vector<IndexUse>& uses) {
+  for (const auto& u : uses) {
+    const Tensor& it = T.at(u.index);
+    for (int64_t f = 0; f < it.numel(); ++f) {
+      const int64_t v = it.int_at(f);
+      if (v < 0 || v >= u.extent) {
+        throw IndexRangeError("index tensor " + u.index + " value " + std::to_string(v) +
+                              " at position [" + std::to_string(f) + "] out of range for dim " +
+                              std::to_string(u.dim) + " of " + u.target + " (extent " +
+                              std::to_string(u.extent) + ")");
+      }
+    }
+  }
+}
 
 }  // namespace
+
+double device_tolerance(const EinsumStmt& stmt) {
+  auto m = match(stmt);
+  if (!m) return 0.0;
+  // fp32 end to end (compensated sums) vs bf16 operands with fp32 accumulation
+  return (m->wl == Workload::GroupCooSpmm || m->wl == Workload::CooSpmm) ? 1e-5 : 1e-2;
+}
 
 ModeResult execute(const BoundProblem& problem) {
   const auto t0 = std::chrono::steady_clock::now();
@@ -97,85 +244,81 @@ ModeResult execute(const BoundProblem& problem) {
   const auto& T = problem.tensors;
   const Tensor& out = problem.out;
   const int acc = st.accumulate ? 1 : 0;
+  auto m = match(st);
+  if (!m) throw std::invalid_argument("b200 mode: statement outside the hot path: " + to_string(st));
+  const auto& n = m->t;
+  auto at = [&](const char* role) -> const Tensor& { return T.at(n.at(role)); };
   ModeResult mo;
   mo.kernel_count = 1;
-  const auto& o = st.output;
-  const auto& in = st.inputs;
-  // -- GroupCOO / COO SpMM: C[AM[p..],n] (+)= AV[p..] * B[AK[p..],n]
-  if (in.size() == 2 && o.indices.size() == 2 && !direct(o.indices[0]) && direct(o.indices[1]) &&
-      in[1].indices.size() == 2 && !direct(in[1].indices[0])) {
-    const Tensor& AM = T.at(ind(o.indices[0]).tensor);
-    const Tensor& AK = T.at(ind(in[1].indices[0]).tensor);
-    const Tensor& AV = T.at(in[0].tensor);
-    const Tensor& B = T.at(in[1].tensor);
-    const int64_t G = AM.numel(), g = G ? AV.numel() / G : 1;
-    auto dAM = up_index(AM), dAK = up_index(AK);
-    auto dAV = up_f32(AV), dB = up_f32(B), dC = up_f32(out);
-    rethrow(ixb_spmm_groupcoo(static_cast<int32_t*>(dAM->p), static_cast<int32_t*>(dAK->p),
-                              static_cast<float*>(dAV->p), G, g, static_cast<float*>(dB->p),
-                              B.dim(0), B.dim(1), static_cast<float*>(dC->p), out.dim(0), acc, 0,
-                              nullptr),
-            st);
-    mo.result = down(*dC, out);
-    mo.counters = {G * g, G, G * B.dim(1)};
-  } else if (in.size() == 2 && o.indices.size() == 3 && !direct(o.indices[0])) {
-    // -- BlockGroupCOO SpMM: C[AM[p],bm,n] (+)= AV[p,q,bm,bk] * B[AK[p,q],bk,n]
-    const Tensor& AM = T.at(ind(o.indices[0]).tensor);
-    const Tensor& AK = T.at(ind(in[1].indices[0]).tensor);
-    const Tensor& AV = T.at(in[0].tensor);
-    const Tensor& B = T.at(in[1].tensor);
-    auto dAM = up_index(AM), dAK = up_index(AK), dAV = up_bf16(AV), dB = up_bf16(B);
-    auto dC = up_f32(out);
-    rethrow(ixb_spmm_blockgroupcoo(static_cast<int32_t*>(dAM->p), static_cast<int32_t*>(dAK->p),
-                                   dAV->p, AV.dim(0), AV.dim(1), AV.dim(2), AV.dim(3), dB->p,
-                                   B.dim(0), B.dim(2), static_cast<float*>(dC->p), out.dim(0),
-                                   acc, 0, nullptr),
-            st);
-    mo.result = down(*dC, out);
-    mo.counters = {AV.dim(0) * AV.dim(1), AV.dim(0), AV.dim(0) * AV.dim(2) * B.dim(2)};
-  } else if (in.size() == 3 && o.indices.size() == 2 && !direct(o.indices[0])) {
-    // -- (grouped) sparse conv: Out[MAPX[..],m] += MAPV[..] * In[MAPY[..],c] * W[MAPZ[p],c,m]
-    const Tensor& MX = T.at(ind(o.indices[0]).tensor);
-    const Tensor& MV = T.at(in[0].tensor);
-    const Tensor& In = T.at(in[1].tensor);
-    const Tensor& MY = T.at(ind(in[1].indices[0]).tensor);
-    const Tensor& W = T.at(in[2].tensor);
-    const Tensor& MZ = T.at(ind(in[2].indices[0]).tensor);
-    const int64_t G = MZ.numel(), g = G ? MX.numel() / G : 1;
-    auto dMX = up_index(MX), dMY = up_index(MY), dMZ = up_index(MZ), dMV = up_f32(MV);
-    auto dIn = up_bf16(In), dW = up_bf16(W), dO = up_f32(out);
-    rethrow(ixb_conv_grouped(static_cast<int32_t*>(dMZ->p), static_cast<int32_t*>(dMX->p),
-                             static_cast<int32_t*>(dMY->p), static_cast<float*>(dMV->p), G, g,
-                             dIn->p, In.dim(0), In.dim(1), dW->p, W.dim(0), W.dim(2),
-                             static_cast<float*>(dO->p), out.dim(0), acc, 0, nullptr),
-            st);
-    mo.result = down(*dO, out);
-    mo.counters = {G * g, G, G * W.dim(2)};
-  } else if (in.size() == 4 && o.indices.size() == 3 && direct(o.indices[0])) {
-    // -- CG tensor product: Z[b,CGI[p,q],w] += CGV * X[b,CGJ,u] * Y[b,CGK] * W[(b,)CGL[p],u,w]
-    const Tensor& CI = T.at(ind(o.indices[1]).tensor);
-    const Tensor& CV = T.at(in[0].tensor);
-    const Tensor& X = T.at(in[1].tensor);
-    const Tensor& CJ = T.at(ind(in[1].indices[1]).tensor);
-    const Tensor& Y = T.at(in[2].tensor);
-    const Tensor& CK = T.at(ind(in[2].indices[1]).tensor);
-    const Tensor& W = T.at(in[3].tensor);
-    const bool per_b = W.rank() == 4;
-    const Tensor& CL = T.at(ind(in[3].indices[per_b ? 1 : 0]).tensor);
-    const int64_t G = CL.numel(), g = G ? CI.numel() / G : 1;
-    auto dL = up_index(CL), dI = up_index(CI), dJ = up_index(CJ), dK = up_index(CK);
-    auto dV = up_f32(CV), dX = up_bf16(X), dY = up_bf16(Y), dW = up_bf16(W), dZ = up_f32(out);
-    rethrow(ixb_tp_grouped(static_cast<int32_t*>(dL->p), static_cast<int32_t*>(dI->p),
-                           static_cast<int32_t*>(dJ->p), static_cast<int32_t*>(dK->p),
-                           static_cast<float*>(dV->p), G, g, dX->p, dY->p, dW->p, per_b ? 1 : 0,
-                           X.dim(0), out.dim(1), X.dim(1), Y.dim(1), W.dim(per_b ? 1 : 0),
-                           X.dim(2), W.dim(per_b ? 3 : 2), static_cast<float*>(dZ->p), acc, 0,
-                           nullptr),
-            st);
-    mo.result = down(*dZ, out);
-    mo.counters = {G * g, G, G * X.dim(0) * W.dim(per_b ? 3 : 2)};
-  } else {
-    throw std::invalid_argument("b200 mode: statement outside the hot path: " + to_string(st));
+  bool wide = false;  // an index value beyond int32
+  switch (m->wl) {
+    case Workload::GroupCooSpmm:
+    case Workload::CooSpmm: {
+      const Tensor &AM = at("AM"), &AK = at("AK"), &AV = at("AV"), &B = at("B");
+      const int64_t G = AM.numel(), g = G ? AV.numel() / G : 1;
+      auto dAM = up_index(AM, wide), dAK = up_index(AK, wide);
+      if (wide) host_check(T, {{n.at("AK"), n.at("B"), 0, B.dim(0)}, {n.at("AM"), n.at("C"), 0, out.dim(0)}});
+      auto dAV = up_f32(AV), dB = up_f32(B), dC = up_f32(out);
+      check(ixb_spmm_groupcoo(dAM->as<int32_t>(), dAK->as<int32_t>(), dAV->as<float>(), G, g,
+                              dB->as<float>(), B.dim(0), B.dim(1), dC->as<float>(), out.dim(0),
+                              acc, 0, nullptr));
+      mo.result = down(*dC, out);
+      mo.counters = {G * g, G, G * B.dim(1)};
+      break;
+    }
+    case Workload::BlockGroupCooSpmm: {
+      const Tensor &AM = at("AM"), &AK = at("AK"), &AV = at("AV"), &B = at("B");
+      auto dAM = up_index(AM, wide), dAK = up_index(AK, wide);
+      if (wide) host_check(T, {{n.at("AK"), n.at("B"), 0, B.dim(0)}, {n.at("AM"), n.at("C"), 0, out.dim(0)}});
+      auto dAV = up_bf16(AV), dB = up_bf16(B), dC = up_f32(out);
+      check(ixb_spmm_blockgroupcoo(dAM->as<int32_t>(), dAK->as<int32_t>(), dAV->p, AV.dim(0),
+                                   AV.dim(1), AV.dim(2), AV.dim(3), dB->p, B.dim(0), B.dim(2),
+                                   dC->as<float>(), out.dim(0), acc, 0, nullptr));
+      mo.result = down(*dC, out);
+      mo.counters = {AV.dim(0) * AV.dim(1), AV.dim(0), AV.dim(0) * AV.dim(2) * B.dim(2)};
+      break;
+    }
+    case Workload::GroupedConv:
+    case Workload::Conv: {
+      const Tensor &MX = at("MAPX"), &MV = at("MAPV"), &In = at("In"), &MY = at("MAPY"),
+                   &W = at("Weight"), &MZ = at("MAPZ");
+      const int64_t G = MZ.numel(), g = G ? MX.numel() / G : 1;
+      auto dMX = up_index(MX, wide), dMY = up_index(MY, wide), dMZ = up_index(MZ, wide);
+      if (wide)
+        host_check(T, {{n.at("MAPY"), n.at("In"), 0, In.dim(0)},
+                       {n.at("MAPZ"), n.at("Weight"), 0, W.dim(0)},
+                       {n.at("MAPX"), n.at("Out"), 0, out.dim(0)}});
+      auto dMV = up_f32(MV), dIn = up_bf16(In), dW = up_bf16(W), dO = up_f32(out);
+      check(ixb_conv_grouped(dMZ->as<int32_t>(), dMX->as<int32_t>(), dMY->as<int32_t>(),
+                             dMV->as<float>(), G, g, dIn->p, In.dim(0), In.dim(1), dW->p,
+                             W.dim(0), W.dim(2), dO->as<float>(), out.dim(0), acc, 0, nullptr));
+      mo.result = down(*dO, out);
+      mo.counters = {G * g, G, G * W.dim(2)};
+      break;
+    }
+    case Workload::TpPerEdge:
+    case Workload::TpShared: {
+      const Tensor &CI = at("CGI"), &CV = at("CGV"), &X = at("X"), &CJ = at("CGJ"), &Y = at("Y"),
+                   &CK = at("CGK"), &W = at("W"), &CL = at("CGL");
+      const bool per_b = m->wl == Workload::TpPerEdge;
+      const int64_t G = CL.numel(), g = G ? CI.numel() / G : 1;
+      auto dL = up_index(CL, wide), dI = up_index(CI, wide), dJ = up_index(CJ, wide),
+           dK = up_index(CK, wide);
+      if (wide)
+        host_check(T, {{n.at("CGJ"), n.at("X"), 1, X.dim(1)},
+                       {n.at("CGK"), n.at("Y"), 1, Y.dim(1)},
+                       {n.at("CGL"), n.at("W"), per_b ? 1 : 0, W.dim(per_b ? 1 : 0)},
+                       {n.at("CGI"), n.at("Z"), 1, out.dim(1)}});
+      auto dV = up_f32(CV), dX = up_bf16(X), dY = up_bf16(Y), dW = up_bf16(W), dZ = up_f32(out);
+      check(ixb_tp_grouped(dL->as<int32_t>(), dI->as<int32_t>(), dJ->as<int32_t>(),
+                           dK->as<int32_t>(), dV->as<float>(), G, g, dX->p, dY->p, dW->p,
+                           per_b ? 1 : 0, X.dim(0), out.dim(1), X.dim(1), Y.dim(1),
+                           W.dim(per_b ? 1 : 0), X.dim(2), W.dim(per_b ? 3 : 2), dZ->as<float>(),
+                           acc, 0, nullptr));
+      mo.result = down(*dZ, out);
+      mo.counters = {G * g, G, G * X.dim(0) * W.dim(per_b ? 3 : 2)};
+      break;
+    }
   }
   mo.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
                    .count();

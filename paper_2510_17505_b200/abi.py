@@ -110,6 +110,8 @@ _SIGS = {
     "ixb_tp_plan_run_host": (C.c_int, [C.c_void_p] * 4 + [C.c_int64, C.c_void_p, C.c_int,
                                                           C.c_int, C.c_int, C.c_void_p]),
     "ixb_shard_groups": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "ixb_tune_brute": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]),
     "ixb_tune_report": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ixb_ixt_info": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]),

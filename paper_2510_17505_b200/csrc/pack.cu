@@ -87,7 +87,7 @@ __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
 int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_empty_rows,
                       cudaStream_t s, double* gstar_out, int64_t* cand_g = nullptr,
                       double* cand_score = nullptr, int* ncand = nullptr,
-                      int64_t* total_out = nullptr) {
+                      int64_t* total_out = nullptr, int64_t* maxocc_out = nullptr) {
   Scratch<OccStats> d(1, s);
   IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
   if (n > 0) {
@@ -102,6 +102,7 @@ int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_e
   IXB_CUDA_CHECK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
   IXB_CUDA_CHECK(cudaStreamSynchronize(s));
   if (total_out) *total_out = static_cast<int64_t>(h.S);
+  if (maxocc_out) *maxocc_out = static_cast<int64_t>(h.maxocc);
   // g_star (tuner.cpp:60-65)
   double gs = 1.0;
   if (h.S > 0) {
@@ -161,6 +162,8 @@ template <>
 __device__ __forceinline__ bool nz<uint8_t>(uint8_t v) { return v != 0; }
 template <>
 __device__ __forceinline__ bool nz<double>(double v) { return v != 0.0; }
+template <>
+__device__ __forceinline__ bool nz<int64_t>(int64_t v) { return v != 0; }
 
 // Dense-source element types: fp32, bf16, fp64 (u8 for block flags).
 template <typename F>
@@ -168,13 +171,16 @@ void dispatch_dense(int dtype, F&& f) {
   if (dtype == IXB_F32) f(float{});
   else if (dtype == IXB_BF16) f(__nv_bfloat16{});
   else if (dtype == IXB_F64) f(double{});
+  else if (dtype == IXB_I64) f(int64_t{});
   else f(uint8_t{});
 }
 void check_dense_dtype(int dtype) {
-  if (dtype != IXB_F32 && dtype != IXB_BF16 && dtype != IXB_F64)
+  if (dtype != IXB_F32 && dtype != IXB_BF16 && dtype != IXB_F64 && dtype != IXB_I64)
     fail(IXB_FAILURE, "unsupported dtype");
 }
-int dense_bytes(int dtype) { return dtype == IXB_BF16 ? 2 : dtype == IXB_F64 ? 8 : 4; }
+int dense_bytes(int dtype) {
+  return dtype == IXB_BF16 ? 2 : (dtype == IXB_F64 || dtype == IXB_I64) ? 8 : 4;
+}
 
 template <typename T>
 struct Vec16 {
@@ -309,6 +315,28 @@ __global__ void occupancy_kernel(const int32_t* c, int64_t n, int64_t ext, int32
       if (h[b]) atomicAdd(o + b, h[b]);
   }
 }
+// brute_force_optimal (tuner.cpp:86-97): F(g) = (g+1) * sum_i ceil(occ_i / g)
+// for every g in [1, maxocc]; a CTA per g (grid-stride), threads over rows.
+__global__ void brute_cost_kernel(const int32_t* occ, int64_t n, int64_t maxocc,
+                                  unsigned long long* F) {
+  __shared__ unsigned long long red[kWarp];
+  for (int64_t g = blockIdx.x + 1; g <= maxocc; g += gridDim.x) {
+    unsigned long long sum = 0;
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x)
+      sum += (static_cast<unsigned long long>(occ[r]) + g - 1) / g;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+      F[g - 1] = static_cast<unsigned long long>(g + 1) * t;
+    }
+    __syncthreads();
+  }
+}
+
 void launch_occupancy(const int32_t* coord, int64_t nnz, int64_t extent, int32_t* occ,
                       cudaStream_t s) {
   int64_t grid = ceil_div(nnz, kTB);
@@ -1063,6 +1091,45 @@ int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int c
       launch_occupancy(coord, nnz, extent, occ.p, s);
     }
     *g_out = tune_from_occ(occ.p, extent, extent, count_empty_rows, s, gstar_out);
+  });
+}
+
+int ixb_tune_brute(const int32_t* coord, int64_t nnz, int64_t extent, ixb_stream stream,
+                   int64_t* g_out, int64_t* f_out) {
+  return ixb_guard([&] {
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (!g_out || !f_out) fail(IXB_SHAPE, "ixb_tune_brute: null output");
+    *g_out = 0;
+    *f_out = 0;
+    if (nnz == 0 || extent == 0) return;  // empty profile: nullopt (g_out = 0)
+    Scratch<int32_t> occ(extent + 1, s);
+    IXB_CUDA_CHECK(cudaMemsetAsync(occ.p, 0, (extent + 1) * 4, s));
+    launch_occupancy(coord, nnz, extent, occ.p, s);
+    int64_t maxocc = 0;
+    {
+      // max occupancy from the tuner's one-pass statistics
+      int64_t total = 0;
+      tune_from_occ(occ.p, extent, extent, 0, s, nullptr, nullptr, nullptr, nullptr, &total,
+                    &maxocc);
+    }
+    if (maxocc < 1) return;
+    Scratch<unsigned long long> F(maxocc, s);
+    const int64_t grid = maxocc < 4 * sm_count() ? maxocc : 4 * sm_count();
+    brute_cost_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(occ.p, extent, maxocc, F.p);
+    IXB_LAUNCH_CHECK("brute_cost_kernel");
+    std::vector<unsigned long long> h(static_cast<size_t>(maxocc));
+    IXB_CUDA_CHECK(cudaMemcpyAsync(h.data(), F.p, maxocc * 8, cudaMemcpyDeviceToHost, s));
+    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    int64_t best_g = 1;
+    unsigned long long best_f = h[0];
+    for (int64_t g = 2; g <= maxocc; ++g) {  // strict < : ties keep the smaller g
+      if (h[static_cast<size_t>(g - 1)] < best_f) {
+        best_f = h[static_cast<size_t>(g - 1)];
+        best_g = g;
+      }
+    }
+    *g_out = best_g;
+    *f_out = static_cast<int64_t>(best_f);
   });
 }
 

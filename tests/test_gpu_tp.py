@@ -223,3 +223,48 @@ def test_tp_plan_run_host_per_edge_w(P, ixo):
                   cuda(t2["W"], torch.bfloat16), Z2, accumulate=False, nchunks=3)
     want2 = ixo.einsum(expr, t2, on, np.zeros((Bl, ni, Wd), np.int64))
     np.testing.assert_array_equal(Z2.numpy().astype(np.int64), want2)
+
+
+def test_tp_tcgen05_rotation_equivariance(P):
+    """The tensor-core TP on spherical-harmonic inputs is rotation equivariant:
+    X[b, :, u] = a_u Y(r1_b), Y[b, :] = Y(r2_b) (real SH, l <= 3); rotating every
+    direction rotates each output irrep block, so the norm of every (edge,
+    channel, l3 block) of Z is unchanged. bf16 inputs: held to 2e-2 of the
+    block norm scale."""
+    from scipy.spatial.transform import Rotation
+
+    from test_cg_pinned import real_sh
+    from paper_2510_17505_b200 import synth as S
+    cg = S.cg_table(3)
+    nl = cg["npaths"]
+    l = cg["l"].cuda()
+    gt = P.group_coo_tensor([16, 16, 16, nl], [cg["i"].cuda(), cg["j"].cuda(), cg["k"].cuda(), l],
+                            cg["v"].cuda(), 3, 4)
+    plan = P.TpPlan(gt.group_coord, *gt.member_coords, gt.values, 16, 16, 16, nl)
+    rng = np.random.default_rng(5)
+    Bn = 200
+    r1 = rng.normal(size=(Bn, 3))
+    r2 = rng.normal(size=(Bn, 3))
+    r1 /= np.linalg.norm(r1, axis=1, keepdims=True)
+    r2 /= np.linalg.norm(r2, axis=1, keepdims=True)
+    a = rng.uniform(0.5, 1.5, size=64)
+    W = torch.from_numpy(rng.normal(size=(nl, 64, 64)) / 8).to(torch.bfloat16).cuda()
+
+    def run(d1, d2):
+        sh1 = np.concatenate([real_sh(k, d1) for k in range(4)], axis=1)  # [B, 16]
+        sh2 = np.concatenate([real_sh(k, d2) for k in range(4)], axis=1)
+        X = torch.from_numpy(sh1[:, :, None] * a[None, None, :]).to(torch.bfloat16).cuda()
+        Y = torch.from_numpy(sh2).to(torch.bfloat16).cuda()
+        Z = torch.empty((Bn, 16, 64), device="cuda")
+        plan.run(X.contiguous(), Y.contiguous(), W, Z, accumulate=False)
+        return Z.double()
+
+    R = Rotation.random(random_state=9).as_matrix()
+    Z0, Z1 = run(r1, r2), run(r1 @ R.T, r2 @ R.T)
+    for l3 in range(4):
+        blk = slice(l3 * l3, (l3 + 1) * (l3 + 1))
+        n0 = Z0[:, blk, :].norm(dim=1)
+        n1 = Z1[:, blk, :].norm(dim=1)
+        scale = n0.max().item()
+        assert scale > 0
+        assert ((n1 - n0).abs().max().item()) <= 2e-2 * scale, l3
