@@ -245,13 +245,23 @@ class ConvPlan:
         self.keep = [t.contiguous() if t is not None else None for t in (MAPZ, MAPX, MAPY, MAPV)]
         MAPZ, MAPX, MAPY, MAPV = self.keep
         G, g = MAPX.shape
+        self.n_in, self.n_off, self.n_out = n_in, n_off, n_out
         self._free = lib().ixb_conv_plan_free
         self.h = C.c_void_p()
         check(lib().ixb_conv_plan_create(_ptr(MAPZ), _ptr(MAPX), _ptr(MAPY), _ptr(MAPV), G, g,
                                          n_in, n_off, n_out, flags, _stream(stream),
                                          C.byref(self.h)))
 
+    def _check(self, In, Weight, Out, host):
+        if In.dim() != 2 or Weight.dim() != 3:
+            raise ShapeError(4, "ConvPlan: In is [n_in, Cin], Weight [n_off, Cin, Cout]")
+        cin, cout = In.shape[1], Weight.shape[2]
+        _operand("In", In, (self.n_in, cin), torch.bfloat16, device=not host)
+        _operand("Weight", Weight, (self.n_off, cin, cout), torch.bfloat16)
+        _operand("Out", Out, (self.n_out, cout), torch.float32, device=not host)
+
     def run(self, In, Weight, Out, accumulate=True, flags=0, stream=None):
+        self._check(In, Weight, Out, host=False)
         check(lib().ixb_conv_plan_run(self.h, _ptr(In), In.shape[1], _ptr(Weight),
                                       Weight.shape[2], _ptr(Out), int(accumulate), flags,
                                       _stream(stream)))
@@ -260,9 +270,7 @@ class ConvPlan:
     def run_host(self, In, Weight, Out, accumulate=True, flags=0, nchunks=8, stream=None):
         """In, Out: host tensors (pinned for overlap); Weight: device. Output
         tiles run in chunks as their input rows land (ixb_conv_plan_run_host)."""
-        for t in (In, Out):
-            if t.is_cuda or not t.is_contiguous():
-                raise ValueError("run_host takes contiguous host tensors for In and Out")
+        self._check(In, Weight, Out, host=True)
         check(lib().ixb_conv_plan_run_host(self.h, _ptr(In), In.shape[1], _ptr(Weight),
                                            Weight.shape[2], _ptr(Out), int(accumulate), flags,
                                            nchunks, _stream(stream)))
@@ -318,6 +326,31 @@ def tp_grouped(CGL, CGI, CGJ, CGK, CGV, X, Y, W, Z, accumulate=True, flags=0, st
     return Z
 
 
+def _operand(name, t, shape, dtype, device=True):
+    """Shape/dtype/device/contiguity check of a plan operand: the C-ABI only
+    receives the batch or channel counts, so a mismatched tensor would be read
+    or written out of bounds."""
+    if tuple(t.shape) != tuple(shape):
+        raise ShapeError(4, f"{name}: expected shape {list(shape)}, got {list(t.shape)}")
+    if t.dtype != dtype:
+        raise ShapeError(4, f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ShapeError(4, f"{name}: must be contiguous")
+    if device and not t.is_cuda:
+        raise ShapeError(4, f"{name}: must be a CUDA tensor")
+    if not device and t.is_cuda:
+        raise ShapeError(4, f"{name}: must be a host tensor")
+    return t
+
+
+def _host_out(C_out):
+    """Host output buffer of the *_host calls: written in place, so it must be
+    contiguous (a .contiguous() copy would silently drop the result)."""
+    if C_out.is_cuda or not C_out.is_contiguous() or C_out.dtype != torch.float32:
+        raise ShapeError(4, "C_out must be a contiguous float32 host tensor")
+    return C_out
+
+
 def _host(t, dtype=None):
     if t.is_cuda:
         raise ShapeError(4, "host-buffer calls take CPU tensors (pinned for full overlap)")
@@ -334,7 +367,7 @@ def spmm_groupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=2
     AV2 = AV if AV.dim() == 2 else AV.reshape(-1, 1)
     G, g = AV2.shape
     check(lib().ixb_spmm_groupcoo_host(_ptr(AM), _ptr(AK), _ptr(AV2), G, g, _ptr(B), B.shape[0],
-                                       B.shape[1], _ptr(_host(C_out)), C_out.shape[0],
+                                       B.shape[1], _ptr(_host_out(C_out)), C_out.shape[0],
                                        int(accumulate), flags, nchunks, _stream(stream)))
     return C_out
 
@@ -345,7 +378,7 @@ def spmm_blockgroupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchu
     AM, AK, AV, B = _host(AM, torch.int32), _host(AK, torch.int32), _host(AV), _host(B)
     G, g, bm, bk = AV.shape
     check(lib().ixb_spmm_blockgroupcoo_host(_ptr(AM), _ptr(AK), _ptr(AV), G, g, bm, bk, _ptr(B),
-                                            B.shape[0], B.shape[2], _ptr(_host(C_out)),
+                                            B.shape[0], B.shape[2], _ptr(_host_out(C_out)),
                                             C_out.shape[0], int(accumulate), flags, nchunks,
                                             _stream(stream)))
     return C_out
@@ -362,14 +395,27 @@ class TpPlan:
         self.keep = [t.contiguous() for t in (CGL, CGI, CGJ, CGK, CGV)]
         CGL, CGI, CGJ, CGK, CGV = self.keep
         G, g = CGI.shape
-        self.ni, self.Wd = ni, Wd
+        self.ni, self.nj, self.nk, self.nl, self.U, self.Wd = ni, nj, nk, nl, U, Wd
+        self.w_per_batch = bool(w_per_batch)
         self._free = lib().ixb_tp_plan_free
         self.h = C.c_void_p()
         check(lib().ixb_tp_plan_create(_ptr(CGL), _ptr(CGI), _ptr(CGJ), _ptr(CGK), _ptr(CGV), G,
                                        g, int(w_per_batch), ni, nj, nk, nl, U, Wd, flags,
                                        _stream(stream), C.byref(self.h)))
 
+    def _check(self, X, Y, W, Z, host):
+        if X.dim() != 3:
+            raise ShapeError(4, f"TpPlan: X is [batch, {self.nj}, {self.U}]")
+        b = X.shape[0]
+        _operand("X", X, (b, self.nj, self.U), torch.bfloat16, device=not host)
+        _operand("Y", Y, (b, self.nk), torch.bfloat16, device=not host)
+        wshape = ((b, self.nl, self.U, self.Wd) if self.w_per_batch else
+                  (self.nl, self.U, self.Wd))
+        _operand("W", W, wshape, torch.bfloat16)  # device in both forms
+        _operand("Z", Z, (b, self.ni, self.Wd), torch.float32, device=not host)
+
     def run(self, X, Y, W, Z, accumulate=True, flags=0, stream=None):
+        self._check(X, Y, W, Z, host=False)
         check(lib().ixb_tp_plan_run(self.h, _ptr(X), _ptr(Y), _ptr(W), X.shape[0], _ptr(Z),
                                     int(accumulate), flags, _stream(stream)))
         return Z
@@ -377,9 +423,7 @@ class TpPlan:
     def run_host(self, X, Y, W, Z, accumulate=True, flags=0, nchunks=8, stream=None):
         """X, Y, Z: host tensors (pinned for overlap); W: device. Chunked
         copy-in / evaluate / copy-out on three streams (ixb_tp_plan_run_host)."""
-        for t in (X, Y, Z):
-            if t.is_cuda or not t.is_contiguous():
-                raise ValueError("run_host takes contiguous host tensors for X, Y and Z")
+        self._check(X, Y, W, Z, host=True)
         check(lib().ixb_tp_plan_run_host(self.h, _ptr(X), _ptr(Y), _ptr(W), X.shape[0],
                                          _ptr(Z), int(accumulate), flags, nchunks,
                                          _stream(stream)))

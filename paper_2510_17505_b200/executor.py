@@ -244,9 +244,18 @@ class ModeResult:
     wall_ms: float
 
 
-def _to_dev(x, dtype, device):
+def _to_dev(x, dtype, device, name=None):
     if isinstance(x, np.ndarray):
         x = torch.from_numpy(np.ascontiguousarray(x))
+    if dtype == torch.int32 and x.dtype in (torch.int64, torch.uint64) and x.numel():
+        # device indices are int32: a value beyond it is out of range for any
+        # extent and must raise, not wrap (narrowing is checked, not truncated)
+        lo, hi = int(x.min()), int(x.max())
+        if lo < -2**31 or hi >= 2**31:
+            bad = int((x < -2**31).logical_or(x >= 2**31).nonzero()[0, 0])
+            v = int(x.reshape(-1)[bad])
+            raise IndexRangeError(6, f"index tensor {name} value {v} at position [{bad}] "
+                                     "exceeds the device's int32 range")
     return x.to(device=device, dtype=dtype, non_blocking=True).contiguous()
 
 
@@ -275,10 +284,13 @@ def execute_mode(mode, expr, tensors, out_name, out, value_dtype=None, device=No
         for nm in [a.tensor] + [i.tensor for i in a.indices if not i.direct]:
             if nm not in tensors:
                 raise BindError(3, f"unbound tensor {nm}")
+    for nm in [i.tensor for i in st.output.indices if not i.direct]:  # output indirection
+        if nm not in tensors:
+            raise BindError(3, f"unbound tensor {nm}")
     wl, bind = match_workload(st)
     if wl is None:
         raise ShapeError(4, f"statement is outside the B200 hot path: {expr}")
-    ix = lambda n: _to_dev(tensors[bind[n]], torch.int32, device)
+    ix = lambda n: _to_dev(tensors[bind[n]], torch.int32, device, bind[n])
     acc = st.accumulate
     o_np = out if isinstance(out, np.ndarray) else out.cpu().numpy()
     launches0 = lib().ixb_launch_count()
