@@ -43,6 +43,10 @@ void set_max_dynamic_smem(const void* func, int bytes, const char* name);
 
 // Per-device error record (lazily allocated, reset after each check).
 ErrorRecord* device_error_record();
+// n arrival counters for a kernel launched on `stream` (one region per
+// stream, so concurrent launches never share one): zero on entry, and every
+// kernel using them leaves them zero again.
+unsigned* work_counters(cudaStream_t stream, size_t n);
 // Resets the record on `stream` before a checked launch.
 void reset_error_record(cudaStream_t stream);
 // Syncs `stream`, reads the record; on an offender throws IXB_INDEX_RANGE with

@@ -19,7 +19,13 @@ struct DeviceCtx {
   ixb::ErrorRecord* rec = nullptr;
   int sms = 0;
   std::vector<std::pair<const void*, int>> smem_optin;  // (kernel, bytes) opted in
+  // self-resetting work counters of the persistent kernels, one pair per
+  // stream (kernels on different streams must not share a counter)
+  unsigned* counters = nullptr;
+  std::vector<cudaStream_t> counter_streams;
 };
+constexpr int kCounterSlots = 64;
+constexpr size_t kCountersPerSlot = 16384;
 std::mutex g_mu;
 std::vector<DeviceCtx> g_dev;
 
@@ -72,6 +78,24 @@ void set_max_dynamic_smem(const void* func, int bytes, const char* name) {
 }
 
 ErrorRecord* device_error_record() { return ctx().rec; }
+
+unsigned* work_counters(cudaStream_t stream, size_t n) {
+  if (n > kCountersPerSlot) fail(IXB_FAILURE, "work_counters: too many counters");
+  DeviceCtx& c = ctx();
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!c.counters) {
+    const size_t bytes = kCounterSlots * kCountersPerSlot * sizeof(unsigned);
+    cuda_check(cudaMalloc(&c.counters, bytes), "cudaMalloc(counters)");
+    cuda_check(cudaMemset(c.counters, 0, bytes), "cudaMemset");
+  }
+  size_t i = 0;
+  while (i < c.counter_streams.size() && c.counter_streams[i] != stream) ++i;
+  if (i == c.counter_streams.size()) {
+    if (i == kCounterSlots) fail(IXB_FAILURE, "work_counter: more than 64 streams on one device");
+    c.counter_streams.push_back(stream);
+  }
+  return c.counters + kCountersPerSlot * i;
+}
 
 void reset_error_record(cudaStream_t stream) {
   IXB_CUDA_CHECK(cudaMemsetAsync(&ctx().rec->key, 0xff, sizeof(unsigned long long), stream));

@@ -11,12 +11,15 @@
 //   D         = TMEM, 128 lanes (n) x 16 columns (bm) per 128-wide n subtile.
 // One UMMA M=128,N=16,K=16 per stored block and n subtile.
 //
-// Work split: CTA (chunk of CH group positions, n tile of 128*NSUB columns)
-// owns every row segment (run of equal AM) that starts in its chunk, so each
-// C block-row slice has exactly one writer (deterministic, no atomics).
-// Warp roles: warp 0 = segment scan + TMA producer, warp 1 = TMEM allocator +
-// single-thread UMMA issuer, warps 2..5 = epilogue (TMEM -> registers ->
-// coalesced fp32 stores along n). A STAGES-deep full/empty mbarrier ring
+// Work split: static and balanced. CTA c of NC owns the group positions
+// [G*c/NC, G*(c+1)/NC) (equal slot counts, so equal B-tile bytes and MMAs
+// per CTA); rows crossing a range boundary are summed from per-CTA partials
+// in CTA order by the last CTA to finish its part (no float atomics;
+// deterministic for a given grid). Whole rows are written from TMEM.
+// Warp roles (TcRoles): 4 epilogue warps (TMEM -> registers -> coalesced
+// fp32 stores along n), a scheduler warp (range walk -> segment queue),
+// NPROD TMA producer warps (stage batches round-robin) and NSUB UMMA issuer
+// warps (one per 128-wide n subtile). A STAGES-deep full/empty mbarrier ring
 // feeds the tensor core; accumulators are double buffered in TMEM so the
 // epilogue of segment j overlaps the main loop of segment j+1.
 #include <cudaTypedefs.h>
@@ -33,7 +36,38 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreadsTC = 224;  // 7 warps
+#ifndef IXB_K4_SPS
+#define IXB_K4_SPS 2
+#endif
+#ifndef IXB_K4_STAGES
+#define IXB_K4_STAGES 3
+#endif
+#ifndef IXB_K4_NPROD
+#define IXB_K4_NPROD 2
+#endif
+#ifndef IXB_K4_MINB
+#define IXB_K4_MINB 2
+#endif
+constexpr int kSps = IXB_K4_SPS;
+
+#ifdef IXB_K4_TRACE
+// perf experiment: per-CTA globaltimer stamps of the pipeline's milestones
+__device__ long long g_k4_trace[4096 * 16];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define K4TR(slot) (g_k4_trace[blockIdx.x * 16 + (slot)] = gtimer())
+#define K4TR_FIRST(slot) \
+  do { if (!g_k4_trace[blockIdx.x * 16 + (slot)]) K4TR(slot); } while (0)
+#define K4TR_SET(slot, v) (g_k4_trace[blockIdx.x * 16 + (slot)] = (v))
+#else
+#define K4TR(slot) ((void)0)
+#define K4TR_FIRST(slot) ((void)0)
+#define K4TR_SET(slot, v) ((void)0)
+#endif
+
 constexpr uint32_t kAvBytes = 16 * 16 * 2;
 constexpr uint32_t kSubBytes = 16 * 128 * 2;  // one 128-wide n subtile of a B tile
 
@@ -42,19 +76,34 @@ struct TcArgs {
   const int32_t* AK;
   float* C;
   int64_t G, g, KB, N, MB;
-  int chunk;    // group positions scanned per work item
-  int nchunks;  // ceil(G / chunk)
   int ntiles;   // n tiles of 128*NSUB columns
   int accumulate;
   int check;
   int epi_sleep_ns;  // epilogue warps back off instead of spinning on acc_full
+  float* part;       // [grid][2][16][N] partial block-rows of rows split across CTAs
+  unsigned* rowctr;  // [grid * ntiles] arrival counters of split rows (zero, self-resetting)
   ErrorRecord* err;
 };
 
-// A stage carries SPS consecutive slots of one row segment: SPS B tiles
-// (1024-aligned), then SPS AV blocks. One full/empty round trip and one
-// tcgen05.commit per 2*SPS UMMAs: commits interleaved with tiny MMA batches
-// roughly double the tensor pipe's per-MMA cost (profiles/k4_diag_r1.md).
+// Warp roles. Issue cost on sm_100a is per issuing warp (a UMMA or TMA
+// occupies its warp for ~130-240 cycles however small it is,
+// profiles/k4_diag_r2.md §1), so the small M=128, N=16 block MMAs are spread
+// over NSUB issuer warps (one per 128-wide n subtile) and the TMA boxes over
+// NPROD producer warps; the tensor pipe saturates from ~4 issue streams/SM.
+template <int NSUB, int NPROD>
+struct TcRoles {
+  static constexpr int kEpi = 4;              // warps 0..3: epilogue (TMEM lane quarters)
+  static constexpr int kSched = 4;            // segment scheduler
+  static constexpr int kProd0 = 5;            // producers kProd0 .. kProd0+NPROD-1
+  static constexpr int kIss0 = 5 + NPROD;     // issuers (sub) kIss0 .. kIss0+NSUB-1
+  static constexpr int kWarps = 5 + NPROD + NSUB;
+  static constexpr int kThreads = kWarps * 32;
+};
+
+// A stage carries up to SPS consecutive slots of one row segment: SPS B tiles
+// (the whole 128*NSUB-column n tile of 16 rows, one TMA box each), then the
+// SPS AV blocks (one TMA box for all of them: a segment's slots are
+// contiguous in AV).
 template <int NSUB, int STAGES, int SPS>
 struct TcSmem {
   static constexpr uint32_t kBBytes = NSUB * kSubBytes;
@@ -63,76 +112,49 @@ struct TcSmem {
   static constexpr uint32_t kTotal = kTileBytes + 1024 /*barriers+queue*/ + 1024 /*align*/;
 };
 
-// A row segment (run of equal AM) owned by a work item.
-struct Seg {
-  int64_t s, e;   // group range [s, e)
-  int row, prev;  // AM value, AM[s-1] (or -1)
-  int ntile;      // n tile index
-};
-
-// Walks this CTA's work items (chunk, n tile), round-robin over the grid,
-// and yields every segment that starts inside the chunk. Warp-collective;
-// each role warp runs its own copy and sees the identical sequence.
-struct SegIter {
-  int64_t w;        // current work item
-  int64_t base;     // first group position of the chunk
-  unsigned starts;  // pending segment starts (lane bits) in the chunk
-  int am, amp;      // this lane's AM[base+lane], AM[base+lane-1]
-  int ntile;
-
-  __device__ __forceinline__ void load(const TcArgs& a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t chunk_id = w / a.ntiles;
-    ntile = static_cast<int>(w % a.ntiles);
-    base = chunk_id * a.chunk;
-    const int64_t p = base + lane;
-    const bool in = lane < a.chunk && p < a.G;
-    am = in ? __ldg(a.AM + p) : 0;
-    amp = (in && p > 0) ? __ldg(a.AM + p - 1) : -1;
-    starts = __ballot_sync(0xffffffffu, in && (p == 0 || am != amp));
+// Static balanced schedule. CTA c owns the group positions
+// [G*c/NC, G*(c+1)/NC) of the (row-sorted) format — equal slot counts, so
+// equal B-tile bytes and MMAs per CTA and per SM. A row (run of equal AM)
+// that crosses a range boundary is split: each CTA accumulates its part in
+// TMEM, stores it as a partial block-row, and the last CTA to arrive sums
+// the partials in CTA order (fixed order: deterministic for a given grid).
+// Whole rows — the common case — are written straight from TMEM.
+__device__ __forceinline__ int64_t range_lo(int64_t G, int64_t nc, int64_t c) {
+  return G * c / nc;
+}
+// CTA whose range holds group position p
+__device__ __forceinline__ int owner_cta(int64_t G, int64_t nc, int64_t p) {
+  return static_cast<int>(((p + 1) * nc + G - 1) / G - 1);
+}
+// First position >= p (< lim) whose AM differs from `row` (warp-collective).
+__device__ __forceinline__ int64_t run_end(const int32_t* AM, int64_t p, int64_t lim, int row) {
+  const int lane = threadIdx.x & 31;
+  for (;; p += 32) {
+    const int64_t q = p + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, q >= lim || __ldg(AM + q) != row);
+    if (m) return p + __ffs(m) - 1;
   }
-  __device__ __forceinline__ void init(const TcArgs& a) {
-    w = blockIdx.x;
-    if (w < static_cast<int64_t>(a.nchunks) * a.ntiles) load(a);
-    else starts = 0;
+}
+// First position of the run of `row` that contains position p (warp-collective).
+__device__ __forceinline__ int64_t run_start(const int32_t* AM, int64_t p, int row) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const int64_t q = p - 1 - lane;  // p-1, p-2, ...
+    const unsigned m = __ballot_sync(0xffffffffu, q < 0 || __ldg(AM + q) != row);
+    if (m) return p - (__ffs(m) - 1);
+    p -= 32;
   }
-  __device__ __forceinline__ bool next(const TcArgs& a, Seg& out) {
-    const int64_t total = static_cast<int64_t>(a.nchunks) * a.ntiles;
-    while (starts == 0) {
-      w += gridDim.x;
-      if (w >= total) return false;
-      load(a);
-    }
-    const int lane = threadIdx.x & 31;
-    const int sl = __ffs(starts) - 1;
-    starts &= starts - 1;
-    out.s = base + sl;
-    out.row = __shfl_sync(0xffffffffu, am, sl);
-    out.prev = __shfl_sync(0xffffffffu, amp, sl);
-    out.ntile = ntile;
-    int64_t e = out.s + 1;
-    for (;;) {
-      const int64_t pp = e + lane;
-      const bool diff = pp >= a.G || __ldg(a.AM + pp) != out.row;
-      const unsigned m = __ballot_sync(0xffffffffu, diff);
-      if (m) {
-        e += __ffs(m) - 1;
-        break;
-      }
-      e += 32;
-    }
-    out.e = e;
-    return true;
-  }
-};
+}
 
 constexpr int kQN = 16;  // segment queue depth (scheduler -> roles)
 
-template <int NSUB, int STAGES, int NACC, int SPS, int MINB = 1>
-__global__ void __launch_bounds__(kThreadsTC, MINB)
+template <int NSUB, int STAGES, int NACC, int SPS, int NPROD, int MINB = 1>
+__global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
     bgcoo_tc_kernel(const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmAV, TcArgs a) {
   using L = TcSmem<NSUB, STAGES, SPS>;
+  using R = TcRoles<NSUB, NPROD>;
+  static_assert(32 % SPS == 0, "a stage batch never straddles a 32-slot AK chunk");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -145,10 +167,12 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
   uint64_t* seg_empty = seg_full + kQN;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(seg_empty + kQN);
   int4* segq = reinterpret_cast<int4*>(tmem_base_slot + 4);  // {s, e, row, prev}
-  int* segq_tile = reinterpret_cast<int*>(segq + kQN);
+  int4* segq2 = segq + kQN;                                   // {tile, c0, c1, split}
+  int* epi_flag = reinterpret_cast<int*>(segq2 + kQN);        // split-row combine: last arriver
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) K4TR(0);
   constexpr uint32_t kAccCols = 16 * NSUB;  // one accumulator buffer
   constexpr uint32_t kTmemCols = NACC * kAccCols <= 32    ? 32
                                  : NACC * kAccCols <= 64  ? 64
@@ -156,70 +180,107 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
                                  : NACC * kAccCols <= 256 ? 256
                                                           : 512;
 
-  if (warp == 0) {
+  if (warp == R::kSched) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], 1);
+        mbar_init(&empty[s], NSUB);  // every issuer commits the stage
       }
       for (int b = 0; b < NACC; ++b) {
-        mbar_init(&acc_full[b], 1);
-        mbar_init(&acc_empty[b], 4);
+        mbar_init(&acc_full[b], NSUB);
+        mbar_init(&acc_empty[b], R::kEpi);
       }
       for (int q = 0; q < kQN; ++q) {
         mbar_init(&seg_full[q], 1);
-        mbar_init(&seg_empty[q], 6);  // producer, UMMA issuer, 4 epilogue warps
+        mbar_init(&seg_empty[q], NPROD + NSUB + R::kEpi);
       }
       fence_barrier_init();
-      tma_prefetch_desc(&tmB);
-      tma_prefetch_desc(&tmAV);
     }
-  } else if (warp == 1) {
+  } else if (warp == R::kIss0) {
     tmem_alloc(tmem_base_slot, kTmemCols);
     tmem_relinquish();
+  } else if (warp == R::kProd0 && lane == 0) {
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmAV);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  if (threadIdx.x == 0) K4TR(1);
 
-  // Segment queue consumers: entry q holds {s, e, row, prev} + n tile; s < 0 ends.
+  // Segment queue consumers: entry q holds {s, e, row, prev} + {n tile, c0,
+  // c1, split}; s < 0 ends.
+  int4 sg2;
   auto pop = [&](int j, int4& sg, int& tile) {
     const int q = j % kQN;
     mbar_wait(&seg_full[q], (j / kQN) & 1);
     sg = segq[q];
-    tile = segq_tile[q];
+    sg2 = segq2[q];
+    tile = sg2.x;
   };
   auto release = [&](int j) { mbar_arrive(&seg_empty[j % kQN]); };
 
-  if (warp == 6) {
+  if (warp == R::kSched) {
     // ---------------------------------------------------------- scheduler
-    // Discovers segments ahead of the pipeline so no role stalls on the
-    // dependent AM loads between segments.
-    SegIter it;
-    it.init(a);
-    Seg sg;
+    // Walks this CTA's range and queues its segments (row runs clipped to
+    // the range) ahead of the pipeline, so no role stalls on the dependent
+    // AM loads between segments.
+    const int64_t nc = gridDim.x;
+    const int64_t lo = range_lo(a.G, nc, blockIdx.x), hi = range_lo(a.G, nc, blockIdx.x + 1);
     int j = 0;
-    bool more = true;
-    while (more) {
-      more = it.next(a, sg);
+    auto push = [&](int4 v, int4 v2) {
       const int q = j % kQN;
       if (lane == 0) {
         mbar_wait(&seg_empty[q], ((j / kQN) & 1) ^ 1);
-        segq[q] = more ? make_int4(static_cast<int>(sg.s), static_cast<int>(sg.e), sg.row, sg.prev)
-                       : make_int4(-1, -1, 0, 0);
-        segq_tile[q] = more ? sg.ntile : 0;
+        segq[q] = v;
+        segq2[q] = v2;
         mbar_arrive(&seg_full[q]);
+        if (v.x >= 0) K4TR_FIRST(2); else K4TR(3);
       }
       __syncwarp();
       ++j;
+    };
+    // Order: the segment at lo, then the trailing segment when its row
+    // continues past hi, then the whole rows between. Both split rows of
+    // the range are thus finished (partials stored, combined by whichever
+    // CTA arrives last) early, behind the MMAs of the whole rows, instead of
+    // at the end of the kernel.
+    auto seg = [&](int tile, int64_t s, int64_t e, int row, int64_t rs, int64_t re) {
+      const int prev = rs == s ? (s > 0 ? __ldg(a.AM + s - 1) : -1) : row;
+      push(make_int4(static_cast<int>(s), static_cast<int>(e), row, prev),
+           make_int4(tile, owner_cta(a.G, nc, rs), owner_cta(a.G, nc, re - 1),
+                     rs < lo || re > hi));
+    };
+    for (int tile = 0; tile < a.ntiles; ++tile) {
+      const int row0 = __ldg(a.AM + lo);
+      const int64_t rs0 = run_start(a.AM, lo, row0), re0 = run_end(a.AM, lo + 1, a.G, row0);
+      const int64_t e0 = re0 < hi ? re0 : hi;
+      seg(tile, lo, e0, row0, rs0, re0);
+      int64_t mid_end = hi;
+      if (e0 < hi && hi < a.G) {
+        const int rowt = __ldg(a.AM + hi - 1);
+        if (__ldg(a.AM + hi) == rowt) {  // the last row of the range continues past hi
+          const int64_t ts = run_start(a.AM, hi - 1, rowt);
+          seg(tile, ts, hi, rowt, ts, run_end(a.AM, hi + 1, a.G, rowt));
+          mid_end = ts;
+        }
+      }
+      for (int64_t p = e0; p < mid_end;) {
+        const int row = __ldg(a.AM + p);
+        const int64_t re = run_end(a.AM, p + 1, mid_end, row);
+        seg(tile, p, re, row, p, re);
+        p = re;
+      }
     }
-  } else if (warp == 0) {
-    // ---------------------------------------------------------- TMA producer
+    push(make_int4(-1, -1, 0, 0), make_int4(0, 0, 0, 0));
+  } else if (warp >= R::kProd0 && warp < R::kProd0 + NPROD) {
+    // ---------------------------------------------------------- TMA producers
+    // Producer p issues the stage batches bc with bc % NPROD == p.
+    const int p = warp - R::kProd0;
     const uint64_t keep = l2_evict_last();    // dense operand: re-read by many blocks
     const uint64_t stream = l2_evict_first();  // format: read once
-    int stage = 0;
-    uint32_t phase = 0;
+    int64_t bc = 0;                            // stage batches walked (all producers)
     for (int j = 0;; ++j) {
       int4 sg;
       int tile;
@@ -243,27 +304,28 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
       for (int64_t i0 = s0; i0 < s1; i0 += 32) {
         const int k_next = load_k(i0 + 32);  // prefetch the next 32 member coords
         const int cnt = static_cast<int>(s1 - i0 < 32 ? s1 - i0 : 32);
-        for (int t = 0; t < cnt; t += SPS) {
+        for (int t = 0; t < cnt; t += SPS, ++bc) {
+          if (static_cast<int>(bc % NPROD) != p) continue;
           const int nb = cnt - t < SPS ? cnt - t : SPS;
           int kk[SPS];
 #pragma unroll
           for (int b = 0; b < SPS; ++b) kk[b] = __shfl_sync(0xffffffffu, k, (t + b) & 31);
+          const int stage = static_cast<int>(bc % STAGES);
+          const uint32_t phase = static_cast<uint32_t>((bc / STAGES) & 1);
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* st = tiles + stage * L::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], nb * (L::kBBytes + kAvBytes));
+            mbar_arrive_expect_tx(&full[stage], nb * L::kBBytes + SPS * kAvBytes);
 #pragma unroll
             for (int b = 0; b < SPS; ++b) {
               if (b >= nb) break;
               // one 3-D box {64 n, 16 rows, 2*NSUB atoms} lands as [atom][row][64]
               tma_load_3d(st + b * L::kBBytes, &tmB, &full[stage], 0, kk[b] * 16, n0 / 64, keep);
-              tma_load_2d(st + SPS * L::kBBytes + b * kAvBytes, &tmAV, &full[stage], 0,
-                          static_cast<int32_t>((i0 + t + b) * 16), stream);
             }
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+            // the SPS AV blocks in one box (rows past the format are zero-filled)
+            tma_load_2d(st + SPS * L::kBBytes, &tmAV, &full[stage], 0,
+                        static_cast<int32_t>((i0 + t) * 16), stream);
+            if (p == 0) { K4TR_FIRST(4); K4TR(5); }
           }
         }
         k = k_next;
@@ -271,27 +333,30 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
       __syncwarp();
       if (lane == 0) release(j);
     }
-  } else if (warp == 1) {
-    // ---------------------------------------------------------- UMMA issuer
+  } else if (warp >= R::kIss0) {
+    // ---------------------------------------------------------- UMMA issuers
+    // Issuer `sub` owns n subtile sub of every block: D columns sub*16.
+    const int sub = warp - R::kIss0;
     constexpr uint32_t idesc = idesc_bf16_f32(128, 16, /*A MN-major*/ true, /*B K-major*/ false);
-    int stage = 0;
-    uint32_t phase = 0;
+    int64_t bc = 0;  // stage batches consumed (lane 0)
     for (int j = 0;; ++j) {
       int4 sg;
       int tile;
       pop(j, sg, tile);
       if (sg.x < 0) break;
       const int buf = j % NACC;
-      mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
-      tc_fence_after();
-      const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
-      // same (32-slot chunk, SPS batch) partition as the producer
-      for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
-        const int cnt = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
-        for (int t = 0; t < cnt; t += SPS) {
-          const int nb = cnt - t < SPS ? cnt - t : SPS;
-          if (lane == 0) {
-            mbar_wait(&full[stage], phase);
+      if (lane == 0) {
+        mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + buf * kAccCols + sub * 16;
+        const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
+        // same (32-slot chunk, SPS batch) partition as the producers
+        for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
+          const int cnt = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
+          for (int t = 0; t < cnt; t += SPS, ++bc) {
+            const int nb = cnt - t < SPS ? cnt - t : SPS;
+            const int stage = static_cast<int>(bc % STAGES);
+            mbar_wait(&full[stage], static_cast<uint32_t>((bc / STAGES) & 1));
             tc_fence_after();
             const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
 #pragma unroll
@@ -299,21 +364,14 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
               if (b >= nb) break;
               const uint64_t bdesc =
                   smem_desc(st + SPS * L::kBBytes + b * kAvBytes, 16, 256, kLayoutSW32);
-#pragma unroll
-              for (int sub = 0; sub < NSUB; ++sub) {
-                // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
-                const uint64_t adesc =
-                    smem_desc(st + b * L::kBBytes + sub * kSubBytes, 2048, 1024, kLayoutSW128);
-                umma_f16(tmem_base + buf * kAccCols + sub * 16, adesc, bdesc, idesc,
-                         (i0 + t + b) > 0 ? 1u : 0u);
-              }
+              // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
+              const uint64_t adesc =
+                  smem_desc(st + b * L::kBBytes + sub * kSubBytes, 2048, 1024, kLayoutSW128);
+              umma_f16(d, adesc, bdesc, idesc, (i0 + t + b) > 0 ? 1u : 0u);
             }
             umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
             if (i0 + t + nb == nslots) umma_commit(&acc_full[buf]);
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+            if (sub == 0) { K4TR_FIRST(6); K4TR(7); K4TR_SET(12, bc + 1); }
           }
         }
       }
@@ -333,31 +391,89 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
       const int row = sg.z;
       const int n0 = tile * 128 * NSUB;
       const bool row_ok = row >= 0 && static_cast<int64_t>(row) < a.MB;
+      const bool split = sg2.w && row_ok;
+      const int c0 = sg2.y, c1 = sg2.z;
+      // a split row's partial: slot 1 for the row's first CTA (its last row), else 0
+      float* mypart = a.part + (static_cast<int64_t>(blockIdx.x) * 2 +
+                                (static_cast<int>(blockIdx.x) == c0 ? 1 : 0)) * 16 * a.N;
       mbar_wait_backoff(&acc_full[buf], (j / NACC) & 1, a.epi_sleep_ns);
       tc_fence_after();
-      uint32_t r[NSUB][16];
-#pragma unroll
+#pragma unroll 1
       for (int sub = 0; sub < NSUB; ++sub) {
+        uint32_t r[16];
         tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                buf * kAccCols + sub * 16,
-                           r[sub]);
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM buffer free for segment j+NACC
-      if (row_ok) {
+                           r);
+        tmem_ld_wait();
+        if (sub == NSUB - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM buffer free for segment j+NACC
+        }
+        const int64_t col = n0 + sub * 128 + nloc;
+        if (split) {
 #pragma unroll
-        for (int sub = 0; sub < NSUB; ++sub) {
-          float* c = a.C + static_cast<int64_t>(row) * 16 * a.N + n0 + sub * 128 + nloc;
+          for (int bm = 0; bm < 16; ++bm) __stcg(mypart + bm * a.N + col, __uint_as_float(r[bm]));
+        } else if (row_ok) {
+          float* c = a.C + static_cast<int64_t>(row) * 16 * a.N + col;
 #pragma unroll
           for (int bm = 0; bm < 16; ++bm) {
-            float v = __uint_as_float(r[sub][bm]);
+            float v = __uint_as_float(r[bm]);
             if (a.accumulate) v += c[static_cast<int64_t>(bm) * a.N];
-            c[static_cast<int64_t>(bm) * a.N] = v;
+            __stcs(c + static_cast<int64_t>(bm) * a.N, v);
           }
         }
-      } else if (a.check && warp == 2 && lane == 0 && tile == 0) {
+      }
+      if (split) {
+        // arrive on the row's counter; the last of the c1-c0+1 CTAs sums the
+        // partials in CTA order: C = (C or 0) + P[c0] + ... + P[c1]
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 0 && lane == 0) {
+          unsigned* ctr = a.rowctr + static_cast<int64_t>(c0) * a.ntiles + tile;
+          const unsigned old = atomicAdd(ctr, 1u);
+          const int last = old == static_cast<unsigned>(c1 - c0);
+          if (last) *ctr = 0;  // reset for the next launch
+          *epi_flag = last;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (*epi_flag) {
+          __threadfence();
+#pragma unroll 1
+          for (int sub = 0; sub < NSUB; ++sub) {
+            const int64_t col = n0 + sub * 128 + nloc;
+            float* c = a.C + static_cast<int64_t>(row) * 16 * a.N + col;
+            float v[16];
+#pragma unroll
+            for (int bm = 0; bm < 16; ++bm) v[bm] = a.accumulate ? c[bm * a.N] : 0.f;
+            auto part_at = [&](int cc) {
+              return a.part + (static_cast<int64_t>(cc) * 2 + (cc == c0 ? 1 : 0)) * 16 * a.N + col;
+            };
+            int cc = c0;
+            for (; cc + 1 <= c1; cc += 2) {  // two partials' loads in flight, adds in CTA order
+              const float* p0 = part_at(cc);
+              const float* p1 = part_at(cc + 1);
+              float x0[16], x1[16];
+#pragma unroll
+              for (int bm = 0; bm < 16; ++bm) x0[bm] = __ldcg(p0 + bm * a.N);
+#pragma unroll
+              for (int bm = 0; bm < 16; ++bm) x1[bm] = __ldcg(p1 + bm * a.N);
+#pragma unroll
+              for (int bm = 0; bm < 16; ++bm) v[bm] = (v[bm] + x0[bm]) + x1[bm];
+            }
+            if (cc == c1) {
+              const float* p0 = part_at(cc);
+#pragma unroll
+              for (int bm = 0; bm < 16; ++bm) v[bm] += __ldcg(p0 + bm * a.N);
+            }
+#pragma unroll
+            for (int bm = 0; bm < 16; ++bm) __stcs(c + bm * a.N, v[bm]);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // epi_flag reused by the next split row
+      }
+      if (warp == 0 && lane == 0) { K4TR_FIRST(8); K4TR(9); K4TR_SET(11, j + 1); }
+      if (!row_ok && a.check && warp == 0 && lane == 0 && tile == 0) {
         report_index_error(a.err, 1, sg.x, row);
       }
       if (!a.accumulate) {
@@ -383,10 +499,11 @@ __global__ void __launch_bounds__(kThreadsTC, MINB)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == R::kIss0) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
+  if (threadIdx.x == 0) K4TR(10);
 }
 
 // ----------------------------------------------------- CUDA-core fallback
@@ -440,10 +557,11 @@ __global__ void bgcoo_simt_kernel(const int32_t* AM, const int32_t* AK,
 }
 
 // ------------------------------------------------------------ host side
-template <int NSUB, int STAGES, int NACC, int SPS, int MINB = 1>
+template <int NSUB, int STAGES, int NACC, int SPS, int NPROD, int MINB = 1>
 void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaStream_t s) {
   using L = TcSmem<NSUB, STAGES, SPS>;
-  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC, SPS, MINB>;
+  using R = TcRoles<NSUB, NPROD>;
+  auto kern = bgcoo_tc_kernel<NSUB, STAGES, NACC, SPS, NPROD, MINB>;
   set_max_dynamic_smem(reinterpret_cast<const void*>(kern), L::kTotal,
                        "cudaFuncSetAttribute(bgcoo_tc_kernel)");
   // resident CTAs per SM (registers, smem and TMEM columns): a property of the
@@ -452,19 +570,22 @@ void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaSt
   if (!per_sm) {
     cudaFuncAttributes fa;
     IXB_CUDA_CHECK(cudaFuncGetAttributes(&fa, kern));
-    const int by_regs = 65536 / (((fa.numRegs * 32 + 255) / 256) * 256 * (kThreadsTC / 32));
-    per_sm = static_cast<int>((220u * 1024u) / L::kTotal);
-    if (per_sm > by_regs) per_sm = by_regs;
+    const int by_regs = 65536 / (((fa.numRegs * 32 + 255) / 256) * 256 * R::kWarps);
+    int n = static_cast<int>((220u * 1024u) / L::kTotal);
+    if (n > by_regs) n = by_regs;
+    if (n > 2048 / R::kThreads) n = 2048 / R::kThreads;
     constexpr int kCols = NACC * 16 * NSUB <= 32 ? 32 : NACC * 16 * NSUB <= 64 ? 64
                           : NACC * 16 * NSUB <= 128 ? 128 : NACC * 16 * NSUB <= 256 ? 256 : 512;
-    if (per_sm > 512 / kCols) per_sm = 512 / kCols;  // a CTA must not wait in tcgen05.alloc
-    if (per_sm < 1) per_sm = 1;
+    if (n > 512 / kCols) n = 512 / kCols;  // a CTA must not wait in tcgen05.alloc
+    per_sm = n < 1 ? 1 : n;
   }
   a.ntiles = static_cast<int>(a.N / (128 * NSUB));
-  const int64_t items = static_cast<int64_t>(a.nchunks) * a.ntiles;
-  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // persistent CTAs
-  if (grid > items) grid = items;
-  kern<<<static_cast<unsigned>(grid), kThreadsTC, L::kTotal, s>>>(tmB, tmAV, a);
+  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // every CTA resident
+  if (grid > a.G) grid = a.G;
+  a.rowctr = work_counters(s, static_cast<size_t>(grid) * a.ntiles);
+  Scratch<float> part(static_cast<size_t>(grid) * 2 * 16 * a.N, s);
+  a.part = part.p;
+  kern<<<static_cast<unsigned>(grid), R::kThreads, L::kTotal, s>>>(tmB, tmAV, a);
   IXB_LAUNCH_CHECK("bgcoo_tc_kernel");
 }
 
@@ -519,26 +640,27 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
     a.KB = KB;
     a.N = N;
     a.MB = MB;
-    int64_t ch = MB > 0 ? G / MB : 1;
-    a.chunk = static_cast<int>(ch < 1 ? 1 : (ch > 32 ? 32 : ch));
     a.accumulate = accumulate;
     a.check = check2;
     a.err = err;
-    a.nchunks = static_cast<int>(ceil_div(G, a.chunk));
-    const int nsub = N % 256 == 0 ? 2 : 1;
+#ifndef IXB_K4_NSUB
+#define IXB_K4_NSUB 4
+#endif
+    const int nsub = N % (128 * IXB_K4_NSUB) == 0 ? IXB_K4_NSUB : N % 256 == 0 ? 2 : 1;
     // B viewed as {64 n, rows, N/64 atoms}: one TMA box = the whole n tile of
     // 16 rows, landing as [atom][row][64] (the MN-major SW128 canonical layout)
     const CUtensorMap tmB = make_tmap_3d(B, 64, KB * 16, N / 64, N * 2, 128, 64, 16, 2 * nsub,
                                         CU_TENSOR_MAP_SWIZZLE_128B);
-    const CUtensorMap tmAV = make_tmap_2d(AV, 16, G * g * 16, 32, 16, 16,
+    const CUtensorMap tmAV = make_tmap_2d(AV, 16, G * g * 16, 32, 16, 16 * kSps,
                                          CU_TENSOR_MAP_SWIZZLE_32B);
     a.epi_sleep_ns = 256;  // back-off of the idle epilogue warps' barrier polls
     // 2 slots per stage, 4 stages: ~68 KB -> 3 CTAs (3 independent issue
     // streams) per SM; measured against 1, 4, 8, 12 slots per stage and
     // 1-5 CTAs/SM on cfg2 (profiles/k4_diag_r1.md), and against a panel
     // kernel with B-tile reuse across block rows (profiles/k4_diag_r2.md)
-    if (nsub == 1) launch_tc<1, 8, 4, 2>(tmB, tmAV, a, s);
-    else launch_tc<2, 4, 4, 2>(tmB, tmAV, a, s);
+    if (nsub == 1) launch_tc<1, 8, 4, kSps, 1>(tmB, tmAV, a, s);
+    else if (nsub == 2) launch_tc<2, 4, 4, kSps, 2>(tmB, tmAV, a, s);
+    else launch_tc<IXB_K4_NSUB, IXB_K4_STAGES, 2, kSps, IXB_K4_NPROD, IXB_K4_MINB>(tmB, tmAV, a, s);
   } else {
     const int threads = 256;
     bgcoo_simt_kernel<<<static_cast<unsigned>(G), threads, 0, s>>>(
@@ -553,6 +675,16 @@ void spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV, in
 }
 
 }  // namespace ixb
+
+#ifdef IXB_K4_TRACE
+extern "C" int ixb_debug_k4_trace(long long* host, int clear) {
+  if (clear) {
+    static long long zero[4096 * 16];
+    return cudaMemcpyToSymbol(ixb::g_k4_trace, zero, sizeof zero);
+  }
+  return cudaMemcpyFromSymbol(host, ixb::g_k4_trace, sizeof(long long) * 4096 * 16);
+}
+#endif
 
 extern "C" int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV,
                                       int64_t G, int64_t g, int64_t bm, int64_t bk, const void* B,

@@ -21,16 +21,17 @@ def timed(torch, fn, reps, flush):
         fn()
     g.replay()
     torch.cuda.synchronize()
-    out = []
-    for _ in range(reps):
+    evs = []
+    for _ in range(reps):  # queued back to back (as bench.py): no host launch gap inside
         flush.zero_()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
         g.replay()
         b.record()
-        b.synchronize()
-        out.append(a.elapsed_time(b) * 1e3)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    out = [a.elapsed_time(b) * 1e3 for a, b in evs]
     out.sort()
     return out[len(out) // 2], out[0]
 
