@@ -75,6 +75,15 @@ __device__ __forceinline__ float ldg_f_stream(const float* p, uint64_t pol) {
   return v;
 }
 
+// 16-byte read-only load that skips L1 allocation (gathered rows).
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 }  // namespace ixb

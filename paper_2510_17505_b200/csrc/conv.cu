@@ -253,7 +253,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // - deeper rings at this structure (s4d2 0.645 ms, s5d2 1.13 ms: fewer CTAs
 //   per SM);
 // - TMA tile::gather4 (1.0-3.2 ms; ~43 cycles per 512 B box per SM;
-//   tools/gather4_probe.cu pins its semantics).
+//   tools/gather4_probe.cu pins its semantics);
+// - A in tensor memory (round 2): each thread gathers its row into
+//   registers 2 offsets ahead and tcgen05.st's it into a TMEM A slot, the
+//   MMA reads A from TMEM (umma_f16_ts) and only Weight from shared memory,
+//   epilogue staged through smem for 512 B warp stores: correct (every conv
+//   test) but 0.539 ms against 0.477 — register-staged gathers cap the
+//   bytes in flight per SM below what the cp.async ring keeps.
 constexpr int kOffPad = 28;  // Y row stride (ints): 27 offsets padded to 16 B
 
 struct UnitArgs {

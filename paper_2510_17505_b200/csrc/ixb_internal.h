@@ -47,6 +47,11 @@ ErrorRecord* device_error_record();
 // stream, so concurrent launches never share one): zero on entry, and every
 // kernel using them leaves them zero again.
 unsigned* work_counters(cudaStream_t stream, size_t n);
+// A persistent device buffer of at least `bytes` owned by `stream` (grown on
+// demand, never shrunk): kernel scratch that must not add allocation nodes
+// to a captured CUDA graph. Contents are undefined on entry. Returns null
+// when the buffer would have to grow while `stream` is being captured.
+void* stream_buffer(cudaStream_t stream, size_t bytes);
 // Resets the record on `stream` before a checked launch.
 void reset_error_record(cudaStream_t stream);
 // Syncs `stream`, reads the record; on an offender throws IXB_INDEX_RANGE with

@@ -23,6 +23,7 @@ struct DeviceCtx {
   // stream (kernels on different streams must not share a counter)
   unsigned* counters = nullptr;
   std::vector<cudaStream_t> counter_streams;
+  std::vector<std::pair<void*, size_t>> stream_bufs;  // per counter slot: persistent scratch
 };
 constexpr int kCounterSlots = 64;
 constexpr size_t kCountersPerSlot = 16384;
@@ -95,6 +96,29 @@ unsigned* work_counters(cudaStream_t stream, size_t n) {
     c.counter_streams.push_back(stream);
   }
   return c.counters + kCountersPerSlot * i;
+}
+
+void* stream_buffer(cudaStream_t stream, size_t bytes) {
+  work_counters(stream, 0);  // assigns the stream its slot
+  DeviceCtx& c = ctx();
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t i = 0;
+  while (c.counter_streams[i] != stream) ++i;
+  if (c.stream_bufs.size() <= i) c.stream_bufs.resize(i + 1, {nullptr, 0});
+  auto& b = c.stream_bufs[i];
+  if (b.second < bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;  // caller allocates in the graph
+    if (b.first) {
+      // a kernel still reading the old buffer must finish before it goes
+      cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+      cuda_check(cudaFree(b.first), "cudaFree(stream buffer)");
+    }
+    cuda_check(cudaMalloc(&b.first, bytes), "cudaMalloc(stream buffer)");
+    b.second = bytes;
+  }
+  return b.first;
 }
 
 void reset_error_record(cudaStream_t stream) {

@@ -583,8 +583,13 @@ void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaSt
   int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // every CTA resident
   if (grid > a.G) grid = a.G;
   a.rowctr = work_counters(s, static_cast<size_t>(grid) * a.ntiles);
-  Scratch<float> part(static_cast<size_t>(grid) * 2 * 16 * a.N, s);
-  a.part = part.p;
+  const size_t part_n = static_cast<size_t>(grid) * 2 * 16 * a.N;
+  a.part = static_cast<float*>(stream_buffer(s, part_n * sizeof(float)));
+  Scratch<float> part_graph;  // first use inside a graph capture
+  if (!a.part) {
+    part_graph = Scratch<float>(part_n, s);
+    a.part = part_graph.p;
+  }
   kern<<<static_cast<unsigned>(grid), R::kThreads, L::kTotal, s>>>(tmB, tmAV, a);
   IXB_LAUNCH_CHECK("bgcoo_tc_kernel");
 }

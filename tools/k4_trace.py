@@ -40,6 +40,8 @@ def main():
     f.argtypes = [ctypes.c_void_p, ctypes.c_int]
     f(None, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flush.zero_()  # keeps the GPU busy while the host enqueues: no launch gap in the events
     e0.record()
     run()
     e1.record()
