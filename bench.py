@@ -241,25 +241,25 @@ class GroupCooWorkload:
     def roofline_bound(self):
         return "hbm"
 
-    # --sharded (strong scaling): row-group shards of ONE matrix
-    def shard(self, torch, P, dev, rank, ws):
+    # strong scaling through the native sharded C-ABI:
+    # row-group shards of ONE replicated matrix, each rank writing its rows
+    # of the full C, NCCL in-place broadcasts overlapping the next chunk
+    def shard(self, torch, P, dev, rank, ws, comm=None, nchunks=4):
         from paper_2510_17505_b200 import distributed as D
-        sh = D.shard_plan(self.fmt.AM.cpu().numpy(), self.M, ws)
-        self.sh = sh[rank]
-        s = self.sh
-        self.sg = D.SlabGather(sh, rank, (self.N,), torch.float32, dev)
-        loc = [self.fmt.AM[s.g0:s.g1], self.fmt.AK[s.g0:s.g1], self.fmt.AV[s.g0:s.g1], self.B]
-        self.sh_h_in = [x.cpu().pin_memory() for x in loc]
-        self.sh_d_in = [x.clone() for x in loc]
-        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
-        return {"rows_owned": s.r1 - s.r0, "groups_owned": s.g1 - s.g0}
+        self.sh_plan = D.ShardPlan(self.fmt.AM, self.M, ws, rank, nchunks)
+        self.sh_comm = comm
+        self.C_full = torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
+        g0, _, r0, _ = self.sh_plan.chunk(rank, 0)
+        _, g1, _, r1 = self.sh_plan.chunk(rank, nchunks - 1)
+        return {"rows_owned": r1 - r0, "groups_owned": g1 - g0, "chunks": nchunks}
 
-    def sharded_step(self, P):
+    def replicated(self):
+        return [self.fmt.AM, self.fmt.AK, self.fmt.AV, self.B]
+
+    def sharded_step(self, P, flags=0):
         from paper_2510_17505_b200 import distributed as D
-        AM, AK, AV, B = self.sh_d_in
-        self.sg.local.zero_()
-        D.spmm_groupcoo_into(AM, AK, AV, self.g, B, self.sh, self.sg.local, flags=1 | 2)
-        return self.sg()
+        return D.spmm_groupcoo_sharded(self.sh_plan, self.fmt, self.B, self.C_full,
+                                       self.sh_comm, flags=1 | 2 | flags)
 
     # reference CPU path on a bounded slab of the same matrix
     def cpu_sample(self, ref, budget_rows=None):
@@ -320,9 +320,9 @@ class BlockGroupCooWorkload:
         self.dram_bytes = slots * b * b * 2 + slots * 4 + self.G * 4 + self.K * self.N * 2 + \
             self.M * self.N * 4
         self.gather_bytes = slots * b * self.N * 2
-        # L2 -> SM as the kernel moves it: a 16-row B tile per slot and 256-wide n
-        # tile, AV block + AK per slot and n tile, AM, C written once
-        ntile = max(self.N // 256, 1)
+        # L2 -> SM as the kernel moves it: a 16-row B tile per slot and n tile
+        # (512 wide when N % 512 == 0), AV block + AK per slot and n tile, AM, C once
+        ntile = self.N // 512 if self.N % 512 == 0 else max(self.N // 256, 1)
         self.l2_bytes = self.gather_bytes + slots * (b * b * 2 + 4) * ntile + self.G * 4 + \
             self.M * self.N * 4
         self.tc_flops = 2.0 * self.nblk * b * b * self.N
@@ -355,24 +355,22 @@ class BlockGroupCooWorkload:
     def roofline_bound(self):
         return "tensor"
 
-    def shard(self, torch, P, dev, rank, ws):
+    def shard(self, torch, P, dev, rank, ws, comm=None, nchunks=4):
         from paper_2510_17505_b200 import distributed as D
-        sh = D.shard_plan(self.fmt.AM.cpu().numpy(), self.M // self.b, ws)
-        self.sh = sh[rank]
-        s = self.sh
-        self.sg = D.SlabGather(sh, rank, (self.b, self.N), torch.float32, dev)
-        loc = [self.fmt.AM[s.g0:s.g1], self.fmt.AK[s.g0:s.g1], self.fmt.AV[s.g0:s.g1], self.B]
-        self.sh_h_in = [x.cpu().pin_memory() for x in loc]
-        self.sh_d_in = [x.clone() for x in loc]
-        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
-        return {"block_rows_owned": s.r1 - s.r0, "groups_owned": s.g1 - s.g0}
+        self.sh_plan = D.ShardPlan(self.fmt.AM, self.M // self.b, ws, rank, nchunks)
+        self.sh_comm = comm
+        self.C_full = torch.empty_like(self.C)
+        g0, _, r0, _ = self.sh_plan.chunk(rank, 0)
+        _, g1, _, r1 = self.sh_plan.chunk(rank, nchunks - 1)
+        return {"block_rows_owned": r1 - r0, "groups_owned": g1 - g0, "chunks": nchunks}
 
-    def sharded_step(self, P):
+    def replicated(self):
+        return [self.fmt.AM, self.fmt.AK, self.fmt.AV, self.B]
+
+    def sharded_step(self, P, flags=0):
         from paper_2510_17505_b200 import distributed as D
-        AM, AK, AV, B = self.sh_d_in
-        self.sg.local.zero_()
-        D.spmm_blockgroupcoo_into(AM, AK, AV, B, self.sh, self.sg.local, flags=1 | 2)
-        return self.sg()
+        return D.spmm_blockgroupcoo_sharded(self.sh_plan, self.fmt, self.B, self.C_full,
+                                            self.sh_comm, flags=1 | 2 | flags)
 
     def cpu_sample(self, ref, budget_rows=None):
         import numpy as np
@@ -461,23 +459,20 @@ class TensorProductWorkload:
     def units_total(self):
         return self.batch
 
-    def shard(self, torch, P, dev, rank, ws):
+    def shard(self, torch, P, dev, rank, ws, comm=None, nchunks=1):
+        # edges are independent: each rank evaluates its edge block into its
+        # own Z rows; Z stays sharded (no collective)
         from paper_2510_17505_b200 import distributed as D
-        sh = D.edge_blocks(self.batch, ws)
-        self.sh = sh[rank]
+        self.sh = D.edge_blocks(self.batch, ws)[rank]
         s = self.sh
-        self.sg = D.SlabGather(sh, rank, (16, 64), torch.float32, dev)
-        loc = [self.X[s.r0:s.r1], self.Y[s.r0:s.r1]]
-        self.sh_h_in = [x.cpu().pin_memory() for x in loc]
-        self.sh_d_in = [x.clone() for x in loc]
-        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
-        return {"edges_owned": s.r1 - s.r0}
+        self.sh_X, self.sh_Y = self.X[s.r0:s.r1], self.Y[s.r0:s.r1]
+        self.sh_Z = torch.empty((s.r1 - s.r0, 16, 64), dtype=torch.float32, device=dev)
+        return {"edges_owned": s.r1 - s.r0, "collective": "none (Z stays sharded)"}
 
-    def sharded_step(self, P):
-        if self.sh.r1 > self.sh.r0:
-            self.plan.run(self.sh_d_in[0], self.sh_d_in[1], self.W, self.sg.local,
-                          accumulate=False)
-        return self.sg()
+    def sharded_step(self, P, flags=0):
+        if self.sh.r1 > self.sh.r0 and not flags & 16:
+            self.plan.run(self.sh_X, self.sh_Y, self.W, self.sh_Z, accumulate=False)
+        return self.sh_Z
 
     def cpu_sample(self, ref, budget_rows=None):
         import numpy as np
@@ -578,29 +573,31 @@ class SparseConvWorkload:
     def units_total(self):
         return getattr(self, "pairs_total", 9.12 * self.voxels)
 
-    def shard(self, torch, P, dev, rank, ws):
+    def shard(self, torch, P, dev, rank, ws, comm=None, nchunks=4):
         # point blocks: the map keeps only pairs whose output voxel is in the block
         import time as _t
         from paper_2510_17505_b200 import distributed as D
         n = self.In.shape[0]
         sh = D.point_blocks(n, ws)
         self.sh = sh[rank]
+        self.sh_ws, self.sh_rank, self.sh_chunks, self.sh_comm = ws, rank, nchunks, comm
         torch.cuda.synchronize()
         t0 = _t.perf_counter()
-        self.sh_plan = D.conv_shard_plan(*self.map, n, self.sh, self.g)
+        self.sh_plan = (D.conv_shard_plan(*self.map, n, self.sh, self.g)
+                        if self.sh.r1 > self.sh.r0 else None)
         torch.cuda.synchronize()
-        self.sg = D.SlabGather(sh, rank, (64,), torch.float32, dev)
-        self.sh_h_in = [self.In.cpu().pin_memory()]  # In is replicated
-        self.sh_d_in = [self.In.clone()]
-        self.sh_h_out = torch.empty(self.sg.out.shape, dtype=torch.float32).pin_memory()
-        return {"voxels_owned": self.sh.r1 - self.sh.r0,
-                "pairs_owned": int(self.sh_plan.keep_map.mask.sum().item()),
-                "shard_plan_ms": (_t.perf_counter() - t0) * 1e3}
+        self.Out_full = torch.empty_like(self.Out)
+        pairs = int(self.sh_plan.keep_map.mask.sum().item()) if self.sh_plan else 0
+        return {"voxels_owned": self.sh.r1 - self.sh.r0, "pairs_owned": pairs,
+                "chunks": nchunks, "shard_plan_ms": (_t.perf_counter() - t0) * 1e3}
 
-    def sharded_step(self, P):
-        if self.sh.r1 > self.sh.r0:
-            self.sh_plan.run(self.sh_d_in[0], self.Wt, self.sg.local, accumulate=False)
-        return self.sg()
+    def replicated(self):
+        return [self.In, self.Wt]
+
+    def sharded_step(self, P, flags=0):
+        from paper_2510_17505_b200 import distributed as D
+        return D.conv_sharded(self.sh_plan, self.In, self.Wt, self.Out_full, self.sh_ws,
+                              self.sh_rank, self.sh_chunks, self.sh_comm, flags=flags)
 
     def cpu_sample(self, ref, budget_rows=None):
         import numpy as np
@@ -909,23 +906,26 @@ def run_b200(args, wl):
             dist.init_process_group(backend)
     P.lib()
     if args.sharded:
-        # strong scaling: every rank holds the SAME instance,
-        # evaluates its row / point-block / edge shard into its output slab,
-        # and the slabs are all-gathered over NCCL inside the timed step.
+        # strong scaling: every rank holds the SAME instance
+        # and runs the native sharded C-ABI path (its rows of the full
+        # output, NCCL in-place broadcasts overlapping the next chunk)
+        from paper_2510_17505_b200 import distributed as D
         wl.setup(torch, P, S, dev, wl.seed)
-        shard_info = wl.shard(torch, P, dev, rank, ws)
+        comm = D.Comm(ws, rank) if ws > 1 else None
+        shard_info = wl.shard(torch, P, dev, rank, ws, comm)
 
         def step():
             wl.sharded_step(P)
 
+        out_t = wl.sharded_step(P)
+        h_out = torch.empty(out_t.shape, dtype=out_t.dtype).pin_memory()
+
         def e2e_step():
-            for d, h in zip(wl.sh_d_in, wl.sh_h_in):
-                d.copy_(h, non_blocking=True)
-            wl.sh_h_out.copy_(wl.sharded_step(P), non_blocking=True)
+            # inputs are replicated once (outside the step); the result read back
+            h_out.copy_(wl.sharded_step(P), non_blocking=True)
 
         def e2e_bytes():
-            return sum(x.numel() * x.element_size() for x in wl.sh_h_in), \
-                wl.sh_h_out.numel() * wl.sh_h_out.element_size()
+            return 0, h_out.numel() * h_out.element_size()
         wl.e2e_bytes = e2e_bytes
     else:
         # weak scaling: every rank evaluates its own independent instance of the
@@ -942,7 +942,7 @@ def run_b200(args, wl):
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     m = measure(torch, P, step, e2e_step, args.steps, args.warmup, max(3, min(args.steps, 20)),
-                flush, stream, graph=not args.sharded and not args.no_graph, ws=ws, dist=dist)
+                flush, stream, graph=not args.no_graph, ws=ws, dist=dist)
     rec = workload_record(wl, m, torch, dev, jobs=jobs,
                           kern_scale=ws if args.sharded else 1)
     line = {"metric": rec["metric"], "value": rec["value"], "unit": rec["unit"], "n_gpus": ws,
@@ -952,9 +952,9 @@ def run_b200(args, wl):
             "dtype": rec["dtype"], "data": "synthetic (reference synth streams, seed 1 + rank)",
             "config": dict(rec["config"], l2="flushed between steps (256 MiB memset outside "
                                              "the timed events)",
-                           parallelism=(f"sharded x{ws} + {backend if ws > 1 else 'no'} "
-                                        "all-gather of output slabs"
-                                        if args.sharded else f"weak x{ws}")),
+                           parallelism=(f"sharded x{ws} + {'NCCL in-place broadcast' if ws > 1 else 'no'} "
+                                        "all-gather of output rows"
+                                        if args.sharded else f"weak x{ws} (independent replicas)")),
             "roofline": rec["roofline"], "clocks": rec["clocks"],
             "gpu_launches": rec["gpu_launches"], "e2e": rec["e2e"]}
     if shard_info is not None:
@@ -966,6 +966,9 @@ def run_b200(args, wl):
     builders = {}
     if getattr(wl, "builder", None) and not args.sharded:
         builders[wl.name] = builder_record(wl)
+    if not args.sharded and not args.no_sharded_records:
+        line["sharded"] = sharded_records(torch, P, S, dev, rank, ws, dist, flush, stream,
+                                          args.sub_steps)
     if ws == 1 and not args.sharded and args.workloads != "none":
         # every other BASELINE config, measured the same way in this invocation
         names = SECONDARY if args.workloads == "all" else args.workloads.split(",")
@@ -1004,6 +1007,90 @@ def run_b200(args, wl):
         dist.destroy_process_group()
 
 
+SHARDED = ["cfg3_d0.30", "cfg5"]  # BASELINE configs[2] and [4]: "sharded 1/2/4/8 B200"
+
+
+def time_graph(torch, step, steps, flush, stream, ws, dist):
+    """Mean ms of `steps` CUDA-graph replays of `step` (L2 flushed outside the
+    events, as in measure), max over ranks."""
+    for _ in range(3):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, capture_error_mode="thread_local"):
+        step()
+    g.replay()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    evs = []
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / steps], dtype=torch.float64,
+                     device=flush.device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def sharded_records(torch, P, S, dev, rank, ws, dist, flush, stream, steps, names=SHARDED):
+    """Strong scaling of the BASELINE "sharded 1/2/4/8" configs through the
+    native sharded C-ABI: every rank holds the same instance
+    and evaluates its row-group / point-block shard in 4 chunks into its rows
+    of the full output; chunk c's NCCL in-place broadcasts overlap chunk
+    c+1's kernel. Reported per N: the whole step, the compute alone (no
+    collective) and the all-gather alone, each max over ranks; at N = 1 also
+    the unsharded evaluator for the sharding overhead."""
+    from paper_2510_17505_b200 import distributed as D
+    comm = D.Comm(ws, rank) if ws > 1 else None
+    out = {}
+    for name in names:
+        wl = WORKLOADS[name]()
+        try:
+            wl.setup(torch, P, S, dev, wl.seed)  # same seed: one instance, replicated
+            if comm is not None:  # rank 0's operands are the ones every rank uses
+                comm.broadcast(*wl.replicated())
+                torch.cuda.synchronize()
+            # chunks only buy overlap with the all-gather: one chunk without it
+            info = wl.shard(torch, P, dev, rank, ws, comm, nchunks=4 if ws > 1 else 1)
+            total = time_graph(torch, lambda: wl.sharded_step(P), steps, flush, stream, ws, dist)
+            compute = time_graph(torch, lambda: wl.sharded_step(P, D.SHARD_NO_COMM), steps,
+                                 flush, stream, ws, dist)
+            gather = (time_graph(torch, lambda: wl.sharded_step(P, D.SHARD_COMM_ONLY), steps,
+                                 flush, stream, ws, dist) if comm is not None else 0.0)
+            timelike = getattr(wl, "metric", METRIC) != METRIC
+            rec = {"metric": getattr(wl, "metric", METRIC), "unit": "ms" if timelike else "GFLOP/s",
+                   "value": total if timelike else wl.flops / (total * 1e-3) / 1e9,
+                   "ms_per_step": total, "compute_ms": compute, "gather_ms": gather,
+                   "overlap": (compute + gather - total) / gather if gather > 0 else None,
+                   "n_gpus": ws, "scaling": "strong", "steps": steps,
+                   "config": dict(wl.config(), **wl.info, shard_rank0=info if rank == 0 else None,
+                                  parallelism=f"sharded x{ws}" + (
+                                      " + NCCL in-place broadcast all-gather of output rows, "
+                                      "overlapped by chunk" if ws > 1 else " (no collective)"),
+                                  timing="CUDA-graph replay, max over ranks, L2 flushed")}
+            rec["useful_GFLOPs"] = wl.flops / (total * 1e-3) / 1e9
+            if ws == 1:
+                rec["unsharded_ms"] = time_graph(torch, lambda: wl.step(P), steps, flush, stream,
+                                                 ws, dist)
+                rec["sharding_overhead"] = total / rec["unsharded_ms"] - 1.0
+            out[name] = rec
+        except Exception as e:  # reported per workload, never fatal to the headline
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+        del wl
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    return out
+
+
 def cpu_line(wl, budget=None, steps=1):
     try:
         r = cpu_reference_time(wl, steps=steps, budget_rows=budget)
@@ -1028,6 +1115,8 @@ def main():
                          "'all', 'none' or a comma list")
     ap.add_argument("--sub-steps", type=int, default=10,
                     help="timed steps per secondary workload")
+    ap.add_argument("--no-sharded-records", action="store_true",
+                    help="skip the strong-scaling records of the sharded BASELINE configs")
     ap.add_argument("--sharded", action="store_true",
                     help="strong scaling: shard ONE instance across the ranks (row groups, "
                          "point blocks or edges) and all-gather the output inside the step")

@@ -60,7 +60,11 @@ enum ixb_flags {
    * stable permutation when it is not sorted. */
   IXB_GROUPS_SORTED = 2,
   /* Skip the in-kernel index range checks (inputs already validated). */
-  IXB_UNCHECKED = 4
+  IXB_UNCHECKED = 4,
+  /* Sharded evaluation only (instrumentation): evaluate this rank's chunks
+   * without the output all-gather, or run only the all-gather. */
+  IXB_SHARD_NO_COMM = 8,
+  IXB_SHARD_COMM_ONLY = 16
 };
 
 const char* ixb_last_error(void);
@@ -306,6 +310,58 @@ void ixb_mtx_free(ixb_mtx* mtx);
  * of `parts`. group_coord is a HOST array here. bounds: parts+1 entries.
  * ==================================================================== */
 int ixb_shard_groups(const int32_t* group_coord_host, int64_t G, int parts, int64_t* bounds);
+
+/* Sharded evaluation across the GPUs of one node, one process per GPU
+ * (north_star: "shard across one 8xB200 box by row-group / point-block
+ * partition with a replicated dense operand; NCCL over NVLink only for the
+ * final output all-gather"). The reference's single-process evaluators
+ * (execute_plan plan.hpp:82, interpret_kernel kernel.hpp:184) have no
+ * multi-process form; these entries are what a multi-GPU `execute_mode`
+ * would call on each rank.
+ *
+ * Communicator: NCCL (libnccl.so.2, loaded at first use). Rank 0 creates a
+ * 128-byte id, the caller distributes it (any side channel), every rank
+ * calls ixb_comm_init (world == 1 builds a 1-rank communicator; a null
+ * comm with world == 1 evaluates without any collective). */
+typedef struct ixb_comm ixb_comm;
+int ixb_comm_unique_id(void* id128);
+int ixb_comm_init(const void* id128, int world, int rank, ixb_comm** comm);
+void ixb_comm_free(ixb_comm* comm);
+/* In-place broadcast of `bytes` of a device buffer from `root` (the
+ * one-time replication of the format and dense operand). */
+int ixb_comm_broadcast(ixb_comm* comm, void* buf, int64_t bytes, int root, ixb_stream stream);
+
+/* Shard plan over a sorted group-coordinate array (DEVICE, the replicated
+ * format's AM): every rank's row-aligned group range (ixb_shard_groups),
+ * each cut into `nchunks` row-aligned chunks. One device->host copy. */
+typedef struct ixb_shard_plan ixb_shard_plan;
+int ixb_shard_plan_create(const int32_t* group_coord, int64_t G, int64_t rows, int world,
+                          int rank, int nchunks, ixb_stream stream, ixb_shard_plan** plan);
+int ixb_shard_plan_chunk(const ixb_shard_plan* plan, int rank, int chunk, int64_t* g0,
+                         int64_t* g1, int64_t* r0, int64_t* r1);
+void ixb_shard_plan_free(ixb_shard_plan* plan);
+
+/* `=` evaluation of the plan's rank into its rows of the FULL output C
+ * (GroupCOO C[M,N] fp32; BlockGroupCOO C[MB,16,N] fp32), then every rank's
+ * rows are broadcast in place so that, stream-ordered on return, every rank
+ * holds the whole C. Chunk c's broadcasts (one NCCL group, side stream)
+ * overlap chunk c+1's kernel. AK/AV/B are the full replicated operands. */
+int ixb_spmm_groupcoo_sharded(const ixb_shard_plan* plan, const int32_t* AK, const float* AV,
+                              int64_t g, const float* B, int64_t K, int64_t N, float* C,
+                              int flags, ixb_comm* comm, ixb_stream stream);
+int ixb_spmm_blockgroupcoo_sharded(const ixb_shard_plan* plan, const int32_t* AK, const void* AV,
+                                   int64_t g, int64_t bm, int64_t bk, const void* B, int64_t KB,
+                                   int64_t N, float* C, int flags, ixb_comm* comm,
+                                   ixb_stream stream);
+/* Point-block conv: `local` is this rank's plan over output voxels
+ * [n_total*rank/world, n_total*(rank+1)/world) (the kernel map filtered to
+ * that block, output index re-based; In replicated). Evaluates the block in
+ * `nchunks` tile-aligned chunks into its rows of the FULL Out [n_total,
+ * Cout] and all-gathers Out as above. */
+int ixb_conv_plan_run_sharded(ixb_conv_plan* local, const void* In, int64_t Cin,
+                              const void* Weight, int64_t Cout, float* Out, int64_t n_total,
+                              int world, int rank, int nchunks, int flags, ixb_comm* comm,
+                              ixb_stream stream);
 
 /* ======================================================================
  * Seeded synthetic inputs, host side (synth.hpp:13-29): std::mt19937_64 and

@@ -137,6 +137,24 @@ _SIGS = {
                                        C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ixb_synth_voxel_shells": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p]),
     "ixb_cg_table": (C.c_int, [C.c_int] + [C.c_void_p] * 7),
+    "ixb_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "ixb_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ixb_comm_free": (None, [C.c_void_p]),
+    "ixb_comm_broadcast": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "ixb_shard_plan_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                        C.c_int, C.c_void_p, C.c_void_p]),
+    "ixb_shard_plan_chunk": (C.c_int, [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 4),
+    "ixb_shard_plan_free": (None, [C.c_void_p]),
+    "ixb_spmm_groupcoo_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                            C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                            C.c_int, C.c_void_p, C.c_void_p]),
+    "ixb_spmm_blockgroupcoo_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                                 C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                                 C.c_int64, C.c_void_p, C.c_int, C.c_void_p,
+                                                 C.c_void_p]),
+    "ixb_conv_plan_run_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                            C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                                            C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

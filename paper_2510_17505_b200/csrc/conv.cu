@@ -544,6 +544,28 @@ struct ConvStreams {  // side streams + events of the host-buffer form, per thre
 thread_local ConvStreams t_conv_streams;
 }  // namespace
 
+namespace ixb {
+int64_t conv_plan_rows(const ixb_conv_plan* P) { return P->n_out; }
+
+void conv_plan_run_rows(ixb_conv_plan* P, const void* In, int64_t Cin, const void* Weight,
+                        int64_t Cout, float* Out, int64_t r0, int64_t r1, cudaStream_t s) {
+  const bool unit = !P->conflict && P->unit && Cin == 64 && Cout == 64 &&
+                    reinterpret_cast<uintptr_t>(In) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(Weight) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(Out) % 16 == 0;
+  if (unit) {
+    if (r0 % 128) fail(IXB_SHAPE, "conv chunk must start on a 128-row tile");
+    launch_unit(P, In, Weight, Out, 0, r0 / 128, ceil_div(r1, 128) - r0 / 128, s);
+    return;
+  }
+  if (r0 != 0 || r1 != P->n_out)
+    fail(IXB_SHAPE, "conv map outside the unit tensor-core path: shard with nchunks = 1");
+  const int rc = ixb_conv_plan_run(P, In, Cin, Weight, Cout, Out, 0, 0,
+                                   reinterpret_cast<ixb_stream>(s));
+  if (rc != IXB_OK) fail(rc, ixb_last_error());
+}
+}  // namespace ixb
+
 extern "C" {
 
 int ixb_conv_plan_create(const int32_t* MAPZ, const int32_t* MAPX, const int32_t* MAPY,

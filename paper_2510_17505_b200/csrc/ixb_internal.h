@@ -110,6 +110,13 @@ void sort_groups(const int32_t* AM, int64_t G, cudaStream_t s, Scratch<int32_t>&
 void gather_rows(const int32_t* perm, const void* src, void* dst, int64_t rows, int64_t row_bytes,
                  cudaStream_t s);
 
+// Conv plan helpers for the sharded entry (shard.cpp): output rows of the
+// plan, and `=` evaluation of rows [r0, r1) (r0 a multiple of 128; the unit
+// tensor-core path, or the whole plan with r0 == 0 and r1 == rows).
+int64_t conv_plan_rows(const ixb_conv_plan* plan);
+void conv_plan_run_rows(ixb_conv_plan* plan, const void* In, int64_t Cin, const void* Weight,
+                        int64_t Cout, float* Out, int64_t r0, int64_t r1, cudaStream_t s);
+
 }  // namespace ixb
 
 // ABI guard: converts exceptions into status codes + thread-local message.

@@ -8,6 +8,11 @@ summation order, hence the gathered result is bit-identical for any number
 of ranks. The dense operand is replicated; the only collective is the final
 all-gather of the output row slabs (padded to the largest slab, one
 all_gather_into_tensor).
+
+The native path (Comm, ShardPlan, *_sharded at the end) does the same
+behind the C-ABI: libixb's own NCCL communicator, C++ shard/chunk planning,
+each rank writing straight into its rows of the full output, and the
+all-gather as in-place NCCL broadcasts overlapping the next chunk's kernel.
 """
 from dataclasses import dataclass
 from typing import List
@@ -221,3 +226,142 @@ def sharded_tp(plan, X, Y, W, shards, rank, group=None, gather=True):
     if s.r1 > s.r0:
         plan.run(X[s.r0:s.r1], Y[s.r0:s.r1], W, local, accumulate=False)
     return gather_rows(local, shards, rank, group) if gather else local
+
+
+# ----------------------------------------------- C-ABI sharded evaluation
+# The native multi-GPU path (include/ixb.h "Sharded evaluation"): NCCL
+# communicator owned by libixb, shard + chunk plan in C++, every rank writing
+# its rows straight into the FULL output and the all-gather (grouped in-place
+# broadcasts) overlapping the next chunk's kernel. The torch.distributed
+# helpers above remain for CPU/gloo checks of the partitioning.
+SHARD_NO_COMM, SHARD_COMM_ONLY = 8, 16
+
+
+class Comm:
+    """libixb's NCCL communicator over the ranks of `group` (default: the
+    whole job). Rank 0's id travels over torch.distributed (any backend)."""
+
+    def __init__(self, world, rank, group=None):
+        import ctypes as C
+
+        from .abi import check, lib
+        self.world, self.rank = world, rank
+        idb = (C.c_char * 128)()
+        if rank == 0 and world == 1:
+            check(lib().ixb_comm_unique_id(idb))
+        if world > 1:
+            import torch.distributed as dist
+            if rank == 0:
+                check(lib().ixb_comm_unique_id(idb))
+            obj = [bytes(idb)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(idb, obj[0], 128)
+        self.h = C.c_void_p()
+        check(lib().ixb_comm_init(idb, world, rank, C.byref(self.h)))
+
+    def broadcast(self, *tensors, root=0, stream=None):
+        """In-place NCCL broadcast of device tensors from `root` (replicating
+        the format and the dense operand once, outside any timed step)."""
+        import ctypes as C
+
+        from .abi import check, lib
+        for t in tensors:
+            assert t.is_contiguous() and t.is_cuda
+            check(lib().ixb_comm_broadcast(self.h, C.c_void_p(t.data_ptr()),
+                                           t.numel() * t.element_size(), root, _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                from .abi import lib
+                lib().ixb_comm_free(self.h)
+            except Exception:  # interpreter shutdown: the process exit frees it
+                pass
+            self.h = None
+
+
+class ShardPlan:
+    """Row-aligned group shards of a sorted group-coordinate array (the
+    replicated format's AM, on the device), each cut into `nchunks`
+    row-aligned chunks (ixb_shard_plan_create)."""
+
+    def __init__(self, AM, rows, world, rank, nchunks=4, stream=None):
+        import ctypes as C
+
+        from .abi import check, lib
+        self.world, self.rank, self.nchunks, self.rows = world, rank, nchunks, rows
+        st = stream if stream is not None else torch.cuda.current_stream()
+        self.h = C.c_void_p()
+        check(lib().ixb_shard_plan_create(C.c_void_p(AM.data_ptr()), AM.numel(), rows, world,
+                                          rank, nchunks, C.c_void_p(st.cuda_stream),
+                                          C.byref(self.h)))
+
+    def chunk(self, rank, c):
+        """(g0, g1, r0, r1) of chunk c of `rank`."""
+        import ctypes as C
+
+        from .abi import check, lib
+        v = [C.c_int64() for _ in range(4)]
+        check(lib().ixb_shard_plan_chunk(self.h, rank, c, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def rows_of(self, rank):
+        return self.chunk(rank, 0)[2], self.chunk(rank, self.nchunks - 1)[3]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                from .abi import lib
+                lib().ixb_shard_plan_free(self.h)
+            except Exception:  # interpreter shutdown: the process exit frees it
+                pass
+            self.h = None
+
+
+def _stream(stream):
+    import ctypes as C
+    st = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(st.cuda_stream)
+
+
+def spmm_groupcoo_sharded(plan, fmt, B, C_full, comm=None, flags=2, stream=None):
+    """Rank plan.rank evaluates its chunks of `C = AV * B[AK]` into its rows
+    of C_full [M, N] and all ranks' rows are broadcast in place: every rank
+    ends with the whole C (comm None: world 1 or flags & SHARD_NO_COMM)."""
+    import ctypes as C
+
+    from .abi import check, lib
+    check(lib().ixb_spmm_groupcoo_sharded(
+        plan.h, C.c_void_p(fmt.AK.data_ptr()), C.c_void_p(fmt.AV.data_ptr()), fmt.group_size,
+        C.c_void_p(B.data_ptr()), B.shape[0], B.shape[1], C.c_void_p(C_full.data_ptr()), flags,
+        comm.h if comm is not None else None, _stream(stream)))
+    return C_full
+
+
+def spmm_blockgroupcoo_sharded(plan, fmt, B, C_full, comm=None, flags=2, stream=None):
+    """Block-row form of spmm_groupcoo_sharded: C_full [MB, 16, N]."""
+    import ctypes as C
+
+    from .abi import check, lib
+    G, g, bm, bk = fmt.AV.shape
+    check(lib().ixb_spmm_blockgroupcoo_sharded(
+        plan.h, C.c_void_p(fmt.AK.data_ptr()), C.c_void_p(fmt.AV.data_ptr()), g, bm, bk,
+        C.c_void_p(B.data_ptr()), B.shape[0], B.shape[2], C.c_void_p(C_full.data_ptr()), flags,
+        comm.h if comm is not None else None, _stream(stream)))
+    return C_full
+
+
+def conv_sharded(local_plan, In, Weight, Out_full, world, rank, nchunks=4, comm=None, flags=0,
+                 stream=None):
+    """Rank `rank` runs its point-block plan (conv_shard_plan over
+    point_blocks(n, world)[rank]) in `nchunks` tile chunks into its rows of
+    Out_full [n, 64]; the rows are all-gathered in place as they finish."""
+    import ctypes as C
+
+    from .abi import check, lib
+    check(lib().ixb_conv_plan_run_sharded(
+        local_plan.h if local_plan is not None else None, C.c_void_p(In.data_ptr()), In.shape[1],
+        C.c_void_p(Weight.data_ptr()), Weight.shape[2], C.c_void_p(Out_full.data_ptr()),
+        Out_full.shape[0], world, rank, nchunks, flags, comm.h if comm is not None else None,
+        _stream(stream)))
+    return Out_full

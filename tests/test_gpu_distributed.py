@@ -249,3 +249,106 @@ def test_more_ranks_than_rows_empty_shards(P, ixo):
 
     blocks = edge_blocks(5, world)
     assert [s.r1 - s.r0 for s in blocks].count(0) == 3 and blocks[-1].r1 == 5
+
+
+# ------------------------------------------- native (C-ABI) sharded path
+@pytest.mark.parametrize("world", WORLDS)
+@pytest.mark.parametrize("nchunks", [1, 3])
+def test_native_groupcoo_shards_bit_identical(P, ixo, world, nchunks):
+    """ixb_spmm_groupcoo_sharded: each virtual rank writes its chunks straight
+    into the full output (no collective); the assembled C equals the
+    unsharded K3 bit for bit, empty rows included."""
+    from paper_2510_17505_b200 import distributed as D
+    rng = ixo.Rng(17)
+    a = ixo.synth_sparse_matrix(rng, 700, 300, 0.05)
+    a[[0, 5, 6, 699]] = 0  # empty rows at the edges and between shards
+    b = ixo.synth_dense(rng, (300, 64))
+    fmt = P.dense_to_groupcoo(torch.from_numpy(a.astype(np.float32)).cuda(), g=4)
+    B = torch.from_numpy(b.astype(np.float32)).cuda()
+    full = torch.empty((700, 64), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, B, full, accumulate=False, flags=2)
+    out = torch.full_like(full, float("nan"))
+    for r in range(world):
+        plan = D.ShardPlan(fmt.AM, 700, world, r, nchunks)
+        D.spmm_groupcoo_sharded(plan, fmt, B, out, comm=None, flags=2 | D.SHARD_NO_COMM)
+    assert torch.equal(out, full)
+    plan = D.ShardPlan(fmt.AM, 700, world, 0, nchunks)
+    rows = [plan.chunk(q, c)[2:] for q in range(world) for c in range(nchunks)]
+    assert rows[0][0] == 0 and rows[-1][1] == 700
+    assert all(x[1] == y[0] for x, y in zip(rows, rows[1:]))  # a partition of the rows
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_native_blockgroupcoo_and_conv_shards(P, ixo, world):
+    """K4 block-row chunks (exact on integer data) and K6 point-block tile
+    chunks (bit-identical) through the native sharded entries."""
+    from paper_2510_17505_b200 import distributed as D
+    rng = ixo.Rng(23)
+    a = ixo.synth_block_sparse_matrix(rng, 16 * 60, 16 * 40, 16, 16, 0.2, ixo.INT)
+    b = ixo.synth_dense(rng, (40, 16, 256), ixo.INT)
+    fmt = P.dense_to_blockgroupcoo(bf16_dev(a), 16, 16, 0)
+    B = bf16_dev(b)
+    full = torch.zeros((60, 16, 256), device="cuda")
+    P.spmm_blockgroupcoo(fmt.AM, fmt.AK, fmt.AV, B, full, flags=2)
+    out = torch.full_like(full, float("nan"))
+    for r in range(world):
+        plan = D.ShardPlan(fmt.AM, 60, world, r, 2)
+        D.spmm_blockgroupcoo_sharded(plan, fmt, B, out, flags=2 | D.SHARD_NO_COMM)
+    assert torch.equal(out, full)
+
+    g = np.random.default_rng(5)
+    pts = np.unique(g.integers(0, 24, (6000, 3)), axis=0).astype(np.int32)
+    n = len(pts)
+    mo, mi, mz = P.kernel_map(torch.from_numpy(pts).cuda())
+    ones = torch.ones(mo.numel(), device="cuda")
+    gt = P.group_coo_tensor([n, n, 27], [mo, mi, mz], ones, 2, 16, canonical=True)
+    In = bf16_dev(g.standard_normal((n, 64)))
+    W = bf16_dev(g.standard_normal((27, 64, 64)) * 0.1)
+    ref = torch.zeros((n, 64), device="cuda")
+    P.ConvPlan(gt.group_coord, gt.member_coords[0], gt.member_coords[1], gt.values, n, 27,
+               n).run(In, W, ref, accumulate=False)
+    out = torch.full_like(ref, float("nan"))
+    for r, s in enumerate(D.point_blocks(n, world)):
+        local = D.conv_shard_plan(mo, mi, mz, n, s, 16) if s.r1 > s.r0 else None
+        D.conv_sharded(local, In, W, out, world, r, nchunks=3, flags=D.SHARD_NO_COMM)
+    assert torch.equal(out, ref)
+
+
+def test_native_sharded_with_nccl_comm(P, ixo):
+    """The full native path with a real (1-rank) NCCL communicator: chunk
+    evaluation, in-place broadcasts on the side stream, and the join back
+    onto the caller's stream — also inside a captured CUDA graph."""
+    from paper_2510_17505_b200 import distributed as D
+    rng = ixo.Rng(3)
+    a = ixo.synth_sparse_matrix(rng, 500, 200, 0.05)
+    b = ixo.synth_dense(rng, (200, 128))
+    fmt = P.dense_to_groupcoo(torch.from_numpy(a.astype(np.float32)).cuda(), g=0)
+    B = torch.from_numpy(b.astype(np.float32)).cuda()
+    full = torch.empty((500, 128), device="cuda")
+    P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, B, full, accumulate=False, flags=2)
+    comm = D.Comm(1, 0)
+    plan = D.ShardPlan(fmt.AM, 500, 1, 0, 4)
+    out = torch.full_like(full, float("nan"))
+    D.spmm_groupcoo_sharded(plan, fmt, B, out, comm=comm)
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+    out.fill_(float("nan"))
+    D.spmm_groupcoo_sharded(plan, fmt, B, out, comm=comm, flags=2 | D.SHARD_COMM_ONLY)
+    torch.cuda.synchronize()
+    assert torch.isnan(out).all()  # gather only: nothing computed
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+        D.spmm_groupcoo_sharded(plan, fmt, B, out, comm=comm, flags=1 | 2)  # async index check
+    out.fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+
+
+def test_native_comm_broadcast_one_rank(P):
+    from paper_2510_17505_b200 import distributed as D
+    comm = D.Comm(1, 0)
+    t = torch.arange(1000, dtype=torch.float32, device="cuda")
+    comm.broadcast(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t, torch.arange(1000, dtype=torch.float32, device="cuda"))
