@@ -51,7 +51,9 @@ unsigned* work_counters(cudaStream_t stream, size_t n);
 // demand, never shrunk): kernel scratch that must not add allocation nodes
 // to a captured CUDA graph. Contents are undefined on entry. Returns null
 // when the buffer would have to grow while `stream` is being captured.
-void* stream_buffer(cudaStream_t stream, size_t bytes);
+// `tag` keeps the buffers of different kernels apart.
+enum { kBufK4Partials = 0, kBufK3Split = 1 };
+void* stream_buffer(cudaStream_t stream, size_t bytes, int tag);
 // Resets the record on `stream` before a checked launch.
 void reset_error_record(cudaStream_t stream);
 // Syncs `stream`, reads the record; on an offender throws IXB_INDEX_RANGE with

@@ -23,10 +23,11 @@ struct DeviceCtx {
   // stream (kernels on different streams must not share a counter)
   unsigned* counters = nullptr;
   std::vector<cudaStream_t> counter_streams;
-  std::vector<std::pair<void*, size_t>> stream_bufs;  // per counter slot: persistent scratch
+  // per (counter slot, tag): persistent scratch
+  std::vector<std::vector<std::pair<void*, size_t>>> stream_bufs;
 };
 constexpr int kCounterSlots = 64;
-constexpr size_t kCountersPerSlot = 16384;
+constexpr size_t kCountersPerSlot = 65536;
 std::mutex g_mu;
 std::vector<DeviceCtx> g_dev;
 
@@ -98,14 +99,16 @@ unsigned* work_counters(cudaStream_t stream, size_t n) {
   return c.counters + kCountersPerSlot * i;
 }
 
-void* stream_buffer(cudaStream_t stream, size_t bytes) {
+void* stream_buffer(cudaStream_t stream, size_t bytes, int tag) {
   work_counters(stream, 0);  // assigns the stream its slot
   DeviceCtx& c = ctx();
   std::lock_guard<std::mutex> lk(g_mu);
   size_t i = 0;
   while (c.counter_streams[i] != stream) ++i;
-  if (c.stream_bufs.size() <= i) c.stream_bufs.resize(i + 1, {nullptr, 0});
-  auto& b = c.stream_bufs[i];
+  if (c.stream_bufs.size() <= i) c.stream_bufs.resize(i + 1);
+  if (c.stream_bufs[i].size() <= static_cast<size_t>(tag))
+    c.stream_bufs[i].resize(static_cast<size_t>(tag) + 1, {nullptr, 0});
+  auto& b = c.stream_bufs[i][static_cast<size_t>(tag)];
   if (b.second < bytes) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cuda_check(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");

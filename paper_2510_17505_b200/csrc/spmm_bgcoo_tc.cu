@@ -584,7 +584,7 @@ void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaSt
   if (grid > a.G) grid = a.G;
   a.rowctr = work_counters(s, static_cast<size_t>(grid) * a.ntiles);
   const size_t part_n = static_cast<size_t>(grid) * 2 * 16 * a.N;
-  a.part = static_cast<float*>(stream_buffer(s, part_n * sizeof(float)));
+  a.part = static_cast<float*>(stream_buffer(s, part_n * sizeof(float), kBufK4Partials));
   Scratch<float> part_graph;  // first use inside a graph capture
   if (!a.part) {
     part_graph = Scratch<float>(part_n, s);
