@@ -41,44 +41,50 @@ constexpr int kTB = 256;
 // thread reduces its rows in registers, warps reduce by shuffles, one smem
 // atomic per warp per statistic, one global atomic per CTA per statistic.
 __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
-  __shared__ unsigned long long sh[35];
-  for (int i = threadIdx.x; i < 35; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  unsigned long long S = 0, nz = 0, mx = 0, grp[32] = {};
+  __shared__ unsigned long long part[kTB / 32][35];
+  // 32-bit per-thread partials (a warp's rows hold < 2^32 nonzeros: int32
+  // coordinates), warp sums by REDUX (__reduce_*_sync: one instruction per
+  // statistic instead of five 64-bit shuffle rounds), 64-bit from smem on;
+  // grp[i] is warp-uniform after the reduction: lane i stores it
+  unsigned S = 0, nz = 0, mx = 0, grp[32] = {};
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    unsigned long long o = static_cast<unsigned long long>(occ[r]);
+    const unsigned o = static_cast<unsigned>(occ[r]);
     S += o;
     nz += o > 0;
     mx = o > mx ? o : mx;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) grp[i] += (o + (1ull << i) - 1) >> i;
+    for (int i = 0; i < 32; ++i) grp[i] += static_cast<unsigned>(
+        (static_cast<unsigned long long>(o) + (1ull << i) - 1) >> i);
+  }
+  S = __reduce_add_sync(0xffffffffu, S);
+  nz = __reduce_add_sync(0xffffffffu, nz);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) grp[i] = __reduce_add_sync(0xffffffffu, grp[i]);
+  // per-warp partials to smem, then 35 threads each sum one statistic over
+  // the CTA's warps (no shared-memory atomics) and do one global atomic
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    part[w][0] = S;
+    part[w][1] = nz;
+    part[w][2] = mx;
   }
 #pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    S += __shfl_xor_sync(0xffffffffu, S, off);
-    nz += __shfl_xor_sync(0xffffffffu, nz, off);
-    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, off);
-    mx = m2 > mx ? m2 : mx;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) grp[i] += __shfl_xor_sync(0xffffffffu, grp[i], off);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&sh[0], S);
-    atomicAdd(&sh[1], nz);
-    atomicMax(&sh[2], mx);
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (grp[i]) atomicAdd(&sh[3 + i], grp[i]);
-  }
+  for (int i = 0; i < 32; ++i)
+    if (lane == i) part[w][3 + i] = grp[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (sh[0]) atomicAdd(&out->S, sh[0]);
-    if (sh[1]) atomicAdd(&out->nonzero, sh[1]);
-    atomicMax(&out->maxocc, sh[2]);
+  const int nw = blockDim.x >> 5;
+  if (threadIdx.x < 35) {
+    unsigned long long v = 0;
+    for (int k = 0; k < nw; ++k) {
+      const unsigned long long x = part[k][threadIdx.x];
+      v = threadIdx.x == 2 ? (x > v ? x : v) : v + x;
+    }
+    if (threadIdx.x == 2) atomicMax(&out->maxocc, v);
+    else if (v) atomicAdd(threadIdx.x < 2 ? (threadIdx.x == 0 ? &out->S : &out->nonzero)
+                                          : &out->groups_pow2[threadIdx.x - 3], v);
   }
-  if (threadIdx.x < 32 && sh[3 + threadIdx.x])
-    atomicAdd(&out->groups_pow2[threadIdx.x], sh[3 + threadIdx.x]);
 }
 
 }  // namespace
@@ -416,9 +422,14 @@ __global__ void run_pack_elems(RunPackArgs a) {
   if (a.mask) a.mask[slot] = 1;
 }
 
-__global__ void run_pack_runs(RunPackArgs a) {
-  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// Per run: its group coordinates and the pad slots of its last group.
+// `cta`: one CTA per run, threads striding the run's groups and pads (few
+// long runs, e.g. the 27 offsets of a kernel map); otherwise one thread per
+// run (many short runs).
+__global__ void run_pack_runs(RunPackArgs a, int cta) {
+  const int64_t r = cta ? blockIdx.x : static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= a.R) return;
+  const int64_t t0 = cta ? threadIdx.x : 0, dt = cta ? blockDim.x : 1;
   const int64_t len = a.len[r];
   const int64_t ng = (len + a.g - 1) / a.g;
   const int64_t g0 = a.gofs[r];
@@ -426,9 +437,9 @@ __global__ void run_pack_runs(RunPackArgs a) {
   const int64_t src0 = a.perm ? a.perm[first] : first;
   const int64_t srcl = a.perm ? a.perm[last] : last;
   const int32_t gc = a.gcoord[src0];
-  for (int64_t j = 0; j < ng; ++j) a.gout[g0 + j] = gc;
+  for (int64_t j = t0; j < ng; j += dt) a.gout[g0 + j] = gc;
   const int64_t real_last = len - (ng - 1) * a.g;
-  for (int64_t q = real_last; q < a.g; ++q) {
+  for (int64_t q = real_last + t0; q < a.g; q += dt) {
     const int64_t slot = (g0 + ng - 1) * a.g + q;
     for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][srcl];
     if (a.vbytes == 8) static_cast<unsigned long long*>(a.vout)[slot] = 0ull;  // 0.0 / 0
@@ -773,7 +784,8 @@ void pack_sorted_runs(ixb_pack* P, const void* vals, int dtype, int32_t* gout,
   if (a.n > 0) {
     run_pack_elems<<<ceil_div(a.n, kTB), kTB, 0, P->s>>>(a);
     IXB_LAUNCH_CHECK("run_pack_elems");
-    run_pack_runs<<<ceil_div(a.R, kTB), kTB, 0, P->s>>>(a);
+    if (a.R <= 4 * sm_count()) run_pack_runs<<<a.R, 128, 0, P->s>>>(a, 1);
+    else run_pack_runs<<<ceil_div(a.R, kTB), kTB, 0, P->s>>>(a, 0);
     IXB_LAUNCH_CHECK("run_pack_runs");
   }
 }
