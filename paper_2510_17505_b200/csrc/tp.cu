@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -26,47 +28,19 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kEdges = 64;                         // edges per tile
-constexpr int kMathWarps = 16;                     // 64 edges x 8 u-slices
-constexpr int kMathThreads = kMathWarps * 32;
-constexpr int kEpiWarps = 4;                        // one per TMEM lane quarter
-constexpr int kTpThreads = kMathThreads + 64 + kEpiWarps * 32;  // + UMMA, TMA, epilogue warps
-constexpr int kPairs = 8;                           // component pairs (16 components)
-constexpr int kMaxJobs = 192;
-constexpr int kMaxJSteps = 512;
-constexpr int kMaxPathSeq = 64;
-constexpr int kNU = 2;                              // U ring (job operands, hi + lo)
-constexpr int kNW = 2;                              // W ring (one path each)
-constexpr int kGroupWarps = kMathWarps / 2;         // math warps per job group
-#ifndef IXB_TP_JUNROLL
-#define IXB_TP_JUNROLL 1
-#endif
-constexpr int kJUnroll = IXB_TP_JUNROLL;            // j-step loop unroll
-constexpr uint32_t kUHalf = 128 * 128;              // 128 rows (2 comps x 64 edges) x 64 bf16
-constexpr uint32_t kUSlot = 2 * kUHalf;             // hi, lo
-constexpr uint32_t kWTileTp = 64 * 128;             // 64 u-rows x 64 bf16
-constexpr uint32_t kXTile = kEdges * 16 * 128;      // 64 edges x 16 irrep rows x 64 bf16
-
-// CG table reshaped for the tensor-core path, passed by value (constant bank:
-// every lane reads the same entry, which the constant cache broadcasts).
-// A job's entries are regrouped by input row j ("j-steps"): each X row is
-// loaded and converted once per job and feeds both components of the pair,
-// with coef_h(j) = sum_k v * Y[k] over the component's entries at that j.
-struct TpMeta {
-  int njobs, npaths, ni, present;  // present: bit i = component i receives a job
-  int ncp;                         // component pairs that receive a job
-  int cp_order[kPairs];            // drain order: the ncp pairs with jobs by their last job, then the rest
-  // job: {l | first-touch-of-cp << 8 | last-job-of-path << 9 | first-job-of-path << 10 |
-  //       last-touch-of-cp << 11, cp | path-seq << 8, first j-step | j-step count << 16, 0}
-  int4 job[kMaxJobs];
-  // j-step: {j | n0 << 4 | n1 << 6 | k00 << 8 | k01 << 12 | k10 << 16 | k11 << 20,
-  //          v00, v01, v10 (float bits)} and v11 in jv11: component 2cp has n0 <= 2
-  //          terms (k0t, v0t) at this j, component 2cp+1 has n1 <= 2 (a (component, j)
-  //          with more terms takes several steps)
-  int4 jstep[kMaxJSteps];
-  float jv11[kMaxJSteps];
-  int path_l[kMaxPathSeq];  // W index of each path in job order
-};
+constexpr int kEdges = 64;          // edges per tile: UMMA M = 128 = 2 input rows x 64 edges
+constexpr int kMaxPairs = 8;        // input-row pairs (nj <= 16): TMEM columns [0, 256)
+constexpr int kNWs = 3;             // W ring: slots of two W[l] tiles (a path pair)
+constexpr int kConsumerWarps = 16;  // 4 warpgroups, one output row of the pass each
+constexpr int kTpThreads = (2 + kConsumerWarps) * 32;  // TMA, MMA + consumers
+constexpr uint32_t kXPair = 2 * kEdges * 128;          // [2 rows][64 edges][128 B], SW128
+constexpr uint32_t kWTile = 64 * 128;                  // W[l] [64 u][64 w], SW128 MN-major
+constexpr uint32_t kWSlot = 2 * kWTile;
+constexpr uint32_t kVBase = 256;                       // V ring: 2 x 128 TMEM columns
+constexpr uint32_t kYwgElems = 16 * kEdges;            // per warpgroup: Y [16 k][64 edges] bf16
+constexpr uint32_t kExchF4 = 2 * 4 * kEdges;           // per warpgroup: [half][chunk][edge] float4
+constexpr uint32_t kTpSmem = kMaxPairs * kXPair + kNWs * kWSlot + 2 * 4 * kYwgElems * 2 +
+                             4 * kExchF4 * 16 + 512 + 1024;
 
 // acc(2 lanes) += coef * x(2 lanes): one FFMA2.
 __device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
@@ -80,70 +54,78 @@ __device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
   return r;
 }
 
+// Schedule of one 64-edge tile, built once per CG table (ixb_tp_plan_create).
+//  pass  {first group, groups, out rows of warpgroups 0,1 (int16 each), 2,3}
+//  group {jp | mask << 4 | first use of pair jp << 6 | first group of its W
+//         slot << 7 | last group of its W slot << 8}: one UMMA chain
+//         V = X[rows 2jp, 2jp+1] . [W[la] | W[lb]] (mask: which of the slot's
+//         two paths; both -> N = 128)
+//  refs  [group][path 0/1][warpgroup][half]: CG terms of (l, out row, j =
+//         2jp + half) as offset | count << 24 into terms {k (int bits), v}
+//  wseq  {la, lb or -1}: the W tiles of each W slot, in group order
 struct TpArgs {
+  const int4* pass;
+  const int4* grp;
+  const uint32_t* refs;
+  const float2* terms;
+  const int2* wseq;
   const __nv_bfloat16* Y;  // [B, nk]
   float* Z;                // [B, ni, 64]
   int64_t batch;
-  int nj, nk, ni;
-  int accumulate;
+  int nk, ni, npasses, ngroups, nwseq, pair_mask, y_vec, accumulate;
 };
 
-// Output-side factorisation, batched two output components at
-// a time so every UMMA has M = 128:
-//   U_{l,i}[b,u] = sum_{(j,k,v) in (l,i)} v * Y[b,k] * X[b,j,u]   (CUDA cores)
-//   Z[b,i,:]    += U_{l,i}[b,:] . W[l]                           (tcgen05)
-// A job = (path l, component pair cp): A rows 0..63 = U_{l,2cp}, rows 64..127
-// = U_{l,2cp+1} (zero when the path has no such component), B = W[l], D =
-// TMEM columns [64 cp, 64 cp + 64) (lanes 0..63 component 2cp, 64..127
-// component 2cp+1): 8 pairs x 64 = all 512 columns.
-// Warps 0..15 compute U for job n into a kNU-deep ring (mbarrier handoff,
-// no block-wide barrier per job), warp 16 issues 4 UMMAs (K = 64) per job and
-// commits the slot back, warp 17 streams X tiles and W[l] (kNW ring) by TMA,
-// warps 18..21 drain TMEM into Z. TMEM is handed over per component pair:
-// the issuer commits acc_full[cp] after the pair's last job of the tile and
-// waits on acc_empty[cp] before its first job of the next tile. Paths run
-// in order of their output irrep, so pairs complete one after another and
-// draining overlaps the remaining jobs and the next tile's start.
+// V-first factorisation:
+//   V[b,l,j,:] = X[b,j,:] . W[l]                          (tcgen05, exact bf16 products)
+//   Z[b,i,:]  += sum_{l,j} (sum_k v * Y[b,k]) * V[b,l,j,:] (CUDA cores, fp32)
+// A tile is 64 edges; UMMA rows m < 64 are (edge m, row 2jp), m >= 64 (edge
+// m - 64, row 2jp + 1), so one M = 128 MMA chain covers a pair of input rows.
+// X pairs arrive by TMA ({64 u, 64 edges, 2 rows} boxes, SW128) and are
+// copied into TMEM columns [32 jp, 32 jp + 32) by tcgen05.cp on first use in
+// the tile: the A operand then comes from TMEM and shared memory only feeds W.
+// Output rows are processed four at a time ("passes"); warpgroup h owns
+// output row h of the pass for all 64 columns, so every consumer thread
+// keeps one (edge, row-of-the-pair, out row) accumulator of 64 floats in
+// registers and computes each CG coefficient once. The two rows of a pair
+// sit in different warps (TMEM lanes m and m + 64), so their partial sums
+// meet once per pass through shared memory (each half finalises 32 columns).
+// Warps: 0 TMA (X pairs one tile ahead, W slots paced by the MMA), 1 TMEM
+// alloc + MMA issuer, 2..17 consumers (576 threads: 112 registers each).
 __global__ void __launch_bounds__(kTpThreads, 1)
-    tp_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                 const __grid_constant__ TpMeta meta, TpArgs a) {
+    tp_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                 TpArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  // align by offset (not through an integer cast) so every derived pointer
-  // stays in the shared space: LDS/STS instead of generic loads
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* Xs = smem;                   // [64 edges * nj rows][128 B]
-  uint8_t* Us = Xs + kXTile;            // [kNU][128 rows][128 B]  (SW128 K-major)
-  uint8_t* Ws = Us + kNU * kUSlot;      // [kNW][64 rows][128 B]   (SW128 MN-major)
-  float* Ys = reinterpret_cast<float*>(Ws + kNW * kWTileTp);  // [2 groups][64][16]
-  uint64_t* x_full = reinterpret_cast<uint64_t*>(Ys + 2 * kEdges * 16);
-  uint64_t* x_empty = x_full + 1;
-  uint64_t* w_full = x_empty + 1;
-  uint64_t* w_empty = w_full + kNW;
-  uint64_t* u_full = w_empty + kNW;
-  uint64_t* u_empty = u_full + kNU;
-  uint64_t* acc_full = u_empty + kNU;      // [kPairs]
-  uint64_t* acc_empty = acc_full + kPairs;  // [kPairs]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kPairs);
+  uint8_t* Xs = smem;                                               // [8 pairs][16 KB]
+  uint8_t* Ws = Xs + kMaxPairs * kXPair;                            // [3][2 tiles][8 KB]
+  uint16_t* Yw = reinterpret_cast<uint16_t*>(Ws + kNWs * kWSlot);   // [4 wg][16 k][64 e]
+  uint16_t* Yr = Yw + 4 * kYwgElems;                                // [4 wg][64 e][16 k] raw
+  float4* Ex = reinterpret_cast<float4*>(Yr + 4 * kYwgElems);       // [4 wg][2][4][64]
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(Ex + 4 * kExchF4);
+  uint64_t* x_empty = x_full + kMaxPairs;
+  uint64_t* w_full = x_empty + kMaxPairs;
+  uint64_t* w_empty = w_full + kNWs;
+  uint64_t* v_full = w_empty + kNWs;
+  uint64_t* v_empty = v_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    mbar_init(x_full, 1);
-    mbar_init(x_empty, kMathWarps);
-    for (int s = 0; s < kNW; ++s) {
+    for (int p = 0; p < kMaxPairs; ++p) {
+      mbar_init(&x_full[p], 1);
+      mbar_init(&x_empty[p], 1);
+    }
+    for (int s = 0; s < kNWs; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
     }
-    for (int s = 0; s < kNU; ++s) {
-      mbar_init(&u_full[s], kGroupWarps);  // slot s is written by job group s
-      mbar_init(&u_empty[s], 1);
-    }
-    for (int c = 0; c < kPairs; ++c) {
-      mbar_init(&acc_full[c], 1);
-      mbar_init(&acc_empty[c], kEpiWarps);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], kConsumerWarps);
     }
     fence_barrier_init();
   }
-  if (warp == kMathWarps) {
+  if (warp == 1) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
   }
@@ -152,233 +134,221 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (a.batch + kEdges - 1) / kEdges;
-  const int njobs = meta.njobs, npaths = meta.npaths;
-
-  if (warp == kMathWarps + 1) {
-    // ---------------------------------------------------------- TMA producer
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    // W slots are paced by the MMA (3-deep ring); the X pairs of the next tile
+    // are issued as soon as the current tile has copied each pair into TMEM
+    // (polled between W loads), so X streams one tile ahead of the MMAs.
     if (lane == 0) {
-      tma_prefetch_desc(&tmW);
       tma_prefetch_desc(&tmX);
-      const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
-      // whole 256-row boxes land (out-of-range rows zero-filled), so expect them all
-      const uint32_t x_bytes = static_cast<uint32_t>(((kEdges * a.nj + 255) / 256) * 256 * 128);
-      int64_t wc = 0;  // W loads issued
+      tma_prefetch_desc(&tmW);
+      const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
+      uint32_t wc = 0;
+      int64_t xt = blockIdx.x;  // tile of the next X load
+      int xtl = 0, xp = 0;      // its tile ordinal and pair
+      // issue X loads in (tile, pair) order up to tile ordinal `upto`; without
+      // `block`, stop at the first staging slot not yet copied out
+      auto x_next = [&](int upto, bool block) {
+        while (xt < ntiles && xtl <= upto) {
+          if (!((a.pair_mask >> xp) & 1)) {
+            if (++xp == kMaxPairs) xp = 0, xt += gridDim.x, ++xtl;
+            continue;
+          }
+          const uint32_t par = (xtl & 1) ^ 1;  // previous tile's copy of this pair done
+          if (!block && !mbar_test(&x_empty[xp], par)) return;
+          mbar_wait(&x_empty[xp], par);
+          mbar_arrive_expect_tx(&x_full[xp], kXPair);
+          tma_load_3d(Xs + xp * kXPair, &tmX, &x_full[xp], 0, static_cast<int32_t>(xt * kEdges),
+                      2 * xp, stream);
+          if (++xp == kMaxPairs) xp = 0, xt += gridDim.x, ++xtl;
+        }
+      };
       int tl = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-        mbar_wait_backoff(x_empty, (tl & 1) ^ 1, 128);  // previous tile's X fully consumed
-        mbar_arrive_expect_tx(x_full, x_bytes);
-        for (int r0 = 0; r0 < kEdges * a.nj; r0 += 256)
-          tma_load_2d(Xs + r0 * 128, &tmX, x_full, 0,
-                      static_cast<int32_t>(tile * kEdges * a.nj + r0), stream);
-        for (int ps = 0; ps < npaths; ++ps, ++wc) {
-          const int slot = static_cast<int>(wc % kNW);
-          mbar_wait_backoff(&w_empty[slot], ((wc / kNW) & 1) ^ 1, 64);
-          mbar_arrive_expect_tx(&w_full[slot], kWTileTp);
-          tma_load_2d(Ws + slot * kWTileTp, &tmW, &w_full[slot], 0, meta.path_l[ps] * 64, keep);
+        // this tile's X must be in flight before its W (the MMA needs both)
+        x_next(tl, true);
+        for (int n = 0; n < a.nwseq; ++n, ++wc) {
+          const int2 w = __ldg(&a.wseq[n]);
+          const uint32_t ws = wc % kNWs;
+          while (!mbar_test(&w_empty[ws], ((wc / kNWs) & 1) ^ 1)) x_next(tl + 1, false);
+          mbar_arrive_expect_tx(&w_full[ws], w.y >= 0 ? kWSlot : kWTile);
+          tma_load_2d(Ws + ws * kWSlot, &tmW, &w_full[ws], 0, w.x * 64, keep);
+          if (w.y >= 0) tma_load_2d(Ws + ws * kWSlot + kWTile, &tmW, &w_full[ws], 0, w.y * 64, keep);
+          x_next(tl + 1, false);
         }
       }
     }
-  } else if (warp == kMathWarps) {
-    // ---------------------------------------------------------- UMMA issuer
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, 64, /*A K-major*/ false, /*B MN-major*/ true);
+      constexpr uint32_t idesc64 = idesc_bf16_f32(128, 64, false, /*B MN-major*/ true);
+      constexpr uint32_t idesc128 = idesc_bf16_f32(128, 128, false, true);
+      uint32_t gc = 0, wc = 0;
       int tl = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-        const int64_t jc0 = static_cast<int64_t>(tl) * njobs;
-        const int64_t wc0 = static_cast<int64_t>(tl) * npaths;
-        for (int n = 0; n < njobs; ++n) {
-          const int4 job = meta.job[n];
-          const int cp = job.y & 0xFF, ps = job.y >> 8;
-          const int64_t wc = wc0 + ps;
-          const int wslot = static_cast<int>(wc % kNW);
-          if ((job.x >> 10) & 1) mbar_wait(&w_full[wslot], (wc / kNW) & 1);
-          const int64_t jc = jc0 + n;
-          const int us = static_cast<int>(jc % kNU);
-          mbar_wait(&u_full[us], (jc / kNU) & 1);
-          tc_fence_after();
-          const uint32_t u0 = smem_u32(Us + us * kUSlot);
-          const uint32_t w0 = smem_u32(Ws + wslot * kWTileTp);
-          const bool first = (job.x >> 8) & 1;
-          if (first) {  // this pair's columns drained from the previous tile
-            mbar_wait(&acc_empty[cp], (tl & 1) ^ 1);
+        for (int gi = 0; gi < a.ngroups; ++gi, ++gc) {
+          const int f = __ldg(&a.grp[gi].x);
+          const int jp = f & 15, mask = (f >> 4) & 3;
+          const uint32_t ws = wc % kNWs;
+          if ((f >> 7) & 1) mbar_wait(&w_full[ws], (wc / kNWs) & 1);
+          const uint32_t vs = gc & 1;
+          mbar_wait(&v_empty[vs], ((gc >> 1) & 1) ^ 1);
+          if ((f >> 6) & 1) {  // first use of this pair in the tile: stage it into TMEM
+            mbar_wait(&x_full[jp], tl & 1);
             tc_fence_after();
+            const uint32_t x0 = smem_u32(Xs + jp * kXPair);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tmem_cp_128x256b(tmem + 32 * jp + 8 * kk,
+                               smem_desc(x0 + kk * 32, 16, 1024, kLayoutSW128));
+            umma_commit(&x_empty[jp]);  // staging slot reusable once copied
           }
+          tc_fence_after();
+          const uint32_t d = tmem + kVBase + 128 * vs + (mask == 2 ? 64 : 0);
+          const uint32_t w0 = smem_u32(Ws + ws * kWSlot) + (mask == 2 ? kWTile : 0);
+          const uint32_t idesc = mask == 3 ? idesc128 : idesc64;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
-            umma_f16(tmem + cp * 64, smem_desc(u0 + kk * 32, 16, 1024, kLayoutSW128), bd, idesc,
-                     (!first || kk > 0) ? 1u : 0u);
-            umma_f16(tmem + cp * 64, smem_desc(u0 + kUHalf + kk * 32, 16, 1024, kLayoutSW128), bd,
-                     idesc, 1u);
-          }
-          umma_commit(&u_empty[us]);                         // U slot reusable
-          if ((job.x >> 9) & 1) umma_commit(&w_empty[wslot]);  // last job of this path
-          if ((job.x >> 11) & 1) umma_commit(&acc_full[cp]);   // pair complete for this tile
-        }
-      }
-    }
-  } else if (warp < kMathWarps) {
-    // ---------------------------------------------------------- math warps
-    // Two groups of 8 warps take alternate jobs (job jc -> group jc % 2 -> U
-    // slot jc % 2, the issuer's ring order): one group computes while the
-    // other group's slot is being consumed, so the handoff round trip hides
-    // behind math. A thread owns one edge and 16 u of both components.
-    const int grp = warp / kGroupWarps;
-    const int gt = tid - grp * kGroupWarps * 32;
-    const int b_loc = gt >> 2, slice = gt & 3;  // edge in tile, u chunks {slice, slice + 4}
-    // A thread owns the 8-u chunks cA, cB = {slice, slice + 4}, odd edges in
-    // swapped order: each X load of a warp (8 edges x 4 lanes, edge rows 2 KB
-    // apart) then covers both 64 B halves of the banks, conflict-free.
-    const int cA = slice + 4 * (b_loc & 1), cB = slice + 4 * (~b_loc & 1);
-    uint32_t rowo[2][2];  // [component][chunk A/B] in the SW128 U tile
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int r = h * 64 + b_loc, ch = c ? cB : cA;
-        rowo[h][c] = r * 128 + ((ch ^ (r & 7)) << 4);
-      }
-    const uint8_t* xrow = Xs + b_loc * a.nj * 128;
-    float* yrow = Ys + (grp * kEdges + b_loc) * 16;
-    int tl = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-      const int64_t b = tile * kEdges + b_loc;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = 4 * slice + q;
-        yrow[k] = (b < a.batch && k < a.nk) ? __bfloat162float(a.Y[b * a.nk + k]) : 0.f;
-      }
-      __syncwarp();  // an edge's 4 threads share one warp
-      mbar_wait(x_full, tl & 1);
-      const int64_t jc0 = static_cast<int64_t>(tl) * njobs;
-      for (int n = 0; n < njobs; ++n) {
-        const int64_t jc = jc0 + n;
-        if (static_cast<int>(jc & 1) != grp) continue;
-        const int4 job = meta.job[n];
-        float2 a2[2][8];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) a2[h][q] = make_float2(0.f, 0.f);
-        const int s0 = job.z & 0xFFFF, ns = job.z >> 16;
-        int4 js_next = ns > 0 ? meta.jstep[s0] : make_int4(0, 0, 0, 0);
-#pragma unroll kJUnroll
-        for (int st = s0; st < s0 + ns; ++st) {
-          const int4 js = js_next;
-          if (st + 1 < s0 + ns) js_next = meta.jstep[st + 1];  // next entry in flight
-          const int n0 = (js.x >> 4) & 3, n1 = (js.x >> 6) & 3;
-          const uint8_t* xp = xrow + (js.x & 15) * 128;
-          const uint4 xv0 = *reinterpret_cast<const uint4*>(xp + cA * 16);
-          const uint4 xv1 = *reinterpret_cast<const uint4*>(xp + cB * 16);
-          float c0 = __int_as_float(js.y) * yrow[(js.x >> 8) & 15];
-          float c1 = __int_as_float(js.w) * yrow[(js.x >> 16) & 15];
-          if (n0 > 1) c0 = fmaf(__int_as_float(js.z), yrow[(js.x >> 12) & 15], c0);
-          if (n1 > 1) c1 = fmaf(meta.jv11[st], yrow[(js.x >> 20) & 15], c1);
-          float2 xf[8];
-          const __nv_bfloat162* xh0 = reinterpret_cast<const __nv_bfloat162*>(&xv0);
-          const __nv_bfloat162* xh1 = reinterpret_cast<const __nv_bfloat162*>(&xv1);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            xf[q] = __bfloat1622float2(xh0[q]);
-            xf[4 + q] = __bfloat1622float2(xh1[q]);
-          }
-          if (n0) {  // uniform: every lane runs the same job
-#pragma unroll
-            for (int q = 0; q < 8; ++q) a2[0][q] = ffma2(c0, xf[q], a2[0][q]);
-          }
-          if (n1) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) a2[1][q] = ffma2(c1, xf[q], a2[1][q]);
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16_ts(d, tmem + 32 * jp + 8 * kk,
+                        smem_desc(w0 + kk * 2048, kWTile, 1024, kLayoutSW128), idesc,
+                        kk > 0 ? 1u : 0u);
+          umma_commit(&v_full[vs]);
+          if ((f >> 8) & 1) {
+            umma_commit(&w_empty[ws]);
+            ++wc;
           }
         }
-        // U = hi + lo, both bf16 (the UMMA pair sees U to ~2^-16 relative, so
-        // the only bf16 roundings are the operands X, Y, W)
-        mbar_wait(&u_empty[grp], static_cast<uint32_t>((jc >> 1) & 1) ^ 1);
-        uint8_t* U = Us + grp * kUSlot;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint4 hi, lo;
-            __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(&hi);
-            __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(&lo);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float2 v = a2[h][4 * c + q];
-              ph[q] = __floats2bfloat162_rn(v.x, v.y);
-              const float2 back = __bfloat1622float2(ph[q]);
-              pl[q] = __floats2bfloat162_rn(v.x - back.x, v.y - back.y);
-            }
-            *reinterpret_cast<uint4*>(U + rowo[h][c]) = hi;
-            *reinterpret_cast<uint4*>(U + kUHalf + rowo[h][c]) = lo;
-          }
-        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&u_full[grp]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(x_empty);  // X of this tile no longer read
     }
   } else {
-    // ---------------------------------------------------------- epilogue warps
-    // TMEM lane quarter q = warp % 4: component parity q >> 1, edges (q & 1) * 32 + lane
-    const int quarter = warp & 3;
-    int tl = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-      const int64_t be = tile * kEdges + (quarter & 1) * 32 + lane;
-#pragma unroll 1
-      for (int oc = 0; oc < kPairs; ++oc) {
-        const bool touched = oc < meta.ncp;
-        const int cp = meta.cp_order[oc];
-        const int comp = 2 * cp + (quarter >> 1);
-        if (2 * cp >= a.ni) continue;
-        const bool row_ok = be < a.batch && comp < a.ni;
-        float4* z = reinterpret_cast<float4*>(a.Z + (be * a.ni + comp) * 64);
-        if (!touched) {  // no job writes this pair: `=` stores zeros, `+=` leaves Z
-          if (row_ok && !a.accumulate)
-            for (int c = 0; c < 16; ++c) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-          continue;
-        }
-        mbar_wait_backoff(&acc_full[cp], tl & 1, 256);  // idle polls would steal math issue slots
-        tc_fence_after();
-        const bool has = comp < a.ni && ((meta.present >> comp) & 1);
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {  // 16 columns at a time keeps register pressure low
-          uint32_t r[16];
-          tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cp * 64 + c * 16,
-                             r);
-          tmem_ld_wait();
-          if (row_ok) {
+    // ------------------------------------------------------------ consumers
+    const int cw = warp - 2, h = cw >> 2, q = warp & 3, hf = q >> 1;
+    const int e = ((q & 1) << 5) | lane;          // edge of TMEM lane 32q + lane
+    const int t = (cw & 3) * 32 + lane;           // thread in the warpgroup
+    const int ey = t >> 1, kh = t & 1;            // Y staging: edge ey, k in [8kh, 8kh + 8)
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + kVBase;
+    uint16_t* yw = Yw + h * kYwgElems;
+    float4* ex = Ex + h * kExchF4;
+    // Y rows of the next tile are prefetched by cp.async into this thread's own
+    // 16-byte chunk of a raw [edge][16] staging row (no registers held across
+    // the tile), then transposed to [k][edge] at the tile start.
+    uint16_t* yraw = Yr + h * kYwgElems + ey * 16 + 8 * kh;
+    auto fetch_y = [&](int64_t tile) {
+      const int64_t b = tile * kEdges + ey;
+      if (tile >= ntiles) return;
+      if (a.y_vec) {
+        cp_async_16(smem_u32(yraw), a.Y + (b < a.batch ? b : 0) * 16 + 8 * kh, b < a.batch ? 16 : 0);
+        cp_async_commit();
+      } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float4 v = has ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
-                                           __uint_as_float(r[4 * e + 2]),
-                                           __uint_as_float(r[4 * e + 3]))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-              if (a.accumulate) {
-                const float4 o = z[c * 4 + e];
-                v.x += o.x;
-                v.y += o.y;
-                v.z += o.z;
-                v.w += o.w;
-              }
-              z[c * 4 + e] = v;
+        for (int qq = 0; qq < 8; ++qq) {
+          const int k = 8 * kh + qq;
+          yraw[qq] = (b < a.batch && k < a.nk)
+                         ? __ldg(reinterpret_cast<const uint16_t*>(a.Y) + b * a.nk + k)
+                         : static_cast<uint16_t>(0);
+        }
+      }
+    };
+    fetch_y(blockIdx.x);
+    uint32_t gc = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      {  // publish this tile's Y as [k][edge] (conflict-free per-lane reads)
+        cp_async_wait<0>();
+        const uint4 yv = *reinterpret_cast<const uint4*>(yraw);
+        const uint32_t w4[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          yw[(8 * kh + qq) * kEdges + ey] = static_cast<uint16_t>(w4[qq >> 1] >> (16 * (qq & 1)));
+      }
+      named_bar_sync(1 + h, 128);
+      fetch_y(tile + gridDim.x);
+      const int64_t b = tile * kEdges + e;
+      for (int P = 0; P < a.npasses; ++P) {
+        const int4 ps = __ldg(&a.pass[P]);
+        const int out_i = static_cast<int16_t>(((h < 2 ? ps.z : ps.w) >> (16 * (h & 1))) & 0xFFFF);
+        float2 acc[4][8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) acc[c][qq] = make_float2(0.f, 0.f);
+        for (int gi = ps.x; gi < ps.x + ps.y; ++gi, ++gc) {
+          const uint32_t vs = gc & 1;
+          const uint32_t r0 = __ldg(&a.refs[gi * 16 + h * 2 + hf]);
+          const uint32_t r1 = __ldg(&a.refs[gi * 16 + 8 + h * 2 + hf]);
+          mbar_wait(&v_full[vs], (gc >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int pi = 0; pi < 2; ++pi) {
+            const uint32_t ref = pi ? r1 : r0;
+            const int cnt = static_cast<int>(ref >> 24);
+            if (cnt == 0) continue;  // warp-uniform
+            const float2* tm = a.terms + (ref & 0xFFFFFF);
+            float coef = 0.f;
+            for (int u = 0; u < cnt; ++u) {
+              const float2 term = __ldg(&tm[u]);
+              const int k = __float_as_int(term.x);
+              coef = fmaf(term.y,
+                          __uint_as_float(static_cast<uint32_t>(yw[k * kEdges + e]) << 16), coef);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t r[16];
+              tmem_ld_32x32b_x16(trow + 128 * vs + 64 * pi + 16 * c, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int qq = 0; qq < 8; ++qq)
+                acc[c][qq] = ffma2(coef, make_float2(__uint_as_float(r[2 * qq]),
+                                                     __uint_as_float(r[2 * qq + 1])),
+                                   acc[c][qq]);
             }
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&v_empty[vs]);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[cp]);
+        if (out_i < 0) continue;  // uniform over the warpgroup
+        // the two rows of the pair meet: half 0 finalises columns [0, 32),
+        // half 1 [32, 64), one 16-column chunk per round
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const float2 g0 = hf ? acc[r][2 * qq] : acc[2 + r][2 * qq];
+            const float2 g1 = hf ? acc[r][2 * qq + 1] : acc[2 + r][2 * qq + 1];
+            ex[(hf * 4 + qq) * kEdges + e] = make_float4(g0.x, g0.y, g1.x, g1.y);
+          }
+          named_bar_sync(1 + h, 128);
+          if (b < a.batch) {
+            float4* z = reinterpret_cast<float4*>(a.Z + (b * a.ni + out_i) * 64 + 16 * (hf ? 2 + r : r));
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const float4 o = ex[((1 - hf) * 4 + qq) * kEdges + e];
+              const float2 k0 = hf ? acc[2 + r][2 * qq] : acc[r][2 * qq];
+              const float2 k1 = hf ? acc[2 + r][2 * qq + 1] : acc[r][2 * qq + 1];
+              float4 v = make_float4(k0.x + o.x, k0.y + o.y, k1.x + o.z, k1.y + o.w);
+              if (a.accumulate) {
+                const float4 old = z[qq];
+                v.x += old.x;
+                v.y += old.y;
+                v.z += old.z;
+                v.w += old.w;
+              }
+              z[qq] = v;
+            }
+          }
+          named_bar_sync(1 + h, 128);
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kMathWarps) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
+
 
 // CUDA-core path: thread per (b, i, w); slots of component i in slot order,
 // u innermost, prod = ((CGV * X) * Y) * W as plan.cpp:588-592.
@@ -422,7 +392,13 @@ struct ixb_tp_plan {
   const int32_t *CGL = nullptr, *CGJ = nullptr, *CGK = nullptr;
   const float* CGV = nullptr;
   bool tc = false;  // shape admits the tensor-core path
-  TpMeta meta{};
+  // tensor-core schedule (TpArgs): one device blob, the counts by value
+  void* d_sched = nullptr;
+  const int4 *pass = nullptr, *grp = nullptr;
+  const uint32_t* refs = nullptr;
+  const float2* terms = nullptr;
+  const int2* wseq = nullptr;
+  int npasses = 0, ngroups = 0, nwseq = 0, pair_mask = 0;
   int32_t* d_rowptr = nullptr;  // CUDA-core path: slots per output component
   int32_t* d_slots = nullptr;
 };
@@ -488,106 +464,107 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
     if (!flat.empty())
       IXB_CUDA_CHECK(cudaMemcpyAsync(plan->d_slots, flat.data(), flat.size() * 4,
                                      cudaMemcpyHostToDevice, s));
-    // tensor-core path: jobs (l, component pair) in (l, cp) order; entries
-    // (j, k, v) of each component in slot order, pads (v == 0) dropped
-    bool tc = !w_per_batch && U == 64 && Wd == 64 && ni <= 16 && nj <= 16 && nk <= 16 && nl >= 1;
+    // tensor-core path: the V-first schedule of one 64-edge tile (tp_tc_kernel)
+    bool tc = !w_per_batch && U == 64 && Wd == 64 && nj <= 2 * kMaxPairs && nk <= 16 &&
+              nl >= 1 && ni <= 32767;
     if (tc) {
-      TpMeta& meta = plan->meta;
-      meta.ni = static_cast<int>(ni);
-      std::vector<std::vector<std::vector<int32_t>>> li(nl, std::vector<std::vector<int32_t>>(ni));
+      // (l, i, j) -> CG terms (k, v) in slot order; pads (v == 0) dropped
+      std::map<std::tuple<int, int, int>, std::vector<std::pair<int, float>>> ent;
       for (int64_t sl = 0; sl < slots; ++sl) {
         if (hv[sl] == 0.f) continue;
-        li[hl[sl / g]][hi[sl]].push_back(static_cast<int32_t>(sl));
+        ent[std::make_tuple(hl[sl / g], hi[sl], hj[sl])].emplace_back(hk[sl], hv[sl]);
       }
-      int njob = 0, nst = 0, nps = 0;
-      std::vector<bool> touched((ni + 1) / 2, false);
-      // paths in order of the highest output component they write (stable):
-      // component pairs then complete one after another within a tile
-      std::vector<int> lorder(nl);
-      std::vector<int> top(nl, -1);
-      for (int l = 0; l < nl; ++l) {
-        lorder[l] = l;
-        for (int i = 0; i < ni; ++i)
-          if (!li[l][i].empty()) top[l] = i;
-      }
-      std::stable_sort(lorder.begin(), lorder.end(), [&](int x, int y) { return top[x] < top[y]; });
-      for (int lo = 0; lo < nl && tc; ++lo) {
-        const int l = lorder[lo];
-        const int first_job = njob;
-        for (int cp = 0; cp < (ni + 1) / 2 && tc; ++cp) {
-          // j-steps: distinct input rows j of the pair (ascending); per step the
-          // k-terms of component 2cp, then of 2cp+1, each in slot order
-          const std::vector<int32_t> none;
-          const std::vector<int32_t>& c0 = 2 * cp < ni ? li[l][2 * cp] : none;
-          const std::vector<int32_t>& c1 = 2 * cp + 1 < ni ? li[l][2 * cp + 1] : none;
-          if (c0.empty() && c1.empty()) continue;
-          if (!c0.empty()) meta.present |= 1 << (2 * cp);
-          if (!c1.empty()) meta.present |= 1 << (2 * cp + 1);
-          const int st0 = nst;
-          for (int j = 0; j < nj && tc; ++j) {
-            std::vector<int32_t> t[2];
-            for (int h = 0; h < 2; ++h)
-              for (int32_t sl : h ? c1 : c0)
-                if (hj[sl] == j) t[h].push_back(sl);
-            for (size_t r = 0; r < t[0].size() || r < t[1].size(); r += 2) {
-              if (nst >= kMaxJSteps) {
-                tc = false;
-                break;
-              }
-              int n[2], kk[2][2] = {{0, 0}, {0, 0}};
-              float vv[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-              for (int h = 0; h < 2; ++h) {
-                n[h] = static_cast<int>(std::min<size_t>(2, t[h].size() > r ? t[h].size() - r : 0));
-                for (int q = 0; q < n[h]; ++q) {
-                  kk[h][q] = hk[t[h][r + q]];
-                  vv[h][q] = hv[t[h][r + q]];
+      std::vector<int4> pass, grp;
+      std::vector<uint32_t> refs;
+      std::vector<float2> terms;
+      std::vector<int2> wseq;
+      uint32_t seen = 0;  // pairs already staged in this tile
+      for (int64_t i0 = 0; i0 < ni && tc; i0 += 4) {
+        int outs[4];
+        for (int h = 0; h < 4; ++h) outs[h] = i0 + h < ni ? static_cast<int>(i0 + h) : -1;
+        // paths feeding this pass and the input-row pairs each needs
+        std::map<int, uint32_t> need;
+        for (const auto& kv : ent) {
+          const int l = std::get<0>(kv.first), i = std::get<1>(kv.first), j = std::get<2>(kv.first);
+          if (i >= i0 && i < i0 + 4) need[l] |= 1u << (j / 2);
+        }
+        // paths with the same pair set side by side, then paired into W slots
+        std::vector<std::pair<uint32_t, int>> order;
+        for (const auto& kv : need) order.emplace_back(kv.second, kv.first);
+        std::sort(order.begin(), order.end());
+        const int g0 = static_cast<int>(grp.size());
+        for (size_t o = 0; o < order.size(); o += 2) {
+          const int la = order[o].second;
+          const int lb = o + 1 < order.size() ? order[o + 1].second : -1;
+          const uint32_t ma = order[o].first, mb = lb >= 0 ? order[o + 1].first : 0u;
+          wseq.push_back(make_int2(la, lb));
+          const int first = static_cast<int>(grp.size());
+          for (int jp = 0; jp < kMaxPairs; ++jp) {
+            const int mask = static_cast<int>(((ma >> jp) & 1) | (((mb >> jp) & 1) << 1));
+            if (!mask) continue;
+            int f = jp | (mask << 4);
+            if (!((seen >> jp) & 1)) f |= 1 << 6;
+            seen |= 1u << jp;
+            grp.push_back(make_int4(f, 0, 0, 0));
+            for (int pi = 0; pi < 2; ++pi)
+              for (int h = 0; h < 4; ++h)
+                for (int hf = 0; hf < 2; ++hf) {
+                  const int l = pi ? lb : la, j = 2 * jp + hf;
+                  uint32_t ref = 0;
+                  if (l >= 0 && outs[h] >= 0 && ((mask >> pi) & 1)) {
+                    auto it = ent.find(std::make_tuple(l, outs[h], j));
+                    if (it != ent.end()) {
+                      if (it->second.size() > 255 || terms.size() >= (1u << 24)) tc = false;
+                      ref = static_cast<uint32_t>(terms.size()) |
+                            (static_cast<uint32_t>(it->second.size()) << 24);
+                      for (const auto& kvp : it->second) {
+                        float kf;
+                        std::memcpy(&kf, &kvp.first, sizeof kf);
+                        terms.push_back(make_float2(kf, kvp.second));
+                      }
+                    }
+                  }
+                  refs.push_back(ref);
                 }
-              }
-              auto bits = [](float f) {
-                int b;
-                std::memcpy(&b, &f, sizeof b);
-                return b;
-              };
-              meta.jstep[nst] = make_int4(j | (n[0] << 4) | (n[1] << 6) | (kk[0][0] << 8) |
-                                              (kk[0][1] << 12) | (kk[1][0] << 16) | (kk[1][1] << 20),
-                                          bits(vv[0][0]), bits(vv[0][1]), bits(vv[1][0]));
-              meta.jv11[nst++] = vv[1][1];
-            }
           }
-          if (!tc) break;
-          if (njob >= kMaxJobs || nps >= kMaxPathSeq) {
-            tc = false;
-            break;
-          }
-          const int ft = touched[cp] ? 0 : 1;
-          touched[cp] = true;
-          const int fp = njob == first_job ? 1 : 0;
-          meta.job[njob] = make_int4(l | (ft << 8) | (fp << 10), cp | (nps << 8),
-                                     st0 | ((nst - st0) << 16), 0);
-          ++njob;
+          grp[first].x |= 1 << 7;
+          grp.back().x |= 1 << 8;
         }
-        if (tc && njob > first_job) {
-          meta.job[njob - 1].x |= 1 << 9;  // last job of this path
-          meta.path_l[nps++] = l;
-        }
+        auto pk = [](int x, int y) {
+          return static_cast<int>((static_cast<uint32_t>(x) & 0xFFFF) |
+                                  ((static_cast<uint32_t>(y) & 0xFFFF) << 16));
+        };
+        pass.push_back(make_int4(g0, static_cast<int>(grp.size()) - g0, pk(outs[0], outs[1]),
+                                 pk(outs[2], outs[3])));
       }
-      meta.njobs = njob;
-      meta.npaths = nps;
-      // last job of each pair -> commit flag; drain order = order of last jobs
-      int last[kPairs];
-      for (int c = 0; c < kPairs; ++c) last[c] = -1;
-      for (int n = 0; n < njob; ++n) last[meta.job[n].y & 0xFF] = n;
-      meta.ncp = 0;
-      for (int n = 0; n < njob; ++n) {
-        const int c = meta.job[n].y & 0xFF;
-        if (last[c] == n) {
-          meta.job[n].x |= 1 << 11;
-          meta.cp_order[meta.ncp++] = c;
-        }
+      if (tc) {
+        if (terms.empty()) terms.push_back(make_float2(0.f, 0.f));
+        if (wseq.empty()) wseq.push_back(make_int2(0, -1));
+        const size_t bp = 0, bg = bp + pass.size() * sizeof(int4),
+                     br = bg + grp.size() * sizeof(int4) + 16,
+                     bt = (br + refs.size() * 4 + 15) / 16 * 16,
+                     bw = bt + terms.size() * sizeof(float2), total = bw + wseq.size() * sizeof(int2);
+        std::vector<char> blob(total, 0);
+        std::memcpy(blob.data() + bp, pass.data(), pass.size() * sizeof(int4));
+        std::memcpy(blob.data() + bg, grp.data(), grp.size() * sizeof(int4));
+        std::memcpy(blob.data() + br, refs.data(), refs.size() * 4);
+        std::memcpy(blob.data() + bt, terms.data(), terms.size() * sizeof(float2));
+        std::memcpy(blob.data() + bw, wseq.data(), wseq.size() * sizeof(int2));
+        IXB_CUDA_CHECK(cudaMalloc(&plan->d_sched, total));
+        IXB_CUDA_CHECK(cudaMemcpyAsync(plan->d_sched, blob.data(), total, cudaMemcpyHostToDevice, s));
+        IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // blob is a host temporary
+        char* d = static_cast<char*>(plan->d_sched);
+        plan->pass = reinterpret_cast<const int4*>(d + bp);
+        plan->grp = reinterpret_cast<const int4*>(d + bg);
+        plan->refs = reinterpret_cast<const uint32_t*>(d + br);
+        plan->terms = reinterpret_cast<const float2*>(d + bt);
+        plan->wseq = reinterpret_cast<const int2*>(d + bw);
+        plan->npasses = static_cast<int>(pass.size());
+        plan->ngroups = static_cast<int>(grp.size());
+        plan->nwseq = static_cast<int>(wseq.size());
+        plan->pair_mask = static_cast<int>(seen);
+        if (grp.empty()) plan->nwseq = 0;
       }
-      int k = meta.ncp;
-      for (int c = 0; c < kPairs; ++c)
-        if (last[c] < 0) meta.cp_order[k++] = c;
     }
     plan->tc = tc;
     *out = plan.release();
@@ -610,17 +587,19 @@ extern "C" int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, 
     if (p.tc && aligned) {
       const CUtensorMap tmW = make_tmap_2d(W, 64, static_cast<uint64_t>(p.nl) * 64, 128, 64, 64,
                                            CU_TENSOR_MAP_SWIZZLE_128B);
-      const CUtensorMap tmX = make_tmap_2d(X, 64, static_cast<uint64_t>(batch) * p.nj, 128, 64,
-                                           256, CU_TENSOR_MAP_SWIZZLE_NONE);
-      TpArgs args{static_cast<const __nv_bfloat16*>(Y), Z, batch, static_cast<int>(p.nj),
-                  static_cast<int>(p.nk), static_cast<int>(p.ni), accumulate};
-      const uint32_t smem =
-          kXTile + kNU * kUSlot + kNW * kWTileTp + 2 * kEdges * 16 * 4 + 256 + 1024;
-      set_max_dynamic_smem(reinterpret_cast<const void*>(tp_tc_kernel), smem,
+      // X viewed as (u, edge, row): a {64, 64, 2} box lands as [row][edge][u]
+      const CUtensorMap tmX = make_tmap_3d(X, 64, static_cast<uint64_t>(batch),
+                                           static_cast<uint64_t>(p.nj), p.nj * 128, 128, 64,
+                                           kEdges, 2, CU_TENSOR_MAP_SWIZZLE_128B);
+      TpArgs args{p.pass, p.grp, p.refs, p.terms, p.wseq, static_cast<const __nv_bfloat16*>(Y), Z,
+                  batch, static_cast<int>(p.nk), static_cast<int>(p.ni), p.npasses, p.ngroups,
+                  p.nwseq, p.pair_mask,
+                  p.nk == 16 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 ? 1 : 0, accumulate};
+      set_max_dynamic_smem(reinterpret_cast<const void*>(tp_tc_kernel), kTpSmem,
                            "cudaFuncSetAttribute(tp_tc_kernel)");
       int64_t grid = ceil_div(batch, kEdges);
       if (grid > sm_count()) grid = sm_count();
-      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, smem, s>>>(tmW, tmX, p.meta, args);
+      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, kTpSmem, s>>>(tmX, tmW, args);
       IXB_LAUNCH_CHECK("tp_tc_kernel");
       return;
     }
@@ -718,6 +697,7 @@ extern "C" void ixb_tp_plan_free(ixb_tp_plan* plan) {
   if (!plan) return;
   cudaFree(plan->d_rowptr);  // synchronous: in-flight runs finish first
   cudaFree(plan->d_slots);
+  cudaFree(plan->d_sched);
   delete plan;
 }
 

@@ -268,3 +268,46 @@ def test_tp_tcgen05_rotation_equivariance(P):
         scale = n0.max().item()
         assert scale > 0
         assert ((n1 - n0).abs().max().item()) <= 2e-2 * scale, l3
+
+
+def tp_fp64_reference(cg, X, Y, W):
+    """Z = sum over CG entries v * Y[:, k] * (X[:, j, :] @ W[l]) in fp64 on the
+    device (the einsum of EXPR_S with '=', summed in float64)."""
+    Xd, Yd, Wd = X.double(), Y.double(), W.double()
+    B = X.shape[0]
+    Z = torch.zeros((B, 16, 64), dtype=torch.float64, device="cuda")
+    g = cg["CGI"].shape[1]
+    for p in range(cg["CGL"].shape[0]):
+        l = int(cg["CGL"][p])
+        for q in range(g):
+            v = float(cg["CGV"][p, q])
+            if v == 0.0:
+                continue
+            i, j, k = int(cg["CGI"][p, q]), int(cg["CGJ"][p, q]), int(cg["CGK"][p, q])
+            Z[:, i, :] += v * Yd[:, k:k + 1] * (Xd[:, j, :] @ Wd[l])
+    return Z
+
+
+@pytest.mark.parametrize("B", [148 * 64 * 2 + 37, 148 * 64 * 5])
+def test_tp_tcgen05_many_tiles_per_cta(P, ixo, B):
+    """Batches of several 64-edge tiles per persistent CTA (ring phases, the
+    next tile's X staged while the current one runs, a ragged last tile) for
+    `=` and `+=`, against an fp64 reference. The tensor cores see only the
+    exact bf16 operands and every sum runs in fp32, so the error is fp32
+    rounding (held to 1e-5 relative, tighter than the 1e-2 bf16 contract)."""
+    cg, nl = cg_grouped(P, ixo, 4)
+    dev = {k: cuda(v, torch.float32 if k == "CGV" else torch.int32) for k, v in cg.items()}
+    plan = P.TpPlan(dev["CGL"], dev["CGI"], dev["CGJ"], dev["CGK"], dev["CGV"], 16, 16, 16, nl)
+    gen = torch.Generator(device="cuda").manual_seed(B)
+    X = torch.randn((B, 16, 64), device="cuda", generator=gen).to(torch.bfloat16)
+    Y = torch.randn((B, 16), device="cuda", generator=gen).to(torch.bfloat16)
+    W = (torch.randn((nl, 64, 64), device="cuda", generator=gen) / 8).to(torch.bfloat16)
+    want = tp_fp64_reference(cg, X, Y, W)
+    Z = torch.full((B, 16, 64), float("nan"), device="cuda")
+    plan.run(X, Y, W, Z, accumulate=False)
+    scale = want.abs().max().item()
+    assert (Z.double() - want).abs().max().item() <= 1e-5 * scale
+    Z0 = torch.randn((B, 16, 64), device="cuda", generator=gen)
+    Z1 = Z0.clone()
+    plan.run(X, Y, W, Z1, accumulate=True)
+    assert (Z1.double() - (want + Z0.double())).abs().max().item() <= 1e-5 * scale
