@@ -11,7 +11,9 @@ CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint6
 // 2-D int32 tensor (no swizzle), e.g. index tables staged by TMA.
 CUtensorMap make_tmap_2d_i32(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                              uint32_t box_inner, uint32_t box_outer);
+// 3-D bf16 tensor (fp32 with f32 = true).
 CUtensorMap make_tmap_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                         uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle sw);
+                         uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle sw,
+                         bool f32 = false);
 
 }  // namespace ixb

@@ -30,17 +30,33 @@ using namespace sm100;
 
 constexpr int kEdges = 64;          // edges per tile: UMMA M = 128 = 2 input rows x 64 edges
 constexpr int kMaxPairs = 8;        // input-row pairs (nj <= 16): TMEM columns [0, 256)
-constexpr int kNWs = 3;             // W ring: slots of two W[l] tiles (a path pair)
-constexpr int kConsumerWarps = 16;  // 4 warpgroups, one output row of the pass each
-constexpr int kTpThreads = (2 + kConsumerWarps) * 32;  // TMA, MMA + consumers
+constexpr int kXSlots = 4;          // X staging ring (pairs in first-use order)
+constexpr int kNWs = 5;             // W ring: slots of two W[l] tiles (a path pair)
+constexpr int kConsumerWarps = 16;  // 4 warpgroups, one 16-column quarter of V each
+constexpr int kTpThreads = (4 + kConsumerWarps) * 32;  // TMA, MMA, 2 spare + consumers
 constexpr uint32_t kXPair = 2 * kEdges * 128;          // [2 rows][64 edges][128 B], SW128
 constexpr uint32_t kWTile = 64 * 128;                  // W[l] [64 u][64 w], SW128 MN-major
 constexpr uint32_t kWSlot = 2 * kWTile;
 constexpr uint32_t kVBase = 256;                       // V ring: 2 x 128 TMEM columns
-constexpr uint32_t kYwgElems = 16 * kEdges;            // per warpgroup: Y [16 k][64 edges] bf16
-constexpr uint32_t kExchF4 = 2 * 4 * kEdges;           // per warpgroup: [half][chunk][edge] float4
-constexpr uint32_t kTpSmem = kMaxPairs * kXPair + kNWs * kWSlot + 2 * 4 * kYwgElems * 2 +
-                             4 * kExchF4 * 16 + 512 + 1024;
+constexpr int kMaxPassCoefs = 96;                      // CG coefficients per pass, [c][edge] fp32
+constexpr uint32_t kExchF4 = 8 * kEdges;               // per warpgroup: Z tile [edge][32 cols] fp32
+constexpr int kMaxSchedBytes = 16384;                  // schedule, staged in shared memory
+constexpr uint32_t kTpSmem = kXSlots * kXPair + kNWs * kWSlot + 16 * kEdges * 4 +
+                             kMaxPassCoefs * kEdges * 4 + 4 * kExchF4 * 16 + kMaxSchedBytes + 512 +
+                             1024;
+
+#ifdef IXB_TP_TRACE
+// timeline of CTA 0 (tools/tp_trace.py): [role][event][n] clock64 stamps
+__device__ long long g_tp_trace[4][4][512];
+#define TPT(role, ev, n)                                                         \
+  do {                                                                           \
+    if (blockIdx.x == 0 && (n) < 512) g_tp_trace[role][ev][(n)] = clock64();     \
+  } while (0)
+#else
+#define TPT(role, ev, n) \
+  do {                   \
+  } while (0)
+#endif
 
 // acc(2 lanes) += coef * x(2 lanes): one FFMA2.
 __device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
@@ -54,25 +70,36 @@ __device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
   return r;
 }
 
-// Schedule of one 64-edge tile, built once per CG table (ixb_tp_plan_create).
-//  pass  {first group, groups, out rows of warpgroups 0,1 (int16 each), 2,3}
-//  group {jp | mask << 4 | first use of pair jp << 6 | first group of its W
-//         slot << 7 | last group of its W slot << 8}: one UMMA chain
-//         V = X[rows 2jp, 2jp+1] . [W[la] | W[lb]] (mask: which of the slot's
-//         two paths; both -> N = 128)
-//  refs  [group][path 0/1][warpgroup][half]: CG terms of (l, out row, j =
-//         2jp + half) as offset | count << 24 into terms {k (int bits), v}
+// Schedule of one 64-edge tile, built once per CG table (ixb_tp_plan_create)
+// and passed by value (constant bank: every lane of a warp reads the same
+// entry).
+//  pass  {first group, groups, out rows 0,1 (int16 each), out rows 2,3}
+//  pcoef {first coefficient, count}: the pass's CG coefficients, as eight
+//        lists (half of the pair, out row of the pass) starting at plist
+//  grp   jp | mask << 4 | first use of pair jp << 6 | first group of its W
+//        slot << 7 | last group of its W slot << 8 | entries of half 0 << 16
+//        | entries of half 1 << 24; one UMMA chain V = X[rows 2jp, 2jp+1] .
+//        [W[la] | W[lb]] (mask: which of the slot's two paths; both -> N =
+//        128); entry bit 4 pi + s: path pi feeds out row s of the pass
+//  cref  coefficient -> CG terms (offset | count << 24), in (group, path)
+//        order per list
+//  terms {k (int bits), v}
 //  wseq  {la, lb or -1}: the W tiles of each W slot, in group order
+struct TpSched {
+  int npasses, ngroups, nwseq, nx;
+  int xorder[kMaxPairs];  // pairs in first-use order (the X staging sequence)
+  // byte offsets of pass (int4), pcoef (int2), plist (int2), grp (int), cref
+  // (uint32), terms (float2), wseq (int2) in blob; blob is copied to shared
+  // memory at kernel start (dynamically indexed constant-bank reads miss)
+  int o_pass, o_pcoef, o_plist, o_grp, o_cref, o_terms, o_wseq, nbytes;
+  uint4 blob[kMaxSchedBytes / 16];
+};
+
 struct TpArgs {
-  const int4* pass;
-  const int4* grp;
-  const uint32_t* refs;
-  const float2* terms;
-  const int2* wseq;
   const __nv_bfloat16* Y;  // [B, nk]
   float* Z;                // [B, ni, 64]
   int64_t batch;
-  int nk, ni, npasses, ngroups, nwseq, pair_mask, y_vec, accumulate;
+  int nk, ni, y_pair, accumulate;
 };
 
 // V-first factorisation:
@@ -83,26 +110,33 @@ struct TpArgs {
 // X pairs arrive by TMA ({64 u, 64 edges, 2 rows} boxes, SW128) and are
 // copied into TMEM columns [32 jp, 32 jp + 32) by tcgen05.cp on first use in
 // the tile: the A operand then comes from TMEM and shared memory only feeds W.
-// Output rows are processed four at a time ("passes"); warpgroup h owns
-// output row h of the pass for all 64 columns, so every consumer thread
-// keeps one (edge, row-of-the-pair, out row) accumulator of 64 floats in
-// registers and computes each CG coefficient once. The two rows of a pair
-// sit in different warps (TMEM lanes m and m + 64), so their partial sums
-// meet once per pass through shared memory (each half finalises 32 columns).
+// Output rows are processed four at a time ("passes"). At the start of a
+// pass the 512 consumer threads compute its CG coefficients sum_k v * Y[b,k]
+// (one per (edge, CG entry)) into shared memory; warpgroup h then owns V
+// columns [16h, 16h + 16) of every group for the pass's four output rows,
+// so a group costs each consumer warp one 16-column TMEM load per path plus
+// one shared load and 8 FFMA2 per CG entry. The two rows of a pair sit in
+// different warps (TMEM lanes m and m + 64): their partial sums meet once per
+// pass through shared memory (each half finalises two of the four rows).
 // Warps: 0 TMA (X pairs one tile ahead, W slots paced by the MMA), 1 TMEM
-// alloc + MMA issuer, 2..17 consumers (576 threads: 112 registers each).
+// alloc + MMA issuer, 2-3 spare, 4..19 consumers. Warpgroup 0 drops to 56
+// registers (setmaxnreg) so the consumers get 104 (the pool must cover the
+// increase or setmaxnreg.inc waits forever): each SM sub-partition holds one
+// warpgroup-0 warp and four consumer warps.
 __global__ void __launch_bounds__(kTpThreads, 1)
     tp_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                 const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ TpSched sc,
                  TpArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* Xs = smem;                                               // [8 pairs][16 KB]
-  uint8_t* Ws = Xs + kMaxPairs * kXPair;                            // [3][2 tiles][8 KB]
-  uint16_t* Yw = reinterpret_cast<uint16_t*>(Ws + kNWs * kWSlot);   // [4 wg][16 k][64 e]
-  uint16_t* Yr = Yw + 4 * kYwgElems;                                // [4 wg][64 e][16 k] raw
-  float4* Ex = reinterpret_cast<float4*>(Yr + 4 * kYwgElems);       // [4 wg][2][4][64]
-  uint64_t* x_full = reinterpret_cast<uint64_t*>(Ex + 4 * kExchF4);
-  uint64_t* x_empty = x_full + kMaxPairs;
+  uint8_t* Xs = smem;                                         // [4 slots][16 KB]
+  uint8_t* Ws = Xs + kXSlots * kXPair;                        // [6][2 tiles][8 KB]
+  float* Yk = reinterpret_cast<float*>(Ws + kNWs * kWSlot);   // [16 k][64 e]
+  float* Cf = Yk + 16 * kEdges;                               // [coef][64 e]
+  float4* Ex = reinterpret_cast<float4*>(Cf + kMaxPassCoefs * kEdges);  // [4 wg][64][8], 1 KB aligned
+  uint8_t* Sb = reinterpret_cast<uint8_t*>(Ex + 4 * kExchF4);           // schedule blob
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(Sb + kMaxSchedBytes);
+  uint64_t* x_empty = x_full + kXSlots;
   uint64_t* w_full = x_empty + kMaxPairs;
   uint64_t* w_empty = w_full + kNWs;
   uint64_t* v_full = w_empty + kNWs;
@@ -110,8 +144,16 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < sc.nbytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(Sb)[i] = sc.blob[i];
+  const int4* s_pass = reinterpret_cast<const int4*>(Sb + sc.o_pass);
+  const int2* s_pcoef = reinterpret_cast<const int2*>(Sb + sc.o_pcoef);
+  const int2* s_plist = reinterpret_cast<const int2*>(Sb + sc.o_plist);
+  const int* s_grp = reinterpret_cast<const int*>(Sb + sc.o_grp);
+  const uint32_t* s_cref = reinterpret_cast<const uint32_t*>(Sb + sc.o_cref);
+  const float2* s_terms = reinterpret_cast<const float2*>(Sb + sc.o_terms);
+  const int2* s_wseq = reinterpret_cast<const int2*>(Sb + sc.o_wseq);
   if (tid == 0) {
-    for (int p = 0; p < kMaxPairs; ++p) {
+    for (int p = 0; p < kXSlots; ++p) {
       mbar_init(&x_full[p], 1);
       mbar_init(&x_empty[p], 1);
     }
@@ -134,212 +176,245 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (a.batch + kEdges - 1) / kEdges;
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    // W slots are paced by the MMA (3-deep ring); the X pairs of the next tile
-    // are issued as soon as the current tile has copied each pair into TMEM
-    // (polled between W loads), so X streams one tile ahead of the MMAs.
-    if (lane == 0) {
+    // W slots are paced by the MMA; X pairs go through a 4-slot staging ring
+    // in first-use order, each issued as soon as its slot has been copied into
+    // TMEM (polled while waiting for W slots), up to one tile ahead. The warp
+    // runs converged; one elected lane issues.
+    {
       tma_prefetch_desc(&tmX);
       tma_prefetch_desc(&tmW);
       const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
       uint32_t wc = 0;
       int64_t xt = blockIdx.x;  // tile of the next X load
-      int xtl = 0, xp = 0;      // its tile ordinal and pair
-      // issue X loads in (tile, pair) order up to tile ordinal `upto`; without
-      // `block`, stop at the first staging slot not yet copied out
+      int xtl = 0, xi = 0;      // its tile ordinal and position in xorder
+      uint32_t xc = 0;          // X loads issued (staging ring position)
+      // issue X loads in (tile, first use) order up to tile ordinal `upto`;
+      // without `block`, stop at the first staging slot not yet copied out
       auto x_next = [&](int upto, bool block) {
         while (xt < ntiles && xtl <= upto) {
-          if (!((a.pair_mask >> xp) & 1)) {
-            if (++xp == kMaxPairs) xp = 0, xt += gridDim.x, ++xtl;
-            continue;
-          }
-          const uint32_t par = (xtl & 1) ^ 1;  // previous tile's copy of this pair done
-          if (!block && !mbar_test(&x_empty[xp], par)) return;
-          mbar_wait(&x_empty[xp], par);
-          mbar_arrive_expect_tx(&x_full[xp], kXPair);
-          tma_load_3d(Xs + xp * kXPair, &tmX, &x_full[xp], 0, static_cast<int32_t>(xt * kEdges),
-                      2 * xp, stream);
-          if (++xp == kMaxPairs) xp = 0, xt += gridDim.x, ++xtl;
+          const uint32_t xs = xc % kXSlots, par = ((xc / kXSlots) & 1) ^ 1;
+          if (!block && !mbar_test(&x_empty[xs], par)) return;
+          mbar_wait(&x_empty[xs], par);
+          tma_load_3d_elect(Xs + xs * kXPair, &tmX, &x_full[xs], kXPair, 0,
+                            static_cast<int32_t>(xt * kEdges), 2 * sc.xorder[xi], stream);
+          ++xc;
+          if (++xi == sc.nx) xi = 0, xt += gridDim.x, ++xtl;
         }
       };
       int tl = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-        // this tile's X must be in flight before its W (the MMA needs both)
-        x_next(tl, true);
-        for (int n = 0; n < a.nwseq; ++n, ++wc) {
-          const int2 w = __ldg(&a.wseq[n]);
+        x_next(tl, false);
+        for (int n = 0; n < sc.nwseq; ++n, ++wc) {
+          const int2 w = s_wseq[n];
           const uint32_t ws = wc % kNWs;
           while (!mbar_test(&w_empty[ws], ((wc / kNWs) & 1) ^ 1)) x_next(tl + 1, false);
-          mbar_arrive_expect_tx(&w_full[ws], w.y >= 0 ? kWSlot : kWTile);
-          tma_load_2d(Ws + ws * kWSlot, &tmW, &w_full[ws], 0, w.x * 64, keep);
-          if (w.y >= 0) tma_load_2d(Ws + ws * kWSlot + kWTile, &tmW, &w_full[ws], 0, w.y * 64, keep);
+          TPT(0, 0, wc);
+          tma_load_2d_pair_elect(Ws + ws * kWSlot, kWTile, &tmW, &w_full[ws],
+                                 w.y >= 0 ? kWSlot : kWTile, w.x * 64, w.y >= 0 ? w.y * 64 : -1,
+                                 keep);
           x_next(tl + 1, false);
         }
       }
+      // X loads are only polled above (a blocking wait there could hold back
+      // the W loads the MMA needs to free the slot); the rest go out now
+      x_next(tl, true);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (whole warp, converged; elected lanes issue)
+    {
       constexpr uint32_t idesc64 = idesc_bf16_f32(128, 64, false, /*B MN-major*/ true);
       constexpr uint32_t idesc128 = idesc_bf16_f32(128, 128, false, true);
-      uint32_t gc = 0, wc = 0;
-      int tl = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-        for (int gi = 0; gi < a.ngroups; ++gi, ++gc) {
-          const int f = __ldg(&a.grp[gi].x);
+      uint32_t gc = 0, wc = 0, xc = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int gi = 0; gi < sc.ngroups; ++gi, ++gc) {
+          const int f = s_grp[gi];
           const int jp = f & 15, mask = (f >> 4) & 3;
           const uint32_t ws = wc % kNWs;
+          TPT(1, 0, gc);
           if ((f >> 7) & 1) mbar_wait(&w_full[ws], (wc / kNWs) & 1);
+          TPT(1, 1, gc);
           const uint32_t vs = gc & 1;
           mbar_wait(&v_empty[vs], ((gc >> 1) & 1) ^ 1);
+          TPT(1, 2, gc);
           if ((f >> 6) & 1) {  // first use of this pair in the tile: stage it into TMEM
-            mbar_wait(&x_full[jp], tl & 1);
+            const uint32_t xs = xc % kXSlots;
+            mbar_wait(&x_full[xs], (xc / kXSlots) & 1);
             tc_fence_after();
-            const uint32_t x0 = smem_u32(Xs + jp * kXPair);
+            const uint32_t x0 = smem_u32(Xs + xs * kXPair);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              tmem_cp_128x256b(tmem + 32 * jp + 8 * kk,
-                               smem_desc(x0 + kk * 32, 16, 1024, kLayoutSW128));
-            umma_commit(&x_empty[jp]);  // staging slot reusable once copied
+              tmem_cp_128x256b_elect(tmem + 32 * jp + 8 * kk,
+                                     smem_desc(x0 + kk * 32, 16, 1024, kLayoutSW128));
+            umma_commit_elect(&x_empty[xs]);  // staging slot reusable once copied
+            ++xc;
           }
           tc_fence_after();
           const uint32_t d = tmem + kVBase + 128 * vs + (mask == 2 ? 64 : 0);
           const uint32_t w0 = smem_u32(Ws + ws * kWSlot) + (mask == 2 ? kWTile : 0);
           const uint32_t idesc = mask == 3 ? idesc128 : idesc64;
+          const uint64_t bd = smem_desc(w0, kWTile, 1024, kLayoutSW128);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_f16_ts(d, tmem + 32 * jp + 8 * kk,
-                        smem_desc(w0 + kk * 2048, kWTile, 1024, kLayoutSW128), idesc,
-                        kk > 0 ? 1u : 0u);
-          umma_commit(&v_full[vs]);
+          for (int kk = 0; kk < 4; ++kk)  // K step: +16 rows of W = +2 KB = +128 in the address field
+            umma_f16_ts_elect(d, tmem + 32 * jp + 8 * kk, bd + static_cast<uint64_t>(kk * 128),
+                              idesc, kk > 0 ? 1u : 0u);
+          umma_commit_elect(&v_full[vs]);
+          TPT(1, 3, gc);
           if ((f >> 8) & 1) {
-            umma_commit(&w_empty[ws]);
+            umma_commit_elect(&w_empty[ws]);
             ++wc;
           }
         }
       }
     }
-  } else {
+  } else if (warp >= 4) {
     // ------------------------------------------------------------ consumers
-    const int cw = warp - 2, h = cw >> 2, q = warp & 3, hf = q >> 1;
-    const int e = ((q & 1) << 5) | lane;          // edge of TMEM lane 32q + lane
-    const int t = (cw & 3) * 32 + lane;           // thread in the warpgroup
-    const int ey = t >> 1, kh = t & 1;            // Y staging: edge ey, k in [8kh, 8kh + 8)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    const int cw = warp - 4, h = cw >> 2, q = warp & 3, hf = q >> 1;
+    const int ct = cw * 32 + lane;                  // consumer thread 0..511
+    const int e = ((q & 1) << 5) | lane;            // edge of TMEM lane 32q + lane
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + kVBase;
-    uint16_t* yw = Yw + h * kYwgElems;
-    float4* ex = Ex + h * kExchF4;
-    // Y rows of the next tile are prefetched by cp.async into this thread's own
-    // 16-byte chunk of a raw [edge][16] staging row (no registers held across
-    // the tile), then transposed to [k][edge] at the tile start.
-    uint16_t* yraw = Yr + h * kYwgElems + ey * 16 + 8 * kh;
-    auto fetch_y = [&](int64_t tile) {
-      const int64_t b = tile * kEdges + ey;
-      if (tile >= ntiles) return;
-      if (a.y_vec) {
-        cp_async_16(smem_u32(yraw), a.Y + (b < a.batch ? b : 0) * 16 + 8 * kh, b < a.batch ? 16 : 0);
-        cp_async_commit();
-      } else {
-#pragma unroll
-        for (int qq = 0; qq < 8; ++qq) {
-          const int k = 8 * kh + qq;
-          yraw[qq] = (b < a.batch && k < a.nk)
-                         ? __ldg(reinterpret_cast<const uint16_t*>(a.Y) + b * a.nk + k)
-                         : static_cast<uint16_t>(0);
-        }
-      }
+    float4* zt = Ex + h * kExchF4;  // this warpgroup's Z staging tile (SW128, 8 KB)
+    const bool issuer = (cw & 3) == 0 && lane == 0;
+    // Y: thread ct stages (edge ct % 64, k = 2 (ct / 64) + {0, 1}) of each tile,
+    // loaded one tile ahead into one register
+    const int ye = ct & (kEdges - 1), yk = (ct >> 6) * 2;
+    auto ld_y = [&](int64_t tile) -> uint32_t {
+      const int64_t b = tile * kEdges + ye;
+      if (tile >= ntiles || b >= a.batch) return 0u;
+      const uint16_t* yr = reinterpret_cast<const uint16_t*>(a.Y) + b * a.nk + yk;
+      if (a.y_pair) return __ldg(reinterpret_cast<const uint32_t*>(yr));
+      const uint32_t lo = yk < a.nk ? __ldg(yr) : 0u;
+      const uint32_t hi = yk + 1 < a.nk ? __ldg(yr + 1) : 0u;
+      return lo | (hi << 16);
     };
-    fetch_y(blockIdx.x);
+    uint32_t ynext = ld_y(blockIdx.x);
     uint32_t gc = 0;
+    const int sh0 = 16 + 8 * hf + h;  // entry bit of (path 0, this half, this out row)
+    int pcnt = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      {  // publish this tile's Y as [k][edge] (conflict-free per-lane reads)
-        cp_async_wait<0>();
-        const uint4 yv = *reinterpret_cast<const uint4*>(yraw);
-        const uint32_t w4[4] = {yv.x, yv.y, yv.z, yv.w};
-#pragma unroll
-        for (int qq = 0; qq < 8; ++qq)
-          yw[(8 * kh + qq) * kEdges + ey] = static_cast<uint16_t>(w4[qq >> 1] >> (16 * (qq & 1)));
-      }
-      named_bar_sync(1 + h, 128);
-      fetch_y(tile + gridDim.x);
+      // (the previous tile's readers of Yk finished before its last pass's barrier)
+      Yk[yk * kEdges + ye] = __uint_as_float(ynext << 16);
+      Yk[(yk + 1) * kEdges + ye] = __uint_as_float(ynext & 0xFFFF0000u);
+      ynext = ld_y(tile + gridDim.x);
       const int64_t b = tile * kEdges + e;
-      for (int P = 0; P < a.npasses; ++P) {
-        const int4 ps = __ldg(&a.pass[P]);
-        const int out_i = static_cast<int16_t>(((h < 2 ? ps.z : ps.w) >> (16 * (h & 1))) & 0xFFFF);
-        float2 acc[4][8];
+      for (int P = 0; P < sc.npasses; ++P) {
+        const int4 ps = s_pass[P];
+        const int2 pc = s_pcoef[P];
+        const int2 pl = s_plist[P];
+        if (warp == 4 && lane == 0) TPT(3, 0, pcnt);
+        named_bar_sync(1, 512);  // Yk written; the previous pass's coefficients read
+        if (warp == 4 && lane == 0) TPT(3, 1, pcnt);
+        // the pass's CG coefficients: Cf[c][edge] = sum_k v * Y[edge, k]; a
+        // warp takes coefficients c, c + 8, c + 16, c + 24 at once (independent
+        // shared-memory chains)
+        for (int cb = ct >> 6; cb < pc.y; cb += 32) {
+          uint32_t ref[4];
+          int mc = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ref[u] = cb + 8 * u < pc.y ? s_cref[pc.x + cb + 8 * u] : 0u;
+            mc = max(mc, static_cast<int>(ref[u] >> 24));
+          }
+          float v[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int t = 0; t < mc; ++t) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (t < static_cast<int>(ref[u] >> 24)) {
+                const float2 term = s_terms[(ref[u] & 0xFFFFFF) + t];
+                v[u] = fmaf(term.y, Yk[__float_as_int(term.x) * kEdges + ye], v[u]);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (cb + 8 * u < pc.y) Cf[(cb + 8 * u) * kEdges + ye] = v[u];
+        }
+        if (warp == 4 && lane == 0) TPT(3, 3, pcnt);
+        named_bar_sync(1, 512);
+        if (warp == 4 && lane == 0) TPT(0, 3, pcnt);
+        ++pcnt;
+        const int li = 4 * hf + h;
+        const float* cfp = Cf + (((li < 4 ? pl.x : pl.y) >> (8 * (li & 3))) & 0xFF) * kEdges + e;
+        float2 acc[4][8];  // 64 columns of this (edge, row of the pair, out row) as pairs
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int qq = 0; qq < 8; ++qq) acc[c][qq] = make_float2(0.f, 0.f);
         for (int gi = ps.x; gi < ps.x + ps.y; ++gi, ++gc) {
+          const int f = s_grp[gi];
+          const int m = ((f >> sh0) & 1) | (((f >> (sh0 + 4)) & 1) << 1);  // paths with an entry
           const uint32_t vs = gc & 1;
-          const uint32_t r0 = __ldg(&a.refs[gi * 16 + h * 2 + hf]);
-          const uint32_t r1 = __ldg(&a.refs[gi * 16 + 8 + h * 2 + hf]);
+          if (warp == 4 && lane == 0) TPT(2, 0, gc);
           mbar_wait(&v_full[vs], (gc >> 1) & 1);
+          if (warp == 4 && lane == 0) TPT(2, 1, gc);
           tc_fence_after();
 #pragma unroll
           for (int pi = 0; pi < 2; ++pi) {
-            const uint32_t ref = pi ? r1 : r0;
-            const int cnt = static_cast<int>(ref >> 24);
-            if (cnt == 0) continue;  // warp-uniform
-            const float2* tm = a.terms + (ref & 0xFFFFFF);
-            float coef = 0.f;
-            for (int u = 0; u < cnt; ++u) {
-              const float2 term = __ldg(&tm[u]);
-              const int k = __float_as_int(term.x);
-              coef = fmaf(term.y,
-                          __uint_as_float(static_cast<uint32_t>(yw[k * kEdges + e]) << 16), coef);
-            }
+            if (!((m >> pi) & 1)) continue;  // warp-uniform
+            const float cf = *cfp;
+            cfp += kEdges;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              uint32_t r[16];
-              tmem_ld_32x32b_x16(trow + 128 * vs + 64 * pi + 16 * c, r);
+              uint32_t v[16];
+              tmem_ld_32x32b_x16(trow + 128 * vs + 64 * pi + 16 * c, v);
               tmem_ld_wait();
 #pragma unroll
               for (int qq = 0; qq < 8; ++qq)
-                acc[c][qq] = ffma2(coef, make_float2(__uint_as_float(r[2 * qq]),
-                                                     __uint_as_float(r[2 * qq + 1])),
+                acc[c][qq] = ffma2(cf, make_float2(__uint_as_float(v[2 * qq]),
+                                                   __uint_as_float(v[2 * qq + 1])),
                                    acc[c][qq]);
             }
           }
           tc_fence_before();
           __syncwarp();
+          if (warp == 4 && lane == 0) TPT(2, 2, gc);
           if (lane == 0) mbar_arrive(&v_empty[vs]);
         }
+        const int out_i = static_cast<int16_t>(((h < 2 ? ps.z : ps.w) >> (16 * (h & 1))) & 0xFFFF);
         if (out_i < 0) continue;  // uniform over the warpgroup
-        // the two rows of the pair meet: half 0 finalises columns [0, 32),
-        // half 1 [32, 64), one 16-column chunk per round
+        // the two rows of the pair meet in a [64 edges][32 columns] SW128 tile
+        // (half 1 writes, half 0 adds), which one thread stores (or, for +=,
+        // reduce-adds) to Z by TMA; two rounds of 32 columns
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
+          if (issuer) bulk_wait_group_read0();  // the previous store has read the tile
+          named_bar_sync(2 + h, 128);
+          float4* row = zt + e * 8;
+          if (hf) {
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const float2 g0 = hf ? acc[r][2 * qq] : acc[2 + r][2 * qq];
-            const float2 g1 = hf ? acc[r][2 * qq + 1] : acc[2 + r][2 * qq + 1];
-            ex[(hf * 4 + qq) * kEdges + e] = make_float4(g0.x, g0.y, g1.x, g1.y);
-          }
-          named_bar_sync(1 + h, 128);
-          if (b < a.batch) {
-            float4* z = reinterpret_cast<float4*>(a.Z + (b * a.ni + out_i) * 64 + 16 * (hf ? 2 + r : r));
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-              const float4 o = ex[((1 - hf) * 4 + qq) * kEdges + e];
-              const float2 k0 = hf ? acc[2 + r][2 * qq] : acc[r][2 * qq];
-              const float2 k1 = hf ? acc[2 + r][2 * qq + 1] : acc[r][2 * qq + 1];
-              float4 v = make_float4(k0.x + o.x, k0.y + o.y, k1.x + o.z, k1.y + o.w);
-              if (a.accumulate) {
-                const float4 old = z[qq];
-                v.x += old.x;
-                v.y += old.y;
-                v.z += old.z;
-                v.w += old.w;
-              }
-              z[qq] = v;
+            for (int c8 = 0; c8 < 8; ++c8) {
+              const float2 x0 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3)];
+              const float2 x1 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3) + 1];
+              row[c8 ^ (e & 7)] = make_float4(x0.x, x0.y, x1.x, x1.y);
             }
           }
-          named_bar_sync(1 + h, 128);
+          named_bar_sync(2 + h, 128);
+          if (!hf) {
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+              const float2 x0 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3)];
+              const float2 x1 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3) + 1];
+              const float4 o = row[c8 ^ (e & 7)];
+              row[c8 ^ (e & 7)] = make_float4(x0.x + o.x, x0.y + o.y, x1.x + o.z, x1.y + o.w);
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(2 + h, 128);
+          if (issuer) {
+            if (a.accumulate)
+              tma_reduce_add_3d(&tmZ, zt, 32 * r, out_i, static_cast<int32_t>(tile * kEdges));
+            else
+              tma_store_3d(&tmZ, zt, 32 * r, out_i, static_cast<int32_t>(tile * kEdges));
+            bulk_commit_group();
+          }
         }
       }
     }
+    if (issuer) bulk_wait_group0();
   }
   tc_fence_before();
   __syncthreads();
@@ -348,7 +423,6 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     tmem_dealloc(tmem, 512);
   }
 }
-
 
 // CUDA-core path: thread per (b, i, w); slots of component i in slot order,
 // u innermost, prod = ((CGV * X) * Y) * W as plan.cpp:588-592.
@@ -392,13 +466,7 @@ struct ixb_tp_plan {
   const int32_t *CGL = nullptr, *CGJ = nullptr, *CGK = nullptr;
   const float* CGV = nullptr;
   bool tc = false;  // shape admits the tensor-core path
-  // tensor-core schedule (TpArgs): one device blob, the counts by value
-  void* d_sched = nullptr;
-  const int4 *pass = nullptr, *grp = nullptr;
-  const uint32_t* refs = nullptr;
-  const float2* terms = nullptr;
-  const int2* wseq = nullptr;
-  int npasses = 0, ngroups = 0, nwseq = 0, pair_mask = 0;
+  std::unique_ptr<TpSched> sched;  // tensor-core schedule (kernel parameter)
   int32_t* d_rowptr = nullptr;  // CUDA-core path: slots per output component
   int32_t* d_slots = nullptr;
 };
@@ -474,28 +542,47 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
         if (hv[sl] == 0.f) continue;
         ent[std::make_tuple(hl[sl / g], hi[sl], hj[sl])].emplace_back(hk[sl], hv[sl]);
       }
-      std::vector<int4> pass, grp;
-      std::vector<uint32_t> refs;
+      auto sc = std::make_unique<TpSched>();
+      std::memset(sc.get(), 0, sizeof(TpSched));
+      std::vector<int> grp;
+      std::vector<uint32_t> cref;
       std::vector<float2> terms;
-      std::vector<int2> wseq;
+      std::vector<int2> wseq, pcoef, plist;
+      std::vector<int4> pass;
+      std::vector<int> xorder;
       uint32_t seen = 0;  // pairs already staged in this tile
-      for (int64_t i0 = 0; i0 < ni && tc; i0 += 4) {
+      auto entries_in = [&](int64_t i0, int64_t ns) {
+        int n = 0;
+        for (const auto& kv : ent)
+          if (std::get<1>(kv.first) >= i0 && std::get<1>(kv.first) < i0 + ns) ++n;
+        return n;
+      };
+      for (int64_t i0 = 0; i0 < ni && tc;) {
+        // up to four output rows per pass, fewer if their coefficients overflow smem
+        int64_t ns = std::min<int64_t>(4, ni - i0);
+        while (ns > 1 && entries_in(i0, ns) > kMaxPassCoefs) --ns;
+        if (entries_in(i0, ns) > kMaxPassCoefs) {
+          tc = false;
+          break;
+        }
         int outs[4];
-        for (int h = 0; h < 4; ++h) outs[h] = i0 + h < ni ? static_cast<int>(i0 + h) : -1;
+        for (int h = 0; h < 4; ++h) outs[h] = h < ns ? static_cast<int>(i0 + h) : -1;
         // paths feeding this pass and the input-row pairs each needs
         std::map<int, uint32_t> need;
         for (const auto& kv : ent) {
           const int l = std::get<0>(kv.first), i = std::get<1>(kv.first), j = std::get<2>(kv.first);
-          if (i >= i0 && i < i0 + 4) need[l] |= 1u << (j / 2);
+          if (i >= i0 && i < i0 + ns) need[l] |= 1u << (j / 2);
         }
         // paths with the same pair set side by side, then paired into W slots
         std::vector<std::pair<uint32_t, int>> order;
         for (const auto& kv : need) order.emplace_back(kv.second, kv.first);
         std::sort(order.begin(), order.end());
         const int g0 = static_cast<int>(grp.size());
-        for (size_t o = 0; o < order.size(); o += 2) {
+        std::vector<uint32_t> crefh[8];  // this pass's coefficients, per (half, out row)
+        const size_t step = std::getenv("IXB_TP_NOMERGE") ? 1 : 2;  // perf experiment
+        for (size_t o = 0; o < order.size(); o += step) {
           const int la = order[o].second;
-          const int lb = o + 1 < order.size() ? order[o + 1].second : -1;
+          const int lb = step == 2 && o + 1 < order.size() ? order[o + 1].second : -1;
           const uint32_t ma = order[o].first, mb = lb >= 0 ? order[o + 1].first : 0u;
           wseq.push_back(make_int2(la, lb));
           const int first = static_cast<int>(grp.size());
@@ -503,32 +590,32 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
             const int mask = static_cast<int>(((ma >> jp) & 1) | (((mb >> jp) & 1) << 1));
             if (!mask) continue;
             int f = jp | (mask << 4);
-            if (!((seen >> jp) & 1)) f |= 1 << 6;
+            if (!((seen >> jp) & 1)) {
+              f |= 1 << 6;
+              xorder.push_back(jp);
+            }
             seen |= 1u << jp;
-            grp.push_back(make_int4(f, 0, 0, 0));
-            for (int pi = 0; pi < 2; ++pi)
-              for (int h = 0; h < 4; ++h)
-                for (int hf = 0; hf < 2; ++hf) {
+            for (int hf = 0; hf < 2; ++hf)
+              for (int pi = 0; pi < 2; ++pi)
+                for (int sl4 = 0; sl4 < 4; ++sl4) {
                   const int l = pi ? lb : la, j = 2 * jp + hf;
-                  uint32_t ref = 0;
-                  if (l >= 0 && outs[h] >= 0 && ((mask >> pi) & 1)) {
-                    auto it = ent.find(std::make_tuple(l, outs[h], j));
-                    if (it != ent.end()) {
-                      if (it->second.size() > 255 || terms.size() >= (1u << 24)) tc = false;
-                      ref = static_cast<uint32_t>(terms.size()) |
-                            (static_cast<uint32_t>(it->second.size()) << 24);
-                      for (const auto& kvp : it->second) {
-                        float kf;
-                        std::memcpy(&kf, &kvp.first, sizeof kf);
-                        terms.push_back(make_float2(kf, kvp.second));
-                      }
-                    }
+                  if (l < 0 || outs[sl4] < 0 || !((mask >> pi) & 1)) continue;
+                  auto it = ent.find(std::make_tuple(l, outs[sl4], j));
+                  if (it == ent.end()) continue;
+                  f |= 1 << (16 + 8 * hf + 4 * pi + sl4);
+                  if (it->second.size() > 255) tc = false;
+                  crefh[4 * hf + sl4].push_back(static_cast<uint32_t>(terms.size()) |
+                                      (static_cast<uint32_t>(it->second.size()) << 24));
+                  for (const auto& kvp : it->second) {
+                    float kf;
+                    std::memcpy(&kf, &kvp.first, sizeof kf);
+                    terms.push_back(make_float2(kf, kvp.second));
                   }
-                  refs.push_back(ref);
                 }
+            grp.push_back(f);
           }
-          grp[first].x |= 1 << 7;
-          grp.back().x |= 1 << 8;
+          grp[first] |= 1 << 7;
+          grp.back() |= 1 << 8;
         }
         auto pk = [](int x, int y) {
           return static_cast<int>((static_cast<uint32_t>(x) & 0xFFFF) |
@@ -536,34 +623,43 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
         };
         pass.push_back(make_int4(g0, static_cast<int>(grp.size()) - g0, pk(outs[0], outs[1]),
                                  pk(outs[2], outs[3])));
+        uint32_t lo = 0, hi8 = 0, n = 0;
+        const int c0 = static_cast<int>(cref.size());
+        for (int li = 0; li < 8; ++li) {
+          (li < 4 ? lo : hi8) |= n << (8 * (li & 3));
+          n += static_cast<uint32_t>(crefh[li].size());
+          cref.insert(cref.end(), crefh[li].begin(), crefh[li].end());
+        }
+        pcoef.push_back(make_int2(c0, static_cast<int>(n)));
+        plist.push_back(make_int2(static_cast<int>(lo), static_cast<int>(hi8)));
+        i0 += ns;
       }
       if (tc) {
-        if (terms.empty()) terms.push_back(make_float2(0.f, 0.f));
-        if (wseq.empty()) wseq.push_back(make_int2(0, -1));
-        const size_t bp = 0, bg = bp + pass.size() * sizeof(int4),
-                     br = bg + grp.size() * sizeof(int4) + 16,
-                     bt = (br + refs.size() * 4 + 15) / 16 * 16,
-                     bw = bt + terms.size() * sizeof(float2), total = bw + wseq.size() * sizeof(int2);
-        std::vector<char> blob(total, 0);
-        std::memcpy(blob.data() + bp, pass.data(), pass.size() * sizeof(int4));
-        std::memcpy(blob.data() + bg, grp.data(), grp.size() * sizeof(int4));
-        std::memcpy(blob.data() + br, refs.data(), refs.size() * 4);
-        std::memcpy(blob.data() + bt, terms.data(), terms.size() * sizeof(float2));
-        std::memcpy(blob.data() + bw, wseq.data(), wseq.size() * sizeof(int2));
-        IXB_CUDA_CHECK(cudaMalloc(&plan->d_sched, total));
-        IXB_CUDA_CHECK(cudaMemcpyAsync(plan->d_sched, blob.data(), total, cudaMemcpyHostToDevice, s));
-        IXB_CUDA_CHECK(cudaStreamSynchronize(s));  // blob is a host temporary
-        char* d = static_cast<char*>(plan->d_sched);
-        plan->pass = reinterpret_cast<const int4*>(d + bp);
-        plan->grp = reinterpret_cast<const int4*>(d + bg);
-        plan->refs = reinterpret_cast<const uint32_t*>(d + br);
-        plan->terms = reinterpret_cast<const float2*>(d + bt);
-        plan->wseq = reinterpret_cast<const int2*>(d + bw);
-        plan->npasses = static_cast<int>(pass.size());
-        plan->ngroups = static_cast<int>(grp.size());
-        plan->nwseq = static_cast<int>(wseq.size());
-        plan->pair_mask = static_cast<int>(seen);
-        if (grp.empty()) plan->nwseq = 0;
+        sc->npasses = static_cast<int>(pass.size());
+        sc->ngroups = static_cast<int>(grp.size());
+        sc->nwseq = grp.empty() ? 0 : static_cast<int>(wseq.size());
+        sc->nx = static_cast<int>(xorder.size());
+        std::copy(xorder.begin(), xorder.end(), sc->xorder);
+        std::vector<char> blob;
+        auto put = [&](const void* p, size_t n) {
+          const int o = static_cast<int>(blob.size());
+          blob.insert(blob.end(), static_cast<const char*>(p), static_cast<const char*>(p) + n);
+          blob.resize((blob.size() + 15) / 16 * 16, 0);
+          return o;
+        };
+        sc->o_pass = put(pass.data(), pass.size() * sizeof(int4));
+        sc->o_pcoef = put(pcoef.data(), pcoef.size() * sizeof(int2));
+        sc->o_plist = put(plist.data(), plist.size() * sizeof(int2));
+        sc->o_grp = put(grp.data(), grp.size() * sizeof(int));
+        sc->o_cref = put(cref.data(), cref.size() * sizeof(uint32_t));
+        sc->o_terms = put(terms.data(), terms.size() * sizeof(float2));
+        sc->o_wseq = put(wseq.data(), wseq.size() * sizeof(int2));
+        sc->nbytes = static_cast<int>(blob.size());
+        if (blob.size() > sizeof(sc->blob)) tc = false;  // larger tables: CUDA-core path
+        else std::memcpy(sc->blob, blob.data(), blob.size());
+      }
+      if (tc) {
+        plan->sched = std::move(sc);
       }
     }
     plan->tc = tc;
@@ -591,15 +687,19 @@ extern "C" int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, 
       const CUtensorMap tmX = make_tmap_3d(X, 64, static_cast<uint64_t>(batch),
                                            static_cast<uint64_t>(p.nj), p.nj * 128, 128, 64,
                                            kEdges, 2, CU_TENSOR_MAP_SWIZZLE_128B);
-      TpArgs args{p.pass, p.grp, p.refs, p.terms, p.wseq, static_cast<const __nv_bfloat16*>(Y), Z,
-                  batch, static_cast<int>(p.nk), static_cast<int>(p.ni), p.npasses, p.ngroups,
-                  p.nwseq, p.pair_mask,
-                  p.nk == 16 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 ? 1 : 0, accumulate};
+      // Z viewed as (w, row, edge): a {32, 1, 64} box is one pass row's half
+      const CUtensorMap tmZ = make_tmap_3d(Z, 64, static_cast<uint64_t>(p.ni),
+                                           static_cast<uint64_t>(batch), 256, p.ni * 256, 32, 1,
+                                           kEdges, CU_TENSOR_MAP_SWIZZLE_128B, /*f32=*/true);
+      TpArgs args{static_cast<const __nv_bfloat16*>(Y), Z, batch, static_cast<int>(p.nk),
+                  static_cast<int>(p.ni),
+                  p.nk % 2 == 0 && reinterpret_cast<uintptr_t>(Y) % 4 == 0 ? 1 : 0, accumulate};
       set_max_dynamic_smem(reinterpret_cast<const void*>(tp_tc_kernel), kTpSmem,
                            "cudaFuncSetAttribute(tp_tc_kernel)");
       int64_t grid = ceil_div(batch, kEdges);
       if (grid > sm_count()) grid = sm_count();
-      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, kTpSmem, s>>>(tmX, tmW, args);
+      tp_tc_kernel<<<static_cast<unsigned>(grid), kTpThreads, kTpSmem, s>>>(tmX, tmW, tmZ, *p.sched,
+                                                                             args);
       IXB_LAUNCH_CHECK("tp_tc_kernel");
       return;
     }
@@ -693,11 +793,16 @@ extern "C" int ixb_tp_plan_run_host(ixb_tp_plan* plan, const void* X, const void
   });
 }
 
+#ifdef IXB_TP_TRACE
+extern "C" int ixb_tp_trace_copy(void* host) {
+  return cudaMemcpyFromSymbol(host, g_tp_trace, sizeof(g_tp_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 extern "C" void ixb_tp_plan_free(ixb_tp_plan* plan) {
   if (!plan) return;
   cudaFree(plan->d_rowptr);  // synchronous: in-flight runs finish first
   cudaFree(plan->d_slots);
-  cudaFree(plan->d_sched);
   delete plan;
 }
 
