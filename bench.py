@@ -430,13 +430,16 @@ class TensorProductWorkload:
         self.flops = 2.0 * 99 * 64 * 64 * B  # factorised form (sum over paths of 2*l3+1 = 99)
         self.alg_bytes = B * (16 * 64 * 2 + 16 * 2 + 16 * 64 * 4) + nl * 64 * 64 * 2
         self.dram_bytes = self.alg_bytes
-        # L2 -> SM: X/Y/Z once + W[l] (8 KB) per (path, component-pair) job per 64-edge tile
-        self.l2_bytes = self.alg_bytes + math.ceil(B / 64) * 61 * 64 * 64 * 2
+        # L2 -> SM: X/Y/Z once + W[l] (8 KB) per (pass, path) of the V-first schedule per
+        # 64-edge tile (36 for the l_max = 3 table: 4 passes of 4 output rows)
+        self.l2_bytes = self.alg_bytes + math.ceil(B / 64) * 36 * 64 * 64 * 2
         self.tc_flops = self.flops
         self.info = {"paths": nl, "cg_nnz": int(cg["v"].numel()), "G": gt.num_groups(), "g": g,
                      "plan_ms": plan_ms,
-                     "formulation": "output-side factorised: 99 (path, component) products per "
-                                    "edge as 61 (path, component-pair) UMMA jobs, M=128"}
+                     "formulation": "V-first: V[b,l,j,:] = X[b,j,:].W[l] on tcgen05 (99 (path, "
+                                    "input component) products per edge, M=128 = 2 input rows x "
+                                    "64 edges, A staged into TMEM by tcgen05.cp), Z = sum of "
+                                    "(CG . Y) * V on CUDA cores in fp32"}
         self.h_in = [self.X.cpu().pin_memory(), self.Y.cpu().pin_memory()]
         self.h_out = torch.empty_like(self.Z, device="cpu").pin_memory()
         self.d_in = [torch.empty_like(x, device=dev) for x in self.h_in]
