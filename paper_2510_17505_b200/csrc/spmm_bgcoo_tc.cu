@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
           for (int b = 0; b < SPS; ++b) kk[b] = __shfl_sync(0xffffffffu, k, (t + b) & 31);
           const int stage = static_cast<int>(bc % STAGES);
           const uint32_t phase = static_cast<uint32_t>((bc / STAGES) & 1);
-          if (lane == 0) {
-            mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one_sync()) {
             uint8_t* st = tiles + stage * L::kStageBytes;
             mbar_arrive_expect_tx(&full[stage], nb * L::kBBytes + SPS * kAvBytes);
 #pragma unroll
@@ -345,34 +345,33 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
       pop(j, sg, tile);
       if (sg.x < 0) break;
       const int buf = j % NACC;
-      if (lane == 0) {
-        mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + buf * kAccCols + sub * 16;
-        const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
-        // same (32-slot chunk, SPS batch) partition as the producers
-        for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
-          const int cnt = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
-          for (int t = 0; t < cnt; t += SPS, ++bc) {
-            const int nb = cnt - t < SPS ? cnt - t : SPS;
-            const int stage = static_cast<int>(bc % STAGES);
-            mbar_wait(&full[stage], static_cast<uint32_t>((bc / STAGES) & 1));
-            tc_fence_after();
-            const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
+      // the whole warp walks the batches; one elected lane issues
+      mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + buf * kAccCols + sub * 16;
+      const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
+      // same (32-slot chunk, SPS batch) partition as the producers
+      for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
+        const int cnt = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
+        for (int t = 0; t < cnt; t += SPS, ++bc) {
+          const int nb = cnt - t < SPS ? cnt - t : SPS;
+          const int stage = static_cast<int>(bc % STAGES);
+          mbar_wait(&full[stage], static_cast<uint32_t>((bc / STAGES) & 1));
+          tc_fence_after();
+          const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
 #pragma unroll
-            for (int b = 0; b < SPS; ++b) {
-              if (b >= nb) break;
-              const uint64_t bdesc =
-                  smem_desc(st + SPS * L::kBBytes + b * kAvBytes, 16, 256, kLayoutSW32);
-              // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
-              const uint64_t adesc =
-                  smem_desc(st + b * L::kBBytes + sub * kSubBytes, 2048, 1024, kLayoutSW128);
-              umma_f16(d, adesc, bdesc, idesc, (i0 + t + b) > 0 ? 1u : 0u);
-            }
-            umma_commit(&empty[stage]);  // stage reusable once these UMMAs retire
-            if (i0 + t + nb == nslots) umma_commit(&acc_full[buf]);
-            if (sub == 0) { K4TR_FIRST(6); K4TR(7); K4TR_SET(12, bc + 1); }
+          for (int b = 0; b < SPS; ++b) {
+            if (b >= nb) break;
+            const uint64_t bdesc =
+                smem_desc(st + SPS * L::kBBytes + b * kAvBytes, 16, 256, kLayoutSW32);
+            // A: MN atoms (64 n) at +2048, K groups of 8 rows at +1024
+            const uint64_t adesc =
+                smem_desc(st + b * L::kBBytes + sub * kSubBytes, 2048, 1024, kLayoutSW128);
+            umma_f16_elect(d, adesc, bdesc, idesc, (i0 + t + b) > 0 ? 1u : 0u);
           }
+          umma_commit_elect(&empty[stage]);  // stage reusable once these UMMAs retire
+          if (i0 + t + nb == nslots) umma_commit_elect(&acc_full[buf]);
+          if (sub == 0 && lane == 0) { K4TR_FIRST(6); K4TR(7); K4TR_SET(12, bc + 1); }
         }
       }
       __syncwarp();
