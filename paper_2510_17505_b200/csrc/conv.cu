@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
       const __nv_bfloat16* src = a.In + static_cast<int64_t>(yy > 0 ? yy - 1 : 0) * 64 + chunk * 8;
       cp_async_16(awarp + r * 128 + ((chunk ^ (r & 7)) << 4), src, yy > 0 ? 16u : 0u);
     }
-    if (tid == 0) {
+    if (warp == 0 && elect_one_sync()) {
       mbar_arrive_expect_tx(&w_full[st], kWTile);
       tma_load_2d(W + st * kWTile, &tmW, &w_full[st], 0, z * 64, keep);
     }
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
     cp_async_wait<kUnitDist - 1>();  // this thread's rows of stage k have landed
     fence_proxy_async_smem();        // cp.async (generic proxy) -> tensor core
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {  // whole warp, one elected lane issues
       mbar_wait(&w_full[st], (k / kUnitStages) & 1);
       tc_fence_after();
       const uint32_t a0 = smem_u32(A + st * kATile), w0 = smem_u32(W + st * kWTile);
@@ -375,9 +375,9 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t ad = smem_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
         const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
-        umma_f16(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+        umma_f16_elect(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
       }
-      umma_commit(&mma_done[st]);
+      umma_commit_elect(&mma_done[st]);
     }
     if (k + kUnitDist < nk) {
       // stage k + D reuses the slot of stage k + D - S: wait for its MMAs
