@@ -24,6 +24,7 @@
 // epilogue of segment j overlaps the main loop of segment j+1.
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <cstdlib>
 #include <mutex>
 
@@ -252,19 +253,37 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
            make_int4(tile, owner_cta(a.G, nc, rs), owner_cta(a.G, nc, re - 1),
                      rs < lo || re > hi));
     };
+    // The two boundary segments come from 32-position windows around lo and
+    // hi, loaded together (one dependent round trip instead of a chain of
+    // ballot scans; the scans remain the fallback for longer runs).
+    const int64_t w0 = lo - 32 + lane, w1 = lo + lane, w2 = hi - 32 + lane, w3 = hi + lane;
+    const int a0 = w0 >= 0 ? __ldg(a.AM + w0) : INT_MIN;
+    const int a1 = w1 < a.G ? __ldg(a.AM + w1) : INT_MAX;
+    const int a2 = w2 >= 0 ? __ldg(a.AM + w2) : INT_MIN;
+    const int a3 = w3 < a.G ? __ldg(a.AM + w3) : INT_MAX;
+    const int row0 = __shfl_sync(0xffffffffu, a1, 0);
+    int64_t rs0, re0;
+    {
+      const unsigned mb = __ballot_sync(0xffffffffu, a0 != row0);
+      rs0 = mb ? lo - 32 + (32 - __clz(mb)) : run_start(a.AM, lo - 32, row0);
+      const unsigned ma = __ballot_sync(0xffffffffu, lane >= 1 && a1 != row0);
+      re0 = ma ? lo + __ffs(ma) - 1 : run_end(a.AM, lo + 32, a.G, row0);
+    }
+    const int64_t e0 = re0 < hi ? re0 : hi;
+    int64_t ts = -1, te = -1;  // trailing segment [ts, hi) of a row continuing past hi
+    const int rowt = __shfl_sync(0xffffffffu, a2, 31);
+    if (e0 < hi && hi < a.G && __shfl_sync(0xffffffffu, a3, 0) == rowt) {
+      const unsigned mb = __ballot_sync(0xffffffffu, a2 != rowt);
+      ts = mb ? hi - 32 + (32 - __clz(mb)) : run_start(a.AM, hi - 32, rowt);
+      const unsigned ma = __ballot_sync(0xffffffffu, lane >= 1 && a3 != rowt);
+      te = ma ? hi + __ffs(ma) - 1 : run_end(a.AM, hi + 32, a.G, rowt);
+    }
     for (int tile = 0; tile < a.ntiles; ++tile) {
-      const int row0 = __ldg(a.AM + lo);
-      const int64_t rs0 = run_start(a.AM, lo, row0), re0 = run_end(a.AM, lo + 1, a.G, row0);
-      const int64_t e0 = re0 < hi ? re0 : hi;
       seg(tile, lo, e0, row0, rs0, re0);
       int64_t mid_end = hi;
-      if (e0 < hi && hi < a.G) {
-        const int rowt = __ldg(a.AM + hi - 1);
-        if (__ldg(a.AM + hi) == rowt) {  // the last row of the range continues past hi
-          const int64_t ts = run_start(a.AM, hi - 1, rowt);
-          seg(tile, ts, hi, rowt, ts, run_end(a.AM, hi + 1, a.G, rowt));
-          mid_end = ts;
-        }
+      if (ts >= 0) {
+        seg(tile, ts, hi, rowt, ts, te);
+        mid_end = ts;
       }
       for (int64_t p = e0; p < mid_end;) {
         const int row = __ldg(a.AM + p);
@@ -580,6 +599,7 @@ void launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmAV, TcArgs a, cudaSt
   }
   a.ntiles = static_cast<int>(a.N / (128 * NSUB));
   int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // every CTA resident
+  if (const char* w = std::getenv("IXB_K4_WAVES")) grid *= std::atoi(w);  // perf experiment
   if (grid > a.G) grid = a.G;
   a.rowctr = work_counters(s, static_cast<size_t>(grid) * a.ntiles);
   const size_t part_n = static_cast<size_t>(grid) * 2 * 16 * a.N;
