@@ -91,7 +91,8 @@ struct TpSched {
   // byte offsets of pass (int4), pcoef (int2), plist (int2), grp (int), cref
   // (uint32), terms (float2), wseq (int2) in blob; blob is copied to shared
   // memory at kernel start (dynamically indexed constant-bank reads miss)
-  int o_pass, o_pcoef, o_plist, o_grp, o_cref, o_terms, o_wseq, nbytes;
+  int o_pass, o_pcoef, o_plist, o_grp, o_cref, o_terms, o_wseq, o_crec, nbytes;
+  int two_terms;  // every coefficient has <= 2 CG terms: crec {k0, v0, k1, v1} per coefficient
   uint4 blob[kMaxSchedBytes / 16];
 };
 
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   const uint32_t* s_cref = reinterpret_cast<const uint32_t*>(Sb + sc.o_cref);
   const float2* s_terms = reinterpret_cast<const float2*>(Sb + sc.o_terms);
   const int2* s_wseq = reinterpret_cast<const int2*>(Sb + sc.o_wseq);
+  const float4* s_crec = reinterpret_cast<const float4*>(Sb + sc.o_crec);
   if (tid == 0) {
     for (int p = 0; p < kXSlots; ++p) {
       mbar_init(&x_full[p], 1);
@@ -300,42 +302,48 @@ __global__ void __launch_bounds__(kTpThreads, 1)
       Yk[yk * kEdges + ye] = __uint_as_float(ynext << 16);
       Yk[(yk + 1) * kEdges + ye] = __uint_as_float(ynext & 0xFFFF0000u);
       ynext = ld_y(tile + gridDim.x);
-      const int64_t b = tile * kEdges + e;
-      for (int P = 0; P < sc.npasses; ++P) {
-        const int4 ps = s_pass[P];
-        const int2 pc = s_pcoef[P];
-        const int2 pl = s_plist[P];
-        if (warp == 4 && lane == 0) TPT(3, 0, pcnt);
-        named_bar_sync(1, 512);  // Yk written; the previous pass's coefficients read
-        if (warp == 4 && lane == 0) TPT(3, 1, pcnt);
-        // the pass's CG coefficients: Cf[c][edge] = sum_k v * Y[edge, k]; a
-        // warp takes coefficients c, c + 8, c + 16, c + 24 at once (independent
-        // shared-memory chains)
-        for (int cb = ct >> 6; cb < pc.y; cb += 32) {
-          uint32_t ref[4];
-          int mc = 0;
+      // the pass's CG coefficients: Cf[c][edge] = sum_k v * Y[edge, k]. Records
+      // of at most two terms ({k0, v0, k1, v1}) take the unrolled path: a warp
+      // computes coefficients c, c + 8, c + 16, c + 24 with all loads in flight.
+      auto coefs = [&](int Pn) {
+        const int2 pc = s_pcoef[Pn];
+        if (sc.two_terms) {
+          for (int cb = ct >> 6; cb < pc.y; cb += 32) {
+            float4 rec[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            ref[u] = cb + 8 * u < pc.y ? s_cref[pc.x + cb + 8 * u] : 0u;
-            mc = max(mc, static_cast<int>(ref[u] >> 24));
-          }
-          float v[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int t = 0; t < mc; ++t) {
+            for (int u = 0; u < 4; ++u)
+              rec[u] = cb + 8 * u < pc.y ? s_crec[pc.x + cb + 8 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              if (t < static_cast<int>(ref[u] >> 24)) {
-                const float2 term = s_terms[(ref[u] & 0xFFFFFF) + t];
-                v[u] = fmaf(term.y, Yk[__float_as_int(term.x) * kEdges + ye], v[u]);
-              }
+              const float y0 = Yk[__float_as_int(rec[u].x) * kEdges + ye];
+              const float y1 = Yk[__float_as_int(rec[u].z) * kEdges + ye];
+              if (cb + 8 * u < pc.y) Cf[(cb + 8 * u) * kEdges + ye] = fmaf(rec[u].w, y1, rec[u].y * y0);
             }
           }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (cb + 8 * u < pc.y) Cf[(cb + 8 * u) * kEdges + ye] = v[u];
+          return;
         }
-        if (warp == 4 && lane == 0) TPT(3, 3, pcnt);
-        named_bar_sync(1, 512);
-        if (warp == 4 && lane == 0) TPT(0, 3, pcnt);
+        for (int c = ct >> 6; c < pc.y; c += 8) {
+          const uint32_t ref = s_cref[pc.x + c];
+          float v = 0.f;
+          for (int t = 0; t < static_cast<int>(ref >> 24); ++t) {
+            const float2 term = s_terms[(ref & 0xFFFFFF) + t];
+            v = fmaf(term.y, Yk[__float_as_int(term.x) * kEdges + ye], v);
+          }
+          Cf[c * kEdges + ye] = v;
+        }
+      };
+      for (int P = 0; P < sc.npasses; ++P) {
+        const int4 ps = s_pass[P];
+        const int2 pl = s_plist[P];
+        if (P == 0) {  // later passes' coefficients are computed inside the previous exchange
+          if (warp == 4 && lane == 0) TPT(3, 0, pcnt);
+          named_bar_sync(1, 512);  // Yk written; the previous pass's coefficients read
+          if (warp == 4 && lane == 0) TPT(3, 1, pcnt);
+          coefs(0);
+          if (warp == 4 && lane == 0) TPT(3, 3, pcnt);
+          named_bar_sync(1, 512);
+          if (warp == 4 && lane == 0) TPT(0, 3, pcnt);
+        }
         ++pcnt;
         const int li = 4 * hf + h;
         const float* cfp = Cf + (((li < 4 ? pl.x : pl.y) >> (8 * (li & 3))) & 0xFF) * kEdges + e;
@@ -375,13 +383,22 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           if (lane == 0) mbar_arrive(&v_empty[vs]);
         }
         const int out_i = static_cast<int16_t>(((h < 2 ? ps.z : ps.w) >> (16 * (h & 1))) & 0xFFFF);
-        if (out_i < 0) continue;  // uniform over the warpgroup
-        // the two rows of the pair meet in a [64 edges][32 columns] SW128 tile
+        // The two rows of the pair meet in a [64 edges][32 columns] SW128 tile
         // (half 1 writes, half 0 adds), which one thread stores (or, for +=,
-        // reduce-adds) to Z by TMA; two rounds of 32 columns
+        // reduce-adds) to Z by TMA; two rounds of 32 columns. The next pass's
+        // coefficients are computed between the rounds, while the TMA store of
+        // round 0 reads the tile.
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
+          if (r == 1 && P + 1 < sc.npasses) {
+            named_bar_sync(1, 512);  // every warpgroup is past this pass's groups
+            coefs(P + 1);
+            named_bar_sync(1, 512);
+          }
+          if (out_i < 0) continue;  // uniform over the warpgroup
+          if (warp == 4 && lane == 0) TPT(r ? 0 : 3, 2, pcnt);  // round start
           if (issuer) bulk_wait_group_read0();  // the previous store has read the tile
+          if (warp == 4 && lane == 0 && r == 1) TPT(0, 1, pcnt);
           named_bar_sync(2 + h, 128);
           float4* row = zt + e * 8;
           if (hf) {
@@ -654,6 +671,17 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
         sc->o_cref = put(cref.data(), cref.size() * sizeof(uint32_t));
         sc->o_terms = put(terms.data(), terms.size() * sizeof(float2));
         sc->o_wseq = put(wseq.data(), wseq.size() * sizeof(int2));
+        // fixed two-term records for the unrolled coefficient path
+        std::vector<float4> crec(cref.size());
+        sc->two_terms = 1;
+        for (size_t c = 0; c < cref.size(); ++c) {
+          const uint32_t cnt = cref[c] >> 24, off = cref[c] & 0xFFFFFF;
+          if (cnt > 2) sc->two_terms = 0;
+          float4 r = make_float4(terms[off].x, terms[off].y, terms[off].x, 0.f);
+          if (cnt > 1) r.z = terms[off + 1].x, r.w = terms[off + 1].y;
+          crec[c] = r;
+        }
+        sc->o_crec = put(crec.data(), crec.size() * sizeof(float4));
         sc->nbytes = static_cast<int>(blob.size());
         if (blob.size() > sizeof(sc->blob)) tc = false;  // larger tables: CUDA-core path
         else std::memcpy(sc->blob, blob.data(), blob.size());
