@@ -259,6 +259,33 @@ __device__ __forceinline__ void umma_f16_ts_elect(uint32_t d_tmem, uint32_t a_tm
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One K = 64 chain D (+)= A[tmem] . B[smem] as 4 UMMAs of K = 16 (A columns
+// +8, B descriptor start +2 KB per step: 16 rows of a 128-byte-row MN-major
+// tile), then a commit to `bar`, all by one elected lane.
+__device__ __forceinline__ void umma_ts_k64_commit_elect(uint32_t d_tmem, uint32_t a_tmem,
+                                                         uint64_t b_desc, uint32_t idesc,
+                                                         uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      ".reg .b64 b1, b2, b3;\n"
+      ".reg .b32 a1, a2, a3;\n"
+      "add.u64 b1, %2, 128;\n"
+      "add.u64 b2, %2, 256;\n"
+      "add.u64 b3, %2, 384;\n"
+      "add.u32 a1, %1, 8;\n"
+      "add.u32 a2, %1, 16;\n"
+      "add.u32 a3, %1, 24;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_cp_128x256b_elect(uint32_t taddr, uint64_t sdesc) {
   asm volatile(
       "{\n"

@@ -259,11 +259,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           const uint32_t w0 = smem_u32(Ws + ws * kWSlot) + (mask == 2 ? kWTile : 0);
           const uint32_t idesc = mask == 3 ? idesc128 : idesc64;
           const uint64_t bd = smem_desc(w0, kWTile, 1024, kLayoutSW128);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K step: +16 rows of W = +2 KB = +128 in the address field
-            umma_f16_ts_elect(d, tmem + 32 * jp + 8 * kk, bd + static_cast<uint64_t>(kk * 128),
-                              idesc, kk > 0 ? 1u : 0u);
-          umma_commit_elect(&v_full[vs]);
+          umma_ts_k64_commit_elect(d, tmem + 32 * jp, bd, idesc, &v_full[vs]);
           TPT(1, 3, gc);
           if ((f >> 8) & 1) {
             umma_commit_elect(&w_empty[ws]);
