@@ -371,13 +371,9 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
       mbar_wait(&w_full[st], (k / kUnitStages) & 1);
       tc_fence_after();
       const uint32_t a0 = smem_u32(A + st * kATile), w0 = smem_u32(W + st * kWTile);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t ad = smem_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
-        const uint64_t bd = smem_desc(w0 + kk * 2048, 8192, 1024, kLayoutSW128);
-        umma_f16_elect(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
-      }
-      umma_commit_elect(&mma_done[st]);
+      umma_ss_k64_commit_elect(tmem, smem_desc(a0, 16, 1024, kLayoutSW128),
+                               smem_desc(w0, 8192, 1024, kLayoutSW128), idesc, k > 0 ? 1u : 0u,
+                               &mma_done[st]);
     }
     if (k + kUnitDist < nk) {
       // stage k + D reuses the slot of stage k + D - S: wait for its MMAs

@@ -286,6 +286,32 @@ __device__ __forceinline__ void umma_ts_k64_commit_elect(uint32_t d_tmem, uint32
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(smem_u32(bar))
       : "memory");
 }
+// Same for A in shared memory (K-major SW128: +32 B per K step = +2 in the
+// descriptor's address field), accumulating onto D when `acc0` is set.
+__device__ __forceinline__ void umma_ss_k64_commit_elect(uint32_t d_tmem, uint64_t a_desc,
+                                                         uint64_t b_desc, uint32_t idesc,
+                                                         uint32_t acc0, uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "add.u64 a1, %1, 2;\n"
+      "add.u64 a2, %1, 4;\n"
+      "add.u64 a3, %1, 6;\n"
+      "add.u64 b1, %2, 128;\n"
+      "add.u64 b2, %2, 256;\n"
+      "add.u64 b3, %2, 384;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc0), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_cp_128x256b_elect(uint32_t taddr, uint64_t sdesc) {
   asm volatile(
       "{\n"
