@@ -187,7 +187,9 @@ int ixb_spmm_blockgroupcoo(const int32_t* AM, const int32_t* AK, const void* AV,
 /* K5 — submanifold 3x3x3 kernel map over n voxels (coords [n,3] int32,
  * unique). Pairs (out i, in j, offset z) with coord[j] == coord[i] + delta(z),
  * z = (dx+1)*9 + (dy+1)*3 + (dz+1), ordered by (z, i) — the canonical order
- * of group_coo_tensor(map, 2, g) input. */
+ * of group_coo_tensor(map, 2, g) input. The plan counts the pairs (one
+ * device->host read); pack writes them and reads `coords` again, so coords
+ * must stay valid until pack. */
 typedef struct ixb_kmap ixb_kmap;
 int ixb_kernel_map_plan(const int32_t* coords, int64_t n, ixb_stream stream, ixb_kmap** plan,
                         int64_t* num_pairs);
