@@ -264,6 +264,15 @@ def _check_shape(name, t, shape):
         raise BindError(3, f"tensor {name} shape does not match the statement")
 
 
+def device_tolerance(expr):
+    """Relative tolerance of the b200 result against the fp64 oracle (north_star;
+    integration/ixsum_b200_mode.cpp device_tolerance): GroupCOO / COO SpMM run
+    fp32 end to end (compensated sums) -> 1e-5; the tensor-core paths take
+    bf16 operands with fp32 accumulation -> 1e-2."""
+    wl, _ = match_workload(parse(expr))
+    return 1e-5 if wl in ("groupcoo_spmm", "coo_spmm") else 1e-2
+
+
 def execute_mode(mode, expr, tensors, out_name, out, value_dtype=None, device=None,
                  flags=0):
     """execute_mode("b200", ...) over host or device tensors.

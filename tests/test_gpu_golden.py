@@ -4,6 +4,7 @@ execute_mode("b200", ...), and the BASELINE config slabs through the device
 builders + kernels. Integer-valued fixtures must match bit-for-bit."""
 import glob
 import os
+import zlib
 
 import numpy as np
 import pytest
@@ -33,7 +34,35 @@ def test_corpus_through_execute_mode(P, ixo, path):
     if want.dtype == np.int64:
         np.testing.assert_array_equal(mo.result.astype(np.int64), want)
     else:
-        assert ixo.max_rel_error(want, mo.result) <= 1e-2
+        assert ixo.max_rel_error(want, mo.result) <= P.device_tolerance(str(d["expr"]))
+
+
+@pytest.mark.parametrize("path", CORPUS, ids=[os.path.basename(p) for p in CORPUS])
+def test_corpus_real_values_at_device_tolerance(P, ixo, path):
+    """The corpus specs with real values (seeded, rounded to the device's value
+    dtype first) against the fp64 oracle at the per-path tolerance: 1e-5 for
+    the fp32 GroupCOO / COO SpMM, 1e-2 for bf16 operands."""
+    d = np.load(path)
+    expr = str(d["expr"])
+    tol = P.device_tolerance(expr)
+    fp32 = tol < 1e-3
+    rng = np.random.default_rng(zlib.crc32(os.path.basename(path).encode()))
+    idx = {"AM", "AK", "MAPX", "MAPY", "MAPZ", "CGL", "CGI", "CGJ", "CGK"}
+    tensors = {}
+    for k in d.files:
+        if not k.startswith("t_"):
+            continue
+        name, v = k[2:], d[k]
+        if name in idx:
+            tensors[name] = v
+            continue
+        r = rng.uniform(-1.0, 1.0, v.shape) * (v != 0 if name in ("AV", "CGV", "MAPV") else 1)
+        dt = torch.float32 if fp32 or name in ("CGV", "MAPV") else torch.bfloat16
+        tensors[name] = torch.from_numpy(r).to(dt).double().numpy()
+    out = rng.uniform(-1.0, 1.0, np.asarray(d["out"]).shape)
+    want = ixo.einsum(expr, tensors, str(d["out_name"]), out)
+    mo = P.execute_mode("b200", expr, tensors, str(d["out_name"]), out)
+    assert ixo.max_rel_error(want, mo.result) <= tol
 
 
 @pytest.mark.parametrize("tag,kind", [("real", 0), ("int", 1)])
