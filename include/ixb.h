@@ -250,6 +250,9 @@ int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const int32_t* CG
 int ixb_tp_plan_run(ixb_tp_plan* plan, const void* X, const void* Y, const void* W, int64_t batch,
                     float* Z, int accumulate, int flags, ixb_stream stream);
 void ixb_tp_plan_free(ixb_tp_plan* plan);
+/* 1 if the plan runs on the tensor-core (V-first) kernel, 0 if its shape or
+ * table size sends it to the CUDA-core kernel. */
+int ixb_tp_plan_uses_tensor_cores(const ixb_tp_plan* plan);
 /* Host-buffer form of ixb_tp_plan_run: X [batch, nj, U] bf16, Y [batch, nk]
  * bf16 and Z [batch, ni, Wd] fp32 are HOST arrays (pinned for overlap), W a
  * device array. The batch is cut into `nchunks` runs of whole 64-edge tiles

@@ -403,6 +403,11 @@ class TpPlan:
                                        g, int(w_per_batch), ni, nj, nk, nl, U, Wd, flags,
                                        _stream(stream), C.byref(self.h)))
 
+    @property
+    def uses_tensor_cores(self):
+        """True when the table runs on the V-first tcgen05 kernel."""
+        return bool(lib().ixb_tp_plan_uses_tensor_cores(self.h))
+
     def _check(self, X, Y, W, Z, host):
         if X.dim() != 3:
             raise ShapeError(4, f"TpPlan: X is [batch, {self.nj}, {self.U}]")

@@ -31,7 +31,7 @@ using namespace sm100;
 constexpr int kEdges = 64;          // edges per tile: UMMA M = 128 = 2 input rows x 64 edges
 constexpr int kMaxPairs = 8;        // input-row pairs (nj <= 16): TMEM columns [0, 256)
 constexpr int kXSlots = 4;          // X staging ring (pairs in first-use order)
-constexpr int kNWs = 5;             // W ring: slots of two W[l] tiles (a path pair)
+constexpr int kNWs = 3;             // W ring: slots of two W[l] tiles (a path pair)
 constexpr int kConsumerWarps = 16;  // 4 warpgroups, one 16-column quarter of V each
 constexpr int kTpThreads = (4 + kConsumerWarps) * 32;  // TMA, MMA, 2 spare + consumers
 constexpr uint32_t kXPair = 2 * kEdges * 128;          // [2 rows][64 edges][128 B], SW128
@@ -39,8 +39,8 @@ constexpr uint32_t kWTile = 64 * 128;                  // W[l] [64 u][64 w], SW1
 constexpr uint32_t kWSlot = 2 * kWTile;
 constexpr uint32_t kVBase = 256;                       // V ring: 2 x 128 TMEM columns
 constexpr int kMaxPassCoefs = 96;                      // CG coefficients per pass, [c][edge] fp32
-constexpr uint32_t kExchF4 = 8 * kEdges;               // per warpgroup: Z tile [edge][32 cols] fp32
-constexpr int kMaxSchedBytes = 16384;                  // schedule, staged in shared memory
+constexpr uint32_t kExchF4 = 16 * kEdges;              // per warpgroup: Z tiles [2][edge][32 cols] fp32
+constexpr int kMaxSchedBytes = 12288;                  // schedule, staged in shared memory
 constexpr uint32_t kTpSmem = kXSlots * kXPair + kNWs * kWSlot + 16 * kEdges * 4 +
                              kMaxPassCoefs * kEdges * 4 + 4 * kExchF4 * 16 + kMaxSchedBytes + 512 +
                              1024;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     const int ct = cw * 32 + lane;                  // consumer thread 0..511
     const int e = ((q & 1) << 5) | lane;            // edge of TMEM lane 32q + lane
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + kVBase;
-    float4* zt = Ex + h * kExchF4;  // this warpgroup's Z staging tile (SW128, 8 KB)
+    float4* zt = Ex + h * kExchF4;  // this warpgroup's Z staging tiles (2 x SW128, 8 KB each)
     const bool issuer = (cw & 3) == 0 && lane == 0;
     // Y: thread ct stages (edge ct % 64, k = 2 (ct / 64) + {0, 1}) of each tile,
     // loaded one tile ahead into one register
@@ -379,51 +379,53 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           if (lane == 0) mbar_arrive(&v_empty[vs]);
         }
         const int out_i = static_cast<int16_t>(((h < 2 ? ps.z : ps.w) >> (16 * (h & 1))) & 0xFFFF);
-        // The two rows of the pair meet in a [64 edges][32 columns] SW128 tile
-        // (half 1 writes, half 0 adds), which one thread stores (or, for +=,
-        // reduce-adds) to Z by TMA; two rounds of 32 columns. The next pass's
-        // coefficients are computed between the rounds, while the TMA store of
-        // round 0 reads the tile.
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          if (r == 1 && P + 1 < sc.npasses) {
-            named_bar_sync(1, 512);  // every warpgroup is past this pass's groups
-            coefs(P + 1);
-            named_bar_sync(1, 512);
-          }
-          if (out_i < 0) continue;  // uniform over the warpgroup
-          if (warp == 4 && lane == 0) TPT(r ? 0 : 3, 2, pcnt);  // round start
-          if (issuer) bulk_wait_group_read0();  // the previous store has read the tile
-          if (warp == 4 && lane == 0 && r == 1) TPT(0, 1, pcnt);
+        // The two rows of the pair meet in two [64 edges][32 columns] SW128
+        // tiles (half 1 writes, half 0 adds), which one thread stores (or,
+        // for +=, reduce-adds) to Z by TMA. The tiles were read by the
+        // previous pass's stores long ago; the next pass's coefficients are
+        // computed while these stores read them.
+        if (out_i >= 0) {
+          if (issuer) bulk_wait_group_read0();
           named_bar_sync(2 + h, 128);
-          float4* row = zt + e * 8;
           if (hf) {
 #pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) {
-              const float2 x0 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3)];
-              const float2 x1 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3) + 1];
-              row[c8 ^ (e & 7)] = make_float4(x0.x, x0.y, x1.x, x1.y);
+            for (int c16 = 0; c16 < 16; ++c16) {  // 16-byte chunk c16 of the 64 columns
+              const float2 x0 = acc[c16 >> 2][2 * (c16 & 3)];
+              const float2 x1 = acc[c16 >> 2][2 * (c16 & 3) + 1];
+              zt[(c16 >> 3) * 512 + e * 8 + ((c16 & 7) ^ (e & 7))] =
+                  make_float4(x0.x, x0.y, x1.x, x1.y);
             }
           }
           named_bar_sync(2 + h, 128);
           if (!hf) {
 #pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) {
-              const float2 x0 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3)];
-              const float2 x1 = acc[2 * r + (c8 >> 2)][2 * (c8 & 3) + 1];
-              const float4 o = row[c8 ^ (e & 7)];
-              row[c8 ^ (e & 7)] = make_float4(x0.x + o.x, x0.y + o.y, x1.x + o.z, x1.y + o.w);
+            for (int c16 = 0; c16 < 16; ++c16) {
+              const float2 x0 = acc[c16 >> 2][2 * (c16 & 3)];
+              const float2 x1 = acc[c16 >> 2][2 * (c16 & 3) + 1];
+              float4* t = zt + (c16 >> 3) * 512 + e * 8 + ((c16 & 7) ^ (e & 7));
+              const float4 o = *t;
+              *t = make_float4(x0.x + o.x, x0.y + o.y, x1.x + o.z, x1.y + o.w);
             }
           }
           fence_proxy_async_smem();
           named_bar_sync(2 + h, 128);
           if (issuer) {
-            if (a.accumulate)
-              tma_reduce_add_3d(&tmZ, zt, 32 * r, out_i, static_cast<int32_t>(tile * kEdges));
-            else
-              tma_store_3d(&tmZ, zt, 32 * r, out_i, static_cast<int32_t>(tile * kEdges));
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              if (a.accumulate)
+                tma_reduce_add_3d(&tmZ, zt + half * 512, 32 * half, out_i,
+                                  static_cast<int32_t>(tile * kEdges));
+              else
+                tma_store_3d(&tmZ, zt + half * 512, 32 * half, out_i,
+                             static_cast<int32_t>(tile * kEdges));
+            }
             bulk_commit_group();
           }
+        }
+        if (P + 1 < sc.npasses) {
+          named_bar_sync(1, 512);  // every warpgroup is past this pass's groups
+          coefs(P + 1);
+          named_bar_sync(1, 512);
         }
       }
     }
@@ -822,6 +824,10 @@ extern "C" int ixb_tp_trace_copy(void* host) {
   return cudaMemcpyFromSymbol(host, g_tp_trace, sizeof(g_tp_trace)) == cudaSuccess ? 0 : 1;
 }
 #endif
+
+extern "C" int ixb_tp_plan_uses_tensor_cores(const ixb_tp_plan* plan) {
+  return plan && plan->tc ? 1 : 0;
+}
 
 extern "C" void ixb_tp_plan_free(ixb_tp_plan* plan) {
   if (!plan) return;

@@ -298,6 +298,7 @@ def test_tp_tcgen05_many_tiles_per_cta(P, ixo, B):
     cg, nl = cg_grouped(P, ixo, 4)
     dev = {k: cuda(v, torch.float32 if k == "CGV" else torch.int32) for k, v in cg.items()}
     plan = P.TpPlan(dev["CGL"], dev["CGI"], dev["CGJ"], dev["CGK"], dev["CGV"], 16, 16, 16, nl)
+    assert plan.uses_tensor_cores  # the l_max = 3 schedule fits the kernel's shared memory
     gen = torch.Generator(device="cuda").manual_seed(B)
     X = torch.randn((B, 16, 64), device="cuda", generator=gen).to(torch.bfloat16)
     Y = torch.randn((B, 16), device="cuda", generator=gen).to(torch.bfloat16)
