@@ -38,11 +38,11 @@ constexpr uint32_t kXPair = 2 * kEdges * 128;          // [2 rows][64 edges][128
 constexpr uint32_t kWTile = 64 * 128;                  // W[l] [64 u][64 w], SW128 MN-major
 constexpr uint32_t kWSlot = 2 * kWTile;
 constexpr uint32_t kVBase = 256;                       // V ring: 2 x 128 TMEM columns
-constexpr int kMaxPassCoefs = 96;                      // CG coefficients per pass, [c][edge] fp32
+constexpr int kMaxWgCoefs = 32;                        // CG coefficients per (pass, out row), [c][edge]
 constexpr uint32_t kExchF4 = 16 * kEdges;              // per warpgroup: Z tiles [2][edge][32 cols] fp32
 constexpr int kMaxSchedBytes = 12288;                  // schedule, staged in shared memory
 constexpr uint32_t kTpSmem = kXSlots * kXPair + kNWs * kWSlot + 16 * kEdges * 4 +
-                             kMaxPassCoefs * kEdges * 4 + 4 * kExchF4 * 16 + kMaxSchedBytes + 512 +
+                             4 * kMaxWgCoefs * kEdges * 4 + 4 * kExchF4 * 16 + kMaxSchedBytes + 512 +
                              1024;
 
 #ifdef IXB_TP_TRACE
@@ -74,8 +74,9 @@ __device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
 // and passed by value (constant bank: every lane of a warp reads the same
 // entry).
 //  pass  {first group, groups, out rows 0,1 (int16 each), out rows 2,3}
-//  pcoef {first coefficient, count}: the pass's CG coefficients, as eight
-//        lists (half of the pair, out row of the pass) starting at plist
+//  pwg   [pass][out row h] {first coefficient, n0 | n1 << 16}: warpgroup
+//        h's coefficients for the pass, n0 for rows 2jp of the pairs, then n1
+//        for rows 2jp + 1
 //  grp   jp | mask << 4 | first use of pair jp << 6 | first group of its W
 //        slot << 7 | last group of its W slot << 8 | entries of half 0 << 16
 //        | entries of half 1 << 24; one UMMA chain V = X[rows 2jp, 2jp+1] .
@@ -88,10 +89,10 @@ __device__ __forceinline__ float2 ffma2(float coef, float2 x, float2 acc) {
 struct TpSched {
   int npasses, ngroups, nwseq, nx;
   int xorder[kMaxPairs];  // pairs in first-use order (the X staging sequence)
-  // byte offsets of pass (int4), pcoef (int2), plist (int2), grp (int), cref
+  // byte offsets of pass (int4), pwg (int2), grp (int), cref
   // (uint32), terms (float2), wseq (int2) in blob; blob is copied to shared
   // memory at kernel start (dynamically indexed constant-bank reads miss)
-  int o_pass, o_pcoef, o_plist, o_grp, o_cref, o_terms, o_wseq, o_crec, nbytes;
+  int o_pass, o_pwg, o_grp, o_cref, o_terms, o_wseq, o_crec, nbytes;
   int two_terms;  // every coefficient has <= 2 CG terms: crec {k0, v0, k1, v1} per coefficient
   uint4 blob[kMaxSchedBytes / 16];
 };
@@ -133,8 +134,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   uint8_t* Xs = smem;                                         // [4 slots][16 KB]
   uint8_t* Ws = Xs + kXSlots * kXPair;                        // [6][2 tiles][8 KB]
   float* Yk = reinterpret_cast<float*>(Ws + kNWs * kWSlot);   // [16 k][64 e]
-  float* Cf = Yk + 16 * kEdges;                               // [coef][64 e]
-  float4* Ex = reinterpret_cast<float4*>(Cf + kMaxPassCoefs * kEdges);  // [4 wg][64][8], 1 KB aligned
+  float* Cf = Yk + 16 * kEdges;                               // [4 wg][coef][64 e]
+  float4* Ex = reinterpret_cast<float4*>(Cf + 4 * kMaxWgCoefs * kEdges);  // [4 wg][2][64][8]
   uint8_t* Sb = reinterpret_cast<uint8_t*>(Ex + 4 * kExchF4);           // schedule blob
   uint64_t* x_full = reinterpret_cast<uint64_t*>(Sb + kMaxSchedBytes);
   uint64_t* x_empty = x_full + kXSlots;
@@ -147,8 +148,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < sc.nbytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(Sb)[i] = sc.blob[i];
   const int4* s_pass = reinterpret_cast<const int4*>(Sb + sc.o_pass);
-  const int2* s_pcoef = reinterpret_cast<const int2*>(Sb + sc.o_pcoef);
-  const int2* s_plist = reinterpret_cast<const int2*>(Sb + sc.o_plist);
+  const int2* s_pwg = reinterpret_cast<const int2*>(Sb + sc.o_pwg);
   const int* s_grp = reinterpret_cast<const int*>(Sb + sc.o_grp);
   const uint32_t* s_cref = reinterpret_cast<const uint32_t*>(Sb + sc.o_cref);
   const float2* s_terms = reinterpret_cast<const float2*>(Sb + sc.o_terms);
@@ -294,55 +294,52 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     const int sh0 = 16 + 8 * hf + h;  // entry bit of (path 0, this half, this out row)
     int pcnt = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      // (the previous tile's readers of Yk finished before its last pass's barrier)
+      named_bar_sync(1, 512);  // every warpgroup is done with the previous tile's Yk
       Yk[yk * kEdges + ye] = __uint_as_float(ynext << 16);
       Yk[(yk + 1) * kEdges + ye] = __uint_as_float(ynext & 0xFFFF0000u);
       ynext = ld_y(tile + gridDim.x);
-      // the pass's CG coefficients: Cf[c][edge] = sum_k v * Y[edge, k]. Records
-      // of at most two terms ({k0, v0, k1, v1}) take the unrolled path: a warp
-      // computes coefficients c, c + 8, c + 16, c + 24 with all loads in flight.
+      // This warpgroup's CG coefficients for pass Pn (its out row, both rows
+      // of the pairs): Cf_h[c][edge] = sum_k v * Y[edge, k], computed by the
+      // warpgroup alone (no cross-warpgroup barrier). Records of at most two
+      // terms take the unrolled path, four coefficients in flight per thread.
+      float* cfw = Cf + h * kMaxWgCoefs * kEdges;
+      const int wt = (cw & 3) * 32 + lane, wte = wt & 63;
       auto coefs = [&](int Pn) {
-        const int2 pc = s_pcoef[Pn];
+        const int2 pw = s_pwg[Pn * 4 + h];
+        const int n = (pw.y & 0xFFFF) + (pw.y >> 16);
         if (sc.two_terms) {
-          for (int cb = ct >> 6; cb < pc.y; cb += 32) {
+          for (int cb = wt >> 6; cb < n; cb += 8) {
             float4 rec[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              rec[u] = cb + 8 * u < pc.y ? s_crec[pc.x + cb + 8 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+              rec[u] = cb + 2 * u < n ? s_crec[pw.x + cb + 2 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float y0 = Yk[__float_as_int(rec[u].x) * kEdges + ye];
-              const float y1 = Yk[__float_as_int(rec[u].z) * kEdges + ye];
-              if (cb + 8 * u < pc.y) Cf[(cb + 8 * u) * kEdges + ye] = fmaf(rec[u].w, y1, rec[u].y * y0);
+              const float y0 = Yk[__float_as_int(rec[u].x) * kEdges + wte];
+              const float y1 = Yk[__float_as_int(rec[u].z) * kEdges + wte];
+              if (cb + 2 * u < n) cfw[(cb + 2 * u) * kEdges + wte] = fmaf(rec[u].w, y1, rec[u].y * y0);
             }
           }
           return;
         }
-        for (int c = ct >> 6; c < pc.y; c += 8) {
-          const uint32_t ref = s_cref[pc.x + c];
+        for (int c = wt >> 6; c < n; c += 2) {
+          const uint32_t ref = s_cref[pw.x + c];
           float v = 0.f;
           for (int t = 0; t < static_cast<int>(ref >> 24); ++t) {
             const float2 term = s_terms[(ref & 0xFFFFFF) + t];
-            v = fmaf(term.y, Yk[__float_as_int(term.x) * kEdges + ye], v);
+            v = fmaf(term.y, Yk[__float_as_int(term.x) * kEdges + wte], v);
           }
-          Cf[c * kEdges + ye] = v;
+          cfw[c * kEdges + wte] = v;
         }
       };
+      named_bar_sync(1, 512);  // Yk written (read only by coefficient passes of this tile)
+      coefs(0);
+      named_bar_sync(2 + h, 128);
       for (int P = 0; P < sc.npasses; ++P) {
         const int4 ps = s_pass[P];
-        const int2 pl = s_plist[P];
-        if (P == 0) {  // later passes' coefficients are computed inside the previous exchange
-          if (warp == 4 && lane == 0) TPT(3, 0, pcnt);
-          named_bar_sync(1, 512);  // Yk written; the previous pass's coefficients read
-          if (warp == 4 && lane == 0) TPT(3, 1, pcnt);
-          coefs(0);
-          if (warp == 4 && lane == 0) TPT(3, 3, pcnt);
-          named_bar_sync(1, 512);
-          if (warp == 4 && lane == 0) TPT(0, 3, pcnt);
-        }
         ++pcnt;
-        const int li = 4 * hf + h;
-        const float* cfp = Cf + (((li < 4 ? pl.x : pl.y) >> (8 * (li & 3))) & 0xFF) * kEdges + e;
+        const int2 pw = s_pwg[P * 4 + h];
+        const float* cfp = cfw + (hf ? (pw.y & 0xFFFF) : 0) * kEdges + e;
         float2 acc[4][8];  // 64 columns of this (edge, row of the pair, out row) as pairs
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -423,9 +420,9 @@ __global__ void __launch_bounds__(kTpThreads, 1)
           }
         }
         if (P + 1 < sc.npasses) {
-          named_bar_sync(1, 512);  // every warpgroup is past this pass's groups
+          if (out_i < 0) named_bar_sync(2 + h, 128);  // (the exchange's barriers order it otherwise)
           coefs(P + 1);
-          named_bar_sync(1, 512);
+          named_bar_sync(2 + h, 128);
         }
       }
     }
@@ -562,24 +559,13 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
       std::vector<int> grp;
       std::vector<uint32_t> cref;
       std::vector<float2> terms;
-      std::vector<int2> wseq, pcoef, plist;
+      std::vector<int2> wseq, pwg;
       std::vector<int4> pass;
       std::vector<int> xorder;
       uint32_t seen = 0;  // pairs already staged in this tile
-      auto entries_in = [&](int64_t i0, int64_t ns) {
-        int n = 0;
-        for (const auto& kv : ent)
-          if (std::get<1>(kv.first) >= i0 && std::get<1>(kv.first) < i0 + ns) ++n;
-        return n;
-      };
       for (int64_t i0 = 0; i0 < ni && tc;) {
         // up to four output rows per pass, fewer if their coefficients overflow smem
-        int64_t ns = std::min<int64_t>(4, ni - i0);
-        while (ns > 1 && entries_in(i0, ns) > kMaxPassCoefs) --ns;
-        if (entries_in(i0, ns) > kMaxPassCoefs) {
-          tc = false;
-          break;
-        }
+        const int64_t ns = std::min<int64_t>(4, ni - i0);  // one out row per warpgroup
         int outs[4];
         for (int h = 0; h < 4; ++h) outs[h] = h < ns ? static_cast<int>(i0 + h) : -1;
         // paths feeding this pass and the input-row pairs each needs
@@ -638,15 +624,14 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
         };
         pass.push_back(make_int4(g0, static_cast<int>(grp.size()) - g0, pk(outs[0], outs[1]),
                                  pk(outs[2], outs[3])));
-        uint32_t lo = 0, hi8 = 0, n = 0;
-        const int c0 = static_cast<int>(cref.size());
-        for (int li = 0; li < 8; ++li) {
-          (li < 4 ? lo : hi8) |= n << (8 * (li & 3));
-          n += static_cast<uint32_t>(crefh[li].size());
-          cref.insert(cref.end(), crefh[li].begin(), crefh[li].end());
+        for (int h = 0; h < 4; ++h) {  // warpgroup h: its out row's lists, half 0 then half 1
+          const size_t n0 = crefh[h].size(), n1 = crefh[4 + h].size();
+          if (n0 + n1 > static_cast<size_t>(kMaxWgCoefs)) tc = false;
+          pwg.push_back(make_int2(static_cast<int>(cref.size()),
+                                  static_cast<int>(n0 | (n1 << 16))));
+          cref.insert(cref.end(), crefh[h].begin(), crefh[h].end());
+          cref.insert(cref.end(), crefh[4 + h].begin(), crefh[4 + h].end());
         }
-        pcoef.push_back(make_int2(c0, static_cast<int>(n)));
-        plist.push_back(make_int2(static_cast<int>(lo), static_cast<int>(hi8)));
         i0 += ns;
       }
       if (tc) {
@@ -663,8 +648,7 @@ extern "C" int ixb_tp_plan_create(const int32_t* CGL, const int32_t* CGI, const 
           return o;
         };
         sc->o_pass = put(pass.data(), pass.size() * sizeof(int4));
-        sc->o_pcoef = put(pcoef.data(), pcoef.size() * sizeof(int2));
-        sc->o_plist = put(plist.data(), plist.size() * sizeof(int2));
+        sc->o_pwg = put(pwg.data(), pwg.size() * sizeof(int2));
         sc->o_grp = put(grp.data(), grp.size() * sizeof(int));
         sc->o_cref = put(cref.data(), cref.size() * sizeof(uint32_t));
         sc->o_terms = put(terms.data(), terms.size() * sizeof(float2));
