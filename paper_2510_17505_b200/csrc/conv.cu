@@ -290,7 +290,8 @@ constexpr int kUnitDist = IXB_CONV_DIST;
 constexpr uint32_t kUnitSmem = kUnitStages * (kATile + kWTile) + 1024 + 256;
 
 __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
-    conv_unit_kernel(const __grid_constant__ CUtensorMap tmW, UnitArgs a) {
+    conv_unit_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
+                     UnitArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* A = smem;                         // [kUnitStages][16 KB]
@@ -387,36 +388,42 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
     mbar_wait(&mma_done[(nk - 1) % kUnitStages], ((nk - 1) / kUnitStages) & 1);
     tc_fence_after();
   }
-  const int k = nk;
-  float4* o = reinterpret_cast<float4*>(a.Out + x * 64);
+  // Epilogue: the tile goes out by TMA store (reduce-add for +=) through the
+  // A stages, free once the last MMA has completed: two [128 rows][32 cols]
+  // SW128 halves, thread = row (rows past n_out are clipped by the TMA).
+  float4* ot = reinterpret_cast<float4*>(A);
 #pragma unroll 1
   for (int c = 0; c < 4; ++c) {
     uint32_t r[16];
-    if (k > 0) {
+    if (nk > 0) {
       tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, r);
       tmem_ld_wait();
     } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) r[j] = 0;
     }
-    if (row_ok) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-        if (a.accumulate) {
-          const float4 old = o[c * 4 + j];
-          v.x += old.x;
-          v.y += old.y;
-          v.z += old.z;
-          v.w += old.w;
-        }
-        o[c * 4 + j] = v;
-      }
+    for (int j = 0; j < 4; ++j) {
+      const int chunk = (c & 1) * 4 + j;
+      ot[(c >> 1) * 1024 + tid * 8 + (chunk ^ (tid & 7))] =
+          make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                      __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
     }
   }
+  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      if (a.accumulate)
+        tma_reduce_add_2d(&tmO, ot + half * 1024, 32 * half, static_cast<int32_t>(tile * 128));
+      else
+        tma_store_2d(&tmO, ot + half * 1024, 32 * half, static_cast<int32_t>(tile * 128));
+    }
+    bulk_commit_group();
+    bulk_wait_group_read0();  // the stores have read the tile before the CTA's smem goes
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 64);
@@ -509,11 +516,16 @@ void launch_unit(const ixb_conv_plan* P, const void* In, const void* Weight, flo
   if (ntiles <= 0) return;
   const CUtensorMap tmW = make_tmap_2d(Weight, 64, static_cast<uint64_t>(P->n_off) * 64, 128, 64,
                                        64, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (reinterpret_cast<uintptr_t>(Out) % 16 != 0)
+    fail(IXB_SHAPE, "ixb_conv_plan_run: Out must be 16-byte aligned");
+  // Out viewed as (64 cols, n_out rows): {32, 128} boxes, one per tile half
+  const CUtensorMap tmO = make_tmap_2d_f32(Out, 64, static_cast<uint64_t>(P->n_out), 256, 32, 128,
+                                           CU_TENSOR_MAP_SWIZZLE_128B);
   UnitArgs ua{P->Y.p, P->tile_mask.p, static_cast<const __nv_bfloat16*>(In), Out, P->n_out,
               accumulate, tile0};
   set_max_dynamic_smem(reinterpret_cast<const void*>(conv_unit_kernel), kUnitSmem,
                        "cudaFuncSetAttribute(conv_unit_kernel)");
-  conv_unit_kernel<<<static_cast<unsigned>(ntiles), kConvThreads, kUnitSmem, s>>>(tmW, ua);
+  conv_unit_kernel<<<static_cast<unsigned>(ntiles), kConvThreads, kUnitSmem, s>>>(tmW, tmO, ua);
   IXB_LAUNCH_CHECK("conv_unit_kernel");
 }
 

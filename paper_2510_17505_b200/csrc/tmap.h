@@ -8,6 +8,9 @@ namespace ixb {
 
 CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                          uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);
+// 2-D fp32 tensor (e.g. an output tile written back by TMA store).
+CUtensorMap make_tmap_2d_f32(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                             uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);
 // 2-D int32 tensor (no swizzle), e.g. index tables staged by TMA.
 CUtensorMap make_tmap_2d_i32(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                              uint32_t box_inner, uint32_t box_outer);
