@@ -298,13 +298,15 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
   uint8_t* W = smem + kUnitStages * kATile;  // [kUnitStages][8 KB]
   uint64_t* w_full = reinterpret_cast<uint64_t*>(W + kUnitStages * kWTile);
   uint64_t* mma_done = w_full + kUnitStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + kUnitStages);
+  uint64_t* a_full = mma_done + kUnitStages;  // per stage: the 4 warps' gathered rows are in
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + kUnitStages);
   const int tid = threadIdx.x, warp = tid >> 5;
 
   if (tid == 0) {
     for (int b = 0; b < kUnitStages; ++b) {
       mbar_init(&w_full[b], 1);
       mbar_init(&mma_done[b], 1);
+      mbar_init(&a_full[b], kConvThreads / 32);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmW);
@@ -367,8 +369,10 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
     const int st = k % kUnitStages;
     cp_async_wait<kUnitDist - 1>();  // this thread's rows of stage k have landed
     fence_proxy_async_smem();        // cp.async (generic proxy) -> tensor core
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&a_full[st]);  // this warp's 32 rows of stage k are in
     if (warp == 0) {  // whole warp, one elected lane issues
+      mbar_wait(&a_full[st], (k / kUnitStages) & 1);
       mbar_wait(&w_full[st], (k / kUnitStages) & 1);
       tc_fence_after();
       const uint32_t a0 = smem_u32(A + st * kATile), w0 = smem_u32(W + st * kWTile);
