@@ -159,6 +159,23 @@ int ixb_tune_brute(const int32_t* coord, int64_t nnz, int64_t extent, ixb_stream
 int ixb_tune_group_size(const int32_t* coord, int64_t nnz, int64_t extent, int count_empty_rows,
                         ixb_stream stream, int64_t* g_out, double* gstar_out);
 
+/* GroupCOO helpers (formats.hpp:49-58), device arrays in, host scalars out:
+ * real_count of a pad mask (pad_count = slots - real; formats.cpp:105-113),
+ * is_ell — no two consecutive groups share a coordinate (formats.cpp:202-208),
+ * the occupancy maximum ell_view groups by (g = max(max_occ, 1),
+ * formats.cpp:196-200), and groupcoo_to_coo (formats.cpp:176-194): the
+ * real slots in slot order into caller buffers of real_count entries
+ * (values of `dtype`, or NULL); the reference then canonicalizes, which the
+ * g = 1 grouping does (ixb_groupcoo_plan/pack with g = 1). */
+int ixb_mask_real_count(const uint8_t* mask, int64_t slots, ixb_stream stream, int64_t* real);
+int ixb_is_ell(const int32_t* group_coord, int64_t G, ixb_stream stream, int* is_ell);
+int ixb_max_occupancy(const int32_t* coord, int64_t nnz, int64_t extent, ixb_stream stream,
+                      int64_t* max_occ);
+int ixb_groupcoo_to_coo(const int32_t* group_coord, const int32_t* member_coord,
+                        const void* values, int dtype, const uint8_t* mask, int64_t G, int64_t g,
+                        int group_dim, int32_t* row_out, int32_t* col_out, void* val_out,
+                        ixb_stream stream);
+
 /* ======================================================================
  * Evaluators. Each validates indices in-kernel (unless IXB_UNCHECKED);
  * `accumulate` != 0 is `+=` (the output's contents prime the sum),

@@ -131,6 +131,16 @@ int check_builders() {
       GroupCooMatrix dg = b200::coo_to_groupcoo(dev_coo, dim, dr.chosen);
       rc |= report(("cfg1 coo_to_groupcoo dim" + std::to_string(dim) + " " + k).c_str(),
                    same(rg, dg), ", \"G\": " + std::to_string(dg.num_groups()));
+      // the helpers around the format (formats.cpp:105-113, 176-208)
+      rc |= report(("cfg1 real/pad_count, is_ell, groupcoo_to_coo dim" + std::to_string(dim) +
+                    " " + k).c_str(),
+                   rg.real_count() == b200::real_count(dg) &&
+                       rg.pad_count() == b200::pad_count(dg) && is_ell(rg) == b200::is_ell(dg) &&
+                       structurally_equal(groupcoo_to_coo(rg), b200::groupcoo_to_coo(dg)));
+      GroupCooMatrix re = ell_view(ref_coo, dim), de = b200::ell_view(dev_coo, dim);
+      rc |= report(("cfg1 ell_view dim" + std::to_string(dim) + " " + k).c_str(),
+                   same(re, de) && is_ell(re) == b200::is_ell(de),
+                   ", \"g\": " + std::to_string(de.group_size));
     }
     // canonicalize + grouping of an unsorted (shuffled) COO
     CooMatrix shuf = ref_coo;

@@ -98,6 +98,64 @@ CooMatrix canonicalize(const CooMatrix& c) {
   return out;
 }
 
+int64_t real_count(const GroupCooMatrix& gc) {
+  DevBuf mask(gc.pad_mask.size());
+  detail::cuda_ok(cudaMemcpy(mask.p, gc.pad_mask.data(), gc.pad_mask.size(),
+                             cudaMemcpyHostToDevice),
+                  "cudaMemcpy H2D");
+  int64_t n = 0;
+  check(ixb_mask_real_count(mask.as<uint8_t>(), static_cast<int64_t>(gc.pad_mask.size()), nullptr,
+                            &n));
+  return n;
+}
+
+int64_t pad_count(const GroupCooMatrix& gc) {
+  return static_cast<int64_t>(gc.pad_mask.size()) - b200::real_count(gc);
+}
+
+CooMatrix groupcoo_to_coo(const GroupCooMatrix& gc) {
+  const int64_t G = gc.num_groups(), g = gc.group_size, slots = G * g;
+  auto am = detail::upload_coords(gc.group_coord, "group");
+  auto ak = detail::upload_coords(gc.member_coord, "member");
+  auto av = detail::upload_values(gc.values);
+  DevBuf mask(static_cast<size_t>(slots));
+  detail::cuda_ok(cudaMemcpy(mask.p, gc.pad_mask.data(), static_cast<size_t>(slots),
+                             cudaMemcpyHostToDevice),
+                  "cudaMemcpy H2D");
+  int64_t nnz = 0;
+  check(ixb_mask_real_count(mask.as<uint8_t>(), slots, nullptr, &nnz));
+  DevBuf r(static_cast<size_t>(nnz) * 4), k(static_cast<size_t>(nnz) * 4),
+      v(static_cast<size_t>(nnz) * 8);
+  check(ixb_groupcoo_to_coo(am->as<int32_t>(), ak->as<int32_t>(), av->p,
+                            detail::value_dtype(gc.values), mask.as<uint8_t>(), G, g,
+                            gc.group_dim, r.as<int32_t>(), k.as<int32_t>(), v.p, nullptr));
+  sync();
+  CooMatrix c;
+  c.rows = gc.rows;
+  c.cols = gc.cols;
+  c.row_coord = detail::download_coords(r, nnz);
+  c.col_coord = detail::download_coords(k, nnz);
+  c.values = detail::download_values(v, gc.values.kind(), {nnz});
+  return b200::canonicalize(c);  // formats.cpp:193
+}
+
+GroupCooMatrix ell_view(const CooMatrix& c, int group_dim) {
+  if (group_dim != 0 && group_dim != 1) throw ShapeError("occupancy: dim must be 0 or 1");
+  const auto& coord = group_dim == 0 ? c.row_coord : c.col_coord;
+  auto d = detail::upload_coords(coord, group_dim == 0 ? "row" : "col");
+  int64_t m = 0;
+  check(ixb_max_occupancy(d->as<int32_t>(), c.nnz(), group_dim == 0 ? c.rows : c.cols, nullptr,
+                          &m));
+  return b200::coo_to_groupcoo(c, group_dim, m > 1 ? m : 1);
+}
+
+bool is_ell(const GroupCooMatrix& gc) {
+  auto am = detail::upload_coords(gc.group_coord, "group");
+  int f = 1;
+  check(ixb_is_ell(am->as<int32_t>(), gc.num_groups(), nullptr, &f));
+  return f != 0;
+}
+
 BlockGroupCooMatrix dense_to_blockgroupcoo(const Tensor& t, int64_t block_rows,
                                            int64_t block_cols, int64_t g, int group_dim) {
   // formats.cpp:226-228, then group_dim through coo_to_groupcoo (:265)

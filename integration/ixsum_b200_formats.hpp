@@ -24,6 +24,15 @@ GroupCooMatrix coo_to_groupcoo(const CooMatrix& c, int group_dim, int64_t g);
 /// dense_to_blockgroupcoo (formats.hpp:81-83, formats.cpp:224-292).
 BlockGroupCooMatrix dense_to_blockgroupcoo(const Tensor& t, int64_t block_rows,
                                            int64_t block_cols, int64_t g, int group_dim = 0);
+/// GroupCooMatrix::real_count / pad_count (formats.hpp:49-50, formats.cpp:105-113).
+int64_t real_count(const GroupCooMatrix& gc);
+int64_t pad_count(const GroupCooMatrix& gc);
+/// groupcoo_to_coo (formats.hpp:54, formats.cpp:176-194): real slots, canonicalized.
+CooMatrix groupcoo_to_coo(const GroupCooMatrix& gc);
+/// ell_view (formats.hpp:57, formats.cpp:196-200): g = max occupancy along group_dim.
+GroupCooMatrix ell_view(const CooMatrix& c, int group_dim = 0);
+/// is_ell (formats.hpp:58, formats.cpp:202-208).
+bool is_ell(const GroupCooMatrix& gc);
 /// group_coo_tensor (formats.hpp:141, formats.cpp:417-479).
 GroupCooTensor group_coo_tensor(const CooTensor& c, int group_dim, int64_t g);
 /// select() over the occupancy of c along `dim` (tuner.hpp:63, tuner.cpp:100-118,

@@ -21,7 +21,8 @@ from .api import (BlockGroupCoo, GroupCoo, GroupCooTensor, dense_to_blockgroupco
                   group_coo_tensor, kernel_map, tune_group_size, spmm_groupcoo,
                   spmm_blockgroupcoo, conv_grouped, tp_grouped, shard_groups, ConvPlan, TpPlan,
                   spmm_groupcoo_host, spmm_blockgroupcoo_host,
-                  count_accesses_model)
+                  count_accesses_model, real_count, pad_count, is_ell, ell_view,
+                  groupcoo_to_coo)
 from .executor import device_tolerance, execute_mode, match_workload, WORKLOADS
 from . import io
 from .io import (ixt_info, load_ixt, save_ixt, load_matrix_market, read_matrix_market_host,
@@ -34,7 +35,8 @@ __all__ = [
     "dense_to_groupcoo", "dense_to_blockgroupcoo", "group_coo_tensor", "emit_operands",
     "kernel_map", "tune_group_size", "spmm_groupcoo", "spmm_blockgroupcoo", "conv_grouped",
     "tp_grouped", "shard_groups", "ConvPlan", "TpPlan", "spmm_groupcoo_host",
-    "spmm_blockgroupcoo_host", "count_accesses_model", "device_tolerance", "execute_mode", "match_workload",
+    "spmm_blockgroupcoo_host", "count_accesses_model", "real_count", "pad_count", "is_ell",
+    "ell_view", "groupcoo_to_coo", "device_tolerance", "execute_mode", "match_workload",
     "WORKLOADS", "io", "ixt_info", "load_ixt", "save_ixt", "load_matrix_market",
     "read_matrix_market_host", "save_format", "load_format", "convert", "tune_report", "tune_measured",
 ]

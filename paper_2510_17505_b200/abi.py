@@ -108,6 +108,12 @@ _SIGS = {
                                                      C.c_void_p]),
     "ixb_tp_plan_free": (None, [C.c_void_p]),
     "ixb_tp_plan_uses_tensor_cores": (C.c_int, [C.c_void_p]),
+    "ixb_mask_real_count": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "ixb_is_ell": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "ixb_max_occupancy": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "ixb_groupcoo_to_coo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                      C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]),
     "ixb_tp_plan_run_host": (C.c_int, [C.c_void_p] * 4 + [C.c_int64, C.c_void_p, C.c_int,
                                                           C.c_int, C.c_int, C.c_void_p]),
     "ixb_shard_groups": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),

@@ -139,6 +139,56 @@ def coo_to_groupcoo(rows, cols, row_coord, col_coord, values, group_dim, g, cano
     return GroupCoo(rows, cols, group_dim, g, AM, AK, AV, mask)
 
 
+def real_count(fmt, stream=None):
+    """GroupCooMatrix::real_count (formats.cpp:105-108) of a device format."""
+    n = C.c_int64(0)
+    check(lib().ixb_mask_real_count(_ptr(fmt.mask), fmt.mask.numel(), _stream(stream),
+                                    C.byref(n)))
+    return n.value
+
+
+def pad_count(fmt, stream=None):
+    """GroupCooMatrix::pad_count (formats.cpp:110-113)."""
+    return fmt.mask.numel() - real_count(fmt, stream)
+
+
+def is_ell(fmt, stream=None):
+    """is_ell (formats.cpp:202-208): one group per distinct grouped coordinate."""
+    f = C.c_int(0)
+    check(lib().ixb_is_ell(_ptr(fmt.AM), fmt.AM.numel(), _stream(stream), C.byref(f)))
+    return bool(f.value)
+
+
+def ell_view(rows, cols, row_coord, col_coord, values, group_dim=0, canonical=False,
+             stream=None):
+    """ell_view (formats.cpp:196-200): coo_to_groupcoo with g = max occupancy."""
+    coord = _dev(row_coord if group_dim == 0 else col_coord, torch.int32)
+    m = C.c_int64(0)
+    check(lib().ixb_max_occupancy(_ptr(coord), coord.numel(), rows if group_dim == 0 else cols,
+                                  _stream(stream), C.byref(m)))
+    return coo_to_groupcoo(rows, cols, row_coord, col_coord, values, group_dim, max(m.value, 1),
+                           canonical=canonical, stream=stream)
+
+
+def groupcoo_to_coo(fmt, stream=None):
+    """groupcoo_to_coo (formats.cpp:176-194): the real slots, canonicalized
+    (row-major, the g = 1 grouping) -> (row_coord, col_coord, values) on the device."""
+    n = real_count(fmt, stream)
+    dev = fmt.AM.device
+    r = torch.empty(n, dtype=torch.int32, device=dev)
+    c = torch.empty(n, dtype=torch.int32, device=dev)
+    v = None if fmt.AV is None else torch.empty(n, dtype=fmt.AV.dtype, device=dev)
+    G, g = fmt.AK.shape
+    check(lib().ixb_groupcoo_to_coo(_ptr(fmt.AM), _ptr(fmt.AK), _ptr(fmt.AV),
+                                    0 if v is None else _dtype_code(fmt.AV), _ptr(fmt.mask), G, g,
+                                    fmt.group_dim, _ptr(r), _ptr(c), _ptr(v), _stream(stream)))
+    if n == 0:
+        return r, c, v
+    canon = coo_to_groupcoo(fmt.rows, fmt.cols, r, c, v, 0, 1, stream=stream)
+    return canon.AM.clone(), canon.AK.reshape(-1).clone(), \
+        None if v is None else canon.AV.reshape(-1).clone()
+
+
 def dense_to_groupcoo(dense, g=0, group_dim=0, stream=None):
     """dense_to_coo + coo_to_groupcoo fused (driver.cpp:101-116 `groupcoo`/`auto`)."""
     dense = _dev(dense)

@@ -364,3 +364,41 @@ def test_cfg3_length_rows_within_fp32_tolerance(P, ixo):
     P.spmm_groupcoo(fmt.AM, fmt.AK, fmt.AV, torch.from_numpy(b).cuda(), C)
     want = a.astype(np.float64) @ b.astype(np.float64)
     assert ixo.max_rel_error(want, C.double().cpu().numpy()) <= 1e-5
+
+
+def test_groupcoo_helpers_match_reference_semantics(P, ixo):
+    """real_count / pad_count, is_ell, ell_view and groupcoo_to_coo on the
+    device (formats.cpp:105-113, 176-208): the round trip returns the
+    canonical COO bit for bit, for both group dims and every g up to the
+    maximum occupancy (test_formats.cpp:107-131's check, on the device)."""
+    rng = ixo.Rng(23)
+    for it in range(12):
+        t = ixo.synth_sparse_matrix(rng, 40, 33, 0.2)
+        r, c, v = ixo.dense_to_coo(t)
+        gd = it % 2
+        occ = ixo.occupancy(r if gd == 0 else c, 40 if gd == 0 else 33)
+        rd = torch.from_numpy(r.astype(np.int32)).cuda()
+        cd = torch.from_numpy(c.astype(np.int32)).cuda()
+        vd = torch.from_numpy(v).float().cuda()
+        ell = P.ell_view(40, 33, rd, cd, vd, gd, canonical=True)
+        assert ell.group_size == max(int(occ.max()), 1) and P.is_ell(ell)
+        want = ixo.coo_to_groupcoo(40, 33, r, c, v, gd, ell.group_size)
+        np.testing.assert_array_equal(ell.AM.cpu().numpy(), want["AM"])
+        for g in sorted({1, 2, 3, max(int(occ.max()), 1)}):
+            fmt = P.coo_to_groupcoo(40, 33, rd, cd, vd, gd, g, canonical=True)
+            w = ixo.coo_to_groupcoo(40, 33, r, c, v, gd, g)
+            real = int(w["mask"].sum())
+            assert P.real_count(fmt) == real == r.size
+            assert P.pad_count(fmt) == w["mask"].size - real
+            am = w["AM"]
+            assert P.is_ell(fmt) == bool(np.all(am[1:] != am[:-1]))
+            rr, cc, vv = P.groupcoo_to_coo(fmt)
+            np.testing.assert_array_equal(rr.cpu().numpy(), r)
+            np.testing.assert_array_equal(cc.cpu().numpy(), c)
+            np.testing.assert_array_equal(vv.cpu().numpy(), v.astype(np.float32))
+    # empty format
+    e = P.coo_to_groupcoo(4, 4, torch.empty(0, dtype=torch.int32).cuda(),
+                          torch.empty(0, dtype=torch.int32).cuda(),
+                          torch.empty(0).cuda(), 0, 2, canonical=True)
+    assert P.real_count(e) == 0 and P.is_ell(e)
+    assert all(x is None or x.numel() == 0 for x in P.groupcoo_to_coo(e))
