@@ -300,6 +300,36 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
     const uint64_t keep = l2_evict_last();    // dense operand: re-read by many blocks
     const uint64_t stream = l2_evict_first();  // format: read once
     int64_t bc = 0;                            // stage batches walked (all producers)
+    // Early start: the first segment always begins at this CTA's range start
+    // lo (tile 0), and a group holds g >= (NPROD + 1) * SPS slots, so batch p
+    // (slots lo*g + p*SPS ...) is known before the scheduler's first push.
+    const int64_t lo0 = range_lo(a.G, gridDim.x, blockIdx.x);
+    const bool early = a.g >= static_cast<int64_t>((NPROD + 1) * SPS) &&
+                       lo0 < range_lo(a.G, gridDim.x, blockIdx.x + 1);
+    if (early) {
+      const int64_t slot0 = lo0 * a.g + static_cast<int64_t>(p) * SPS;
+      int k = 0;
+      if (lane < SPS) {
+        k = __ldg(a.AK + slot0 + lane);
+        if (k < 0 || static_cast<int64_t>(k) >= a.KB) {
+          if (a.check) report_index_error(a.err, 0, slot0 + lane, k);
+          k = 0;
+        }
+      }
+      int kk[SPS];
+#pragma unroll
+      for (int b = 0; b < SPS; ++b) kk[b] = __shfl_sync(0xffffffffu, k, b);
+      const int stage = p % STAGES;  // batch p, first use of its stage
+      if (elect_one_sync()) {
+        uint8_t* st = tiles + stage * L::kStageBytes;
+        mbar_arrive_expect_tx(&full[stage], SPS * L::kBBytes + SPS * kAvBytes);
+#pragma unroll
+        for (int b = 0; b < SPS; ++b)
+          tma_load_3d(st + b * L::kBBytes, &tmB, &full[stage], 0, kk[b] * 16, 0, keep);
+        tma_load_2d(st + SPS * L::kBBytes, &tmAV, &full[stage], 0,
+                    static_cast<int32_t>(slot0 * 16), stream);
+      }
+    }
     for (int j = 0;; ++j) {
       int4 sg;
       int tile;
@@ -325,6 +355,7 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
         const int cnt = static_cast<int>(s1 - i0 < 32 ? s1 - i0 : 32);
         for (int t = 0; t < cnt; t += SPS, ++bc) {
           if (static_cast<int>(bc % NPROD) != p) continue;
+          if (early && bc < NPROD) continue;  // issued before the first pop
           const int nb = cnt - t < SPS ? cnt - t : SPS;
           int kk[SPS];
 #pragma unroll
@@ -358,6 +389,31 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
     const int sub = warp - R::kIss0;
     constexpr uint32_t idesc = idesc_bf16_f32(128, 16, /*A MN-major*/ true, /*B K-major*/ false);
     int64_t bc = 0;  // stage batches consumed (lane 0)
+    // Early start (the producers' first NPROD batches, see there): the first
+    // segment's first batches go to accumulator 0 before the first pop.
+    const bool early = a.g >= static_cast<int64_t>((NPROD + 1) * SPS) &&
+                       range_lo(a.G, gridDim.x, blockIdx.x) <
+                           range_lo(a.G, gridDim.x, blockIdx.x + 1);
+    if (early) {
+      mbar_wait(&acc_empty[0], 1);  // fresh barrier: passes
+      tc_fence_after();
+      const uint32_t d = tmem_base + sub * 16;
+      for (int e = 0; e < NPROD; ++e) {
+        const int stage = e % STAGES;
+        mbar_wait(&full[stage], 0);
+        tc_fence_after();
+        const uint32_t st = smem_u32(tiles + stage * L::kStageBytes);
+#pragma unroll
+        for (int b = 0; b < SPS; ++b) {
+          const uint64_t bdesc =
+              smem_desc(st + SPS * L::kBBytes + b * kAvBytes, 16, 256, kLayoutSW32);
+          const uint64_t adesc =
+              smem_desc(st + b * L::kBBytes + sub * kSubBytes, 2048, 1024, kLayoutSW128);
+          umma_f16_elect(d, adesc, bdesc, idesc, (e > 0 || b > 0) ? 1u : 0u);
+        }
+        umma_commit_elect(&empty[stage]);
+      }
+    }
     for (int j = 0;; ++j) {
       int4 sg;
       int tile;
@@ -365,7 +421,7 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
       if (sg.x < 0) break;
       const int buf = j % NACC;
       // the whole warp walks the batches; one elected lane issues
-      mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
+      if (!(early && j == 0)) mbar_wait(&acc_empty[buf], ((j / NACC) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + buf * kAccCols + sub * 16;
       const int64_t nslots = (static_cast<int64_t>(sg.y) - sg.x) * a.g;
@@ -373,6 +429,7 @@ __global__ void __launch_bounds__(TcRoles<NSUB, NPROD>::kThreads, MINB)
       for (int64_t i0 = 0; i0 < nslots; i0 += 32) {
         const int cnt = static_cast<int>(nslots - i0 < 32 ? nslots - i0 : 32);
         for (int t = 0; t < cnt; t += SPS, ++bc) {
+          if (early && bc < NPROD) continue;  // issued before the first pop
           const int nb = cnt - t < SPS ? cnt - t : SPS;
           const int stage = static_cast<int>(bc % STAGES);
           mbar_wait(&full[stage], static_cast<uint32_t>((bc / STAGES) & 1));
