@@ -17,6 +17,7 @@
 // (formats.cpp:155-160, 454-468).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <cmath>
 #include <memory>
@@ -89,31 +90,16 @@ __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
 
 }  // namespace
 
-// select() of tuner.cpp:100-118 over device occupancy counts.
-int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_empty_rows,
-                      cudaStream_t s, double* gstar_out, int64_t* cand_g = nullptr,
-                      double* cand_score = nullptr, int* ncand = nullptr,
-                      int64_t* total_out = nullptr, int64_t* maxocc_out = nullptr) {
-  Scratch<OccStats> d(1, s);
-  IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
-  if (n > 0) {
-    // one row per thread up to two CTAs per SM (latency-bound for short
-    // profiles), grid-stride beyond; one global atomic per statistic per CTA
-    int64_t grid = ceil_div(n, kTB);
-    if (grid > 2 * sm_count()) grid = 2 * sm_count();
-    occ_stats_kernel<<<grid, kTB, 0, s>>>(occ, n, d.p);
-    IXB_LAUNCH_CHECK("occ_stats_kernel");
-  }
-  OccStats h;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
-  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
-  if (total_out) *total_out = static_cast<int64_t>(h.S);
-  if (maxocc_out) *maxocc_out = static_cast<int64_t>(h.maxocc);
+// select() of tuner.cpp:100-118 from the occupancy statistics (host or
+// device: IEEE double sqrt/division, the same result either side).
+__host__ __device__ int64_t choose_group_size(const OccStats& h, int64_t extent,
+                                              int count_empty_rows, double* gstar_out,
+                                              int64_t* cand_g, double* cand_score, int* ncand) {
   // g_star (tuner.cpp:60-65)
   double gs = 1.0;
   if (h.S > 0) {
     double nn = count_empty_rows ? static_cast<double>(extent) : static_cast<double>(h.nonzero);
-    gs = nn <= 0 ? 1.0 : std::sqrt(static_cast<double>(h.S) / nn);
+    gs = nn <= 0 ? 1.0 : sqrt(static_cast<double>(h.S) / nn);
   }
   if (gstar_out) *gstar_out = gs;
   if (h.S == 0) {  // candidate_group_sizes: {1}
@@ -151,6 +137,30 @@ int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_e
     }
   }
   return chosen;
+}
+
+
+// select() of tuner.cpp:100-118 over device occupancy counts.
+int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_empty_rows,
+                      cudaStream_t s, double* gstar_out, int64_t* cand_g = nullptr,
+                      double* cand_score = nullptr, int* ncand = nullptr,
+                      int64_t* total_out = nullptr, int64_t* maxocc_out = nullptr) {
+  Scratch<OccStats> d(1, s);
+  IXB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(OccStats), s));
+  if (n > 0) {
+    // one row per thread up to two CTAs per SM (latency-bound for short
+    // profiles), grid-stride beyond; one global atomic per statistic per CTA
+    int64_t grid = ceil_div(n, kTB);
+    if (grid > 2 * sm_count()) grid = 2 * sm_count();
+    occ_stats_kernel<<<grid, kTB, 0, s>>>(occ, n, d.p);
+    IXB_LAUNCH_CHECK("occ_stats_kernel");
+  }
+  OccStats h;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (total_out) *total_out = static_cast<int64_t>(h.S);
+  if (maxocc_out) *maxocc_out = static_cast<int64_t>(h.maxocc);
+  return choose_group_size(h, extent, count_empty_rows, gstar_out, cand_g, cand_score, ncand);
 }
 
 namespace {
@@ -351,11 +361,6 @@ void launch_occupancy(const int32_t* coord, int64_t nnz, int64_t extent, int32_t
   IXB_LAUNCH_CHECK("occupancy_kernel");
 }
 
-__global__ void groups_per_run_kernel(const int32_t* occ, int64_t n, int64_t g, int32_t* ng) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) ng[i] = static_cast<int32_t>((static_cast<int64_t>(occ[i]) + g - 1) / g);
-}
-
 // ---------------------------------------------------------- sorted runs
 __global__ void iota32(int32_t* x, int64_t n) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -473,10 +478,12 @@ __global__ void block_flags_kernel(const T* __restrict__ dense, int64_t rows, in
 // bm rows with coalesced 512-byte loads; the lanes of one block OR their
 // "any nonzero" bits by shuffles. Needs bk * sizeof(T) to divide 512 and 16-byte
 // aligned rows (the shape check is on the host); ragged edges are masked.
+// With `occ`, the warp also adds its nonzero-block count to occ[block row]
+// (the block row occupancy the grouping needs: no separate count pass).
 template <typename T>
 __global__ void block_flags_vec_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
                                        int64_t bm, int64_t bk, int64_t gr, int64_t gcn,
-                                       uint8_t* flags) {
+                                       uint8_t* flags, int32_t* occ) {
   constexpr int V = 16 / sizeof(T);  // elements per chunk
   const int lane = lane_id();
   const int cpb = static_cast<int>(bk / V);  // chunks per block row segment
@@ -492,6 +499,7 @@ __global__ void block_flags_vec_kernel(const T* __restrict__ dense, int64_t rows
   bool any = false;
   if (in) {
     if (c0 + V <= cols) {
+#pragma unroll 4
       for (int64_t i = br * bm; i < ie; ++i) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(dense + i * cols + c0));
         const T* e = reinterpret_cast<const T*>(&v);
@@ -506,7 +514,121 @@ __global__ void block_flags_vec_kernel(const T* __restrict__ dense, int64_t rows
   unsigned m = __ballot_sync(0xffffffffu, any);
   const int first = (lane / cpb) * cpb;
   const unsigned mine = (m >> first) & ((cpb == 32 ? 0u : (1u << cpb)) - 1u);
-  if (in && lane % cpb == 0) flags[br * gcn + bc] = (cpb == 32 ? m : mine) ? 1 : 0;
+  const bool f = (cpb == 32 ? m : mine) != 0;
+  if (in && lane % cpb == 0) flags[br * gcn + bc] = f ? 1 : 0;
+  if (occ) {
+    const unsigned nzb = __ballot_sync(0xffffffffu, in && lane % cpb == 0 && f);
+    if (lane == 0 && nzb) atomicAdd(&occ[br], __popc(nzb));
+  }
+}
+
+// Fused block-row pack (group_dim 0, 16-byte vector rows): one CTA per
+// block row. Per tile of 16 * kTB block flags the CTA lists the row's
+// nonzero blocks in column order (block scan) into shared memory, writes
+// their AK/mask slots and copies their bm x bk values into AV with all
+// threads (independent 16-byte loads, several in flight per thread); then
+// AM and the padded tail of the row's last group. Replaces row_pack over
+// the flags + a warp-per-slot block copy.
+template <typename T>
+__global__ void __launch_bounds__(kTB) block_row_pack_kernel(
+    const T* __restrict__ dense, int64_t rows, int64_t cols, int64_t bm, int64_t bk, int64_t gcn,
+    const uint8_t* __restrict__ flags, const int32_t* __restrict__ occ,
+    const int32_t* __restrict__ gofs, int64_t g, int32_t* AM, int32_t* AK, T* AV, uint8_t* mask) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int kTile = 16 * kTB;
+  __shared__ int32_t list[kTile];
+  __shared__ int wsum[kTB / 32];
+  __shared__ int last_col_s;
+  const int64_t br = blockIdx.x;
+  const int n = occ[br];
+  if (n == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = gofs[br];
+  const uint8_t* frow = flags + br * gcn;
+  const int cpr = static_cast<int>(bk / V);             // 16-byte chunks per block row
+  const int cpb = static_cast<int>(bm) * cpr;           // chunks per block
+  const int64_t blk = bm * bk;                          // elements per block
+  int64_t k0 = 0;
+  for (int64_t t0 = 0; t0 < gcn; t0 += kTile) {
+    // 16 flags per thread (byte loads: rows of flags need not be aligned)
+    uint32_t bits = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t c = t0 + tid * 16 + q;
+      if (c < gcn && frow[c]) bits |= 1u << q;
+    }
+    const int mine = __popc(bits);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kTB / 32; ++w) {
+      const int v = wsum[w];
+      if (w < warp) wbase += v;
+      tot += v;
+    }
+    int k = wbase + incl - mine;
+    for (uint32_t b = bits; b; b &= b - 1) list[k++] = static_cast<int32_t>(t0 + tid * 16 + __ffs(b) - 1);
+    __syncthreads();
+    for (int i = tid; i < tot; i += kTB) {
+      const int64_t kk = k0 + i;
+      const int64_t slot = (base + kk / g) * g + kk % g;
+      AK[slot] = list[i];
+      if (mask) mask[slot] = 1;
+    }
+    if (tot > 0 && tid == 0) last_col_s = list[tot - 1];
+    if (AV) {
+      // 4 independent 16-byte loads in flight per thread before their stores
+      const int nchunks = tot * cpb;
+      const int g32 = static_cast<int>(g);
+      for (int e0 = tid; e0 < nchunks; e0 += 4 * kTB) {
+        uint4 v[4];
+        T* dst[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * kTB;
+          v[u] = make_uint4(0, 0, 0, 0);
+          dst[u] = nullptr;
+          if (e < nchunks) {
+            const int i = e / cpb, c = e - i * cpb;
+            const int r = c / cpr, j = (c - r * cpr) * V;
+            const int kk = static_cast<int>(k0) + i;
+            const int64_t slot = (base + kk / g32) * g + kk % g32;
+            const int64_t si = br * bm + r, sj = static_cast<int64_t>(list[i]) * bk + j;
+            if (si < rows && sj < cols)
+              v[u] = __ldg(reinterpret_cast<const uint4*>(dense + si * cols + sj));
+            dst[u] = AV + slot * blk + r * bk + j;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (dst[u]) *reinterpret_cast<uint4*>(dst[u]) = v[u];
+      }
+    }
+    k0 += tot;
+    __syncthreads();  // list and wsum reused by the next tile
+  }
+  const int64_t ng = (n + g - 1) / g;
+  for (int64_t j = tid; j < ng; j += kTB) AM[base + j] = static_cast<int32_t>(br);
+  const int64_t real_last = n - (ng - 1) * g;  // real entries in the last group
+  const int64_t lastg = base + ng - 1;
+  const int lc = last_col_s;
+  for (int64_t q = real_last + tid; q < g; q += kTB) {
+    const int64_t slot = lastg * g + q;
+    AK[slot] = lc;
+    if (mask) mask[slot] = 0;
+  }
+  if (AV) {
+    const int64_t z0 = (lastg * g + real_last) * blk, z1 = (lastg + 1) * g * blk;  // pad values
+    for (int64_t e = z0 + static_cast<int64_t>(tid) * V; e < z1; e += static_cast<int64_t>(kTB) * V)
+      *reinterpret_cast<uint4*>(AV + e) = make_uint4(0, 0, 0, 0);
+  }
 }
 
 // Block copy: one warp per slot, 16-byte chunks (bk * sizeof(T) a multiple of
@@ -609,38 +731,183 @@ void launch_row_pack(const T* d, int64_t rows, int64_t cols, const int32_t* occ,
   IXB_LAUNCH_CHECK("row_pack_kernel");
 }
 
-// Exclusive scan of n int32 into out[0..n] (out[n] = total); returns total (sync).
-__global__ void scan_total_kernel(const int32_t* in, int64_t n, int32_t* out) {
-  out[n] = in[n - 1] + out[n - 1];
-}
-
 // Exclusive scan of n counts into out[0..n), with the total in out[n], all on
-// the device (no host round trip).
-void exclusive_scan_dev(const int32_t* in, int64_t n, int32_t* out, cudaStream_t s) {
-  if (n == 0) {
-    IXB_CUDA_CHECK(cudaMemsetAsync(out, 0, 4, s));
-    return;
-  }
+// the device (no host round trip): out[0] = 0, then an inclusive scan into
+// out + 1.
+template <typename It>
+void exclusive_scan_dev(It in, int64_t n, int32_t* out, cudaStream_t s) {
+  IXB_CUDA_CHECK(cudaMemsetAsync(out, 0, 4, s));
+  if (n == 0) return;
   size_t tb = 0;
-  IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int>(n), s));
+  IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out + 1, static_cast<int>(n), s));
   Scratch<char> tmp(tb, s);
-  IXB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, static_cast<int>(n), s));
+  IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.p, tb, in, out + 1, static_cast<int>(n), s));
   note_launch();
-  scan_total_kernel<<<1, 1, 0, s>>>(in, n, out);
-  IXB_LAUNCH_CHECK("scan_total_kernel");
 }
 
-// exclusive_scan_dev + the total read back (one host sync): the caller sizes
-// its output buffers from it.
-int64_t exclusive_scan_total(const int32_t* in, int64_t n, int32_t* out, cudaStream_t s) {
-  if (n == 0) return 0;
-  exclusive_scan_dev(in, n, out, s);
+// ceil(occ / g): groups of a run (the scan input of the group offsets)
+struct GroupsOf {
+  int64_t g;
+  __host__ __device__ int32_t operator()(int32_t occ) const {
+    return static_cast<int32_t>((static_cast<int64_t>(occ) + g - 1) / g);
+  }
+};
+
+// Short profiles (block rows, matrix rows up to kSmallScan): one CTA scans
+// ceil(in / g) (g = 1: the counts themselves) in tiles of 8 per thread and
+// writes the total to out[n] — one launch instead of cub's init + scan.
+constexpr int kSmallScan = 1 << 16;
+__device__ void block_scan_groups(const int32_t* in, int64_t n, int64_t g, int32_t* out,
+                                  int* wsum /* smem [32] */) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  int carry = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += 8 * blockDim.x) {
+    int v[8], mine = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t i = t0 + tid * 8 + q;
+      v[q] = i < n ? static_cast<int>((static_cast<int64_t>(in[i]) + g - 1) / g) : 0;
+      mine += v[q];
+    }
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int wbase = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      const int x = wsum[w];
+      wbase += w < warp ? x : 0;
+      tot += x;
+    }
+    int run = carry + wbase + incl - mine;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t i = t0 + tid * 8 + q;
+      if (i < n) out[i] = run;
+      run += v[q];
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  if (tid == 0) out[n] = carry;
+}
+
+__global__ void __launch_bounds__(1024) small_scan_kernel(const int32_t* in, int64_t n, int64_t g,
+                                                          int32_t* out) {
+  __shared__ int wsum[32];
+  block_scan_groups(in, n, g, out, wsum);
+}
+
+// Short profiles, one launch and one host read for the whole plan step: the
+// occupancy statistics (S, and with g_req = 0 the tuner's as in
+// occ_stats_kernel), select() on the device (choose_group_size), then the
+// group offsets ceil(occ / g) scanned into out[0..n]. res = {g, S}.
+__global__ void __launch_bounds__(512) tune_scan_kernel(const int32_t* occ, int64_t n,
+                                                         int64_t extent, int count_empty_rows,
+                                                         int64_t g_req, int32_t* out,
+                                                         int64_t* res) {
+  __shared__ unsigned long long part[32][35];
+  __shared__ OccStats st;
+  __shared__ int wsum[32];
+  __shared__ int64_t g_s;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  unsigned S = 0, nz = 0, mx = 0, grp[32] = {};
+  const bool tune = g_req == 0;
+  for (int64_t r = tid; r < n; r += blockDim.x) {
+    const unsigned o = static_cast<unsigned>(occ[r]);
+    S += o;
+    nz += o > 0;
+    mx = o > mx ? o : mx;
+    if (tune) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) grp[i] += static_cast<unsigned>(
+          (static_cast<unsigned long long>(o) + (1ull << i) - 1) >> i);
+    }
+  }
+  S = __reduce_add_sync(0xffffffffu, S);
+  nz = __reduce_add_sync(0xffffffffu, nz);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) grp[i] = __reduce_add_sync(0xffffffffu, grp[i]);
+  if (lane == 0) {
+    part[w][0] = S;
+    part[w][1] = nz;
+    part[w][2] = mx;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (lane == i) part[w][3 + i] = grp[i];
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  if (tid < 35) {
+    unsigned long long v = 0;
+    for (int k = 0; k < nw; ++k) {
+      const unsigned long long x = part[k][tid];
+      v = tid == 2 ? (x > v ? x : v) : v + x;
+    }
+    if (tid == 0) st.S = v;
+    else if (tid == 1) st.nonzero = v;
+    else if (tid == 2) st.maxocc = v;
+    else st.groups_pow2[tid - 3] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    g_s = tune ? choose_group_size(st, extent, count_empty_rows, nullptr, nullptr, nullptr,
+                                   nullptr)
+               : g_req;
+    res[0] = g_s;
+    res[1] = static_cast<int64_t>(st.S);
+  }
+  __syncthreads();
+  block_scan_groups(occ, n, g_s, out, wsum);
+}
+
+int64_t read_scan_total(const int32_t* out, int64_t n, cudaStream_t s) {
   int32_t total = 0;
   IXB_CUDA_CHECK(cudaMemcpyAsync(&total, out + n, 4, cudaMemcpyDeviceToHost, s));
   IXB_CUDA_CHECK(cudaStreamSynchronize(s));
   // counts are non-negative, so a negative int32 total means it wrapped past 2^31
   if (total < 0) fail(IXB_SHAPE, "format exceeds 2^31 entries");
   return total;
+}
+
+// Tuner (g_req = 0) + group offsets of short profiles in one launch and one
+// host read: returns false (nothing done) when n is too long for one CTA.
+bool tune_and_scan(const int32_t* counts, int64_t n, int64_t extent, int count_empty_rows,
+                   int64_t g_req, int32_t* out, cudaStream_t s, int64_t* g, int64_t* S,
+                   int64_t* G) {
+  if (n == 0 || n > kSmallScan) return false;
+  Scratch<int64_t> res(2, s);
+  tune_scan_kernel<<<1, 512, 0, s>>>(counts, n, extent, count_empty_rows, g_req, out, res.p);
+  IXB_LAUNCH_CHECK("tune_scan_kernel");
+  int64_t h[2];
+  int32_t total = 0;
+  IXB_CUDA_CHECK(cudaMemcpyAsync(h, res.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaMemcpyAsync(&total, out + n, 4, cudaMemcpyDeviceToHost, s));
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (total < 0 || h[1] > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 entries");
+  *g = h[0];
+  if (S) *S = h[1];
+  *G = total;
+  return true;
+}
+
+// ceil(counts / g) scanned (exclusive, total in out[n]) and the total read back.
+int64_t groups_scan_total(const int32_t* counts, int64_t n, int64_t g, int32_t* out,
+                          cudaStream_t s) {
+  if (n == 0) return 0;
+  if (n <= kSmallScan) {
+    small_scan_kernel<<<1, 1024, 0, s>>>(counts, n, g, out);
+    IXB_LAUNCH_CHECK("small_scan_kernel");
+  } else {
+    exclusive_scan_dev(thrust::make_transform_iterator(counts, GroupsOf{g}), n, out, s);
+  }
+  return read_scan_total(out, n, s);
 }
 
 void count_rows(ixb_pack* P) {
@@ -652,8 +919,14 @@ void count_rows(ixb_pack* P) {
 }
 
 // Dense-row grouping plan (group_dim 0): occ -> tuner -> groups per row -> gofs.
-void plan_dense_rows(ixb_pack* P, int64_t g_req, int64_t* g_out) {
-  count_rows(P);
+void plan_dense_rows(ixb_pack* P, int64_t g_req, int64_t* g_out, bool have_occ = false) {
+  if (!have_occ) count_rows(P);
+  P->offs = Scratch<int32_t>(P->rows + 1, P->s);
+  if (tune_and_scan(P->occ.p, P->rows, P->rows, 0, g_req, P->offs.p, P->s, &P->g, &P->nnz,
+                    &P->G)) {
+    if (g_out) *g_out = P->g;
+    return;
+  }
   int64_t g = g_req;
   if (g == 0) {
     // the tuner's one read-back also returns S = nnz
@@ -662,17 +935,11 @@ void plan_dense_rows(ixb_pack* P, int64_t g_req, int64_t* g_out) {
     if (P->nnz > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 entries");
   } else {
     Scratch<int32_t> tmp(P->rows + 1, P->s);
-    P->nnz = exclusive_scan_total(P->occ.p, P->rows, tmp.p, P->s);
+    P->nnz = groups_scan_total(P->occ.p, P->rows, 1, tmp.p, P->s);
   }
   P->g = g;
   if (g_out) *g_out = g;
-  Scratch<int32_t> ng(P->rows + 1, P->s);
-  if (P->rows) {
-    groups_per_run_kernel<<<ceil_div(P->rows, kTB), kTB, 0, P->s>>>(P->occ.p, P->rows, g, ng.p);
-    IXB_LAUNCH_CHECK("groups_per_run_kernel");
-  }
-  P->offs = Scratch<int32_t>(P->rows + 1, P->s);
-  P->G = exclusive_scan_total(ng.p, P->rows, P->offs.p, P->s);
+  P->G = groups_scan_total(P->occ.p, P->rows, g, P->offs.p, P->s);
 }
 
 template <typename T>
@@ -742,17 +1009,17 @@ void plan_sorted_runs(ixb_pack* P, bool identity_order, int64_t g_req, int64_t e
     run_lengths<<<ceil_div(R, kTB), kTB, 0, s>>>(P->start.p, R, n, P->len.p);
     IXB_LAUNCH_CHECK("run_lengths");
   }
+  P->gofs = Scratch<int32_t>(R + 1, s);
+  if (tune_and_scan(P->len.p, R, extent, count_empty_rows, g_req, P->gofs.p, s, &P->g, nullptr,
+                    &P->G)) {
+    if (g_out) *g_out = P->g;
+    return;
+  }
   int64_t g = g_req;
   if (g == 0) g = tune_from_occ(P->len.p, R, extent, count_empty_rows, s, nullptr);
   P->g = g;
   if (g_out) *g_out = g;
-  Scratch<int32_t> ng(R + 1, s);
-  if (R) {
-    groups_per_run_kernel<<<ceil_div(R, kTB), kTB, 0, s>>>(P->len.p, R, g, ng.p);
-    IXB_LAUNCH_CHECK("groups_per_run_kernel");
-  }
-  P->gofs = Scratch<int32_t>(R + 1, s);
-  P->G = exclusive_scan_total(ng.p, R, P->gofs.p, s);
+  P->G = groups_scan_total(P->len.p, R, g, P->gofs.p, s);
 }
 
 void pack_sorted_runs(ixb_pack* P, const void* vals, int dtype, int32_t* gout,
@@ -819,7 +1086,7 @@ int ixb_dense_to_coo_plan(const void* dense, int dtype, int64_t rows, int64_t co
     P->cols = cols;
     count_rows(P.get());
     P->offs = Scratch<int32_t>(rows + 1, P->s);
-    P->nnz = exclusive_scan_total(P->occ.p, rows, P->offs.p, P->s);
+    P->nnz = groups_scan_total(P->occ.p, rows, 1, P->offs.p, P->s);
     *nnz = P->nnz;
     *plan = P.release();
   });
@@ -890,7 +1157,7 @@ int ixb_dense_groupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t 
       // columns: dense_to_coo, then the sorted-run engine keyed (col, row)
       count_rows(P.get());
       P->offs = Scratch<int32_t>(rows + 1, P->s);
-      P->nnz = exclusive_scan_total(P->occ.p, rows, P->offs.p, P->s);
+      P->nnz = groups_scan_total(P->occ.p, rows, 1, P->offs.p, P->s);
       P->coo_r = Scratch<int32_t>(P->nnz, P->s);
       P->coo_c = Scratch<int32_t>(P->nnz, P->s);
       dispatch_dense(dtype, [&](auto tag) {
@@ -954,6 +1221,8 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
     P->gcn = ceil_div(cols, bk);
     const int64_t nb = P->gr * P->gcn;
     P->flags = Scratch<uint8_t>(nb + 16, P->s);
+    auto I = std::make_unique<ixb_pack>();
+    bool fused = false;  // flags kernel also counted the block rows (I->occ)
     if (nb) {
       dispatch_dense(dtype, [&](auto tag) {
         using T = decltype(tag);
@@ -964,8 +1233,14 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
         if (vec) {
           const int64_t bpw = 512 / rowb;
           const int64_t warps = P->gr * ceil_div(P->gcn, bpw);
+          fused = group_dim == 0;
+          if (fused) {
+            I->occ = Scratch<int32_t>(P->gr + 1, P->s);
+            IXB_CUDA_CHECK(cudaMemsetAsync(I->occ.p, 0, (P->gr + 1) * 4, P->s));
+          }
           block_flags_vec_kernel<<<ceil_div(warps * 32, kTB), kTB, 0, P->s>>>(
-              static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
+              static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p,
+              fused ? I->occ.p : nullptr);
         } else {
           block_flags_kernel<<<ceil_div(nb, kTB), kTB, 0, P->s>>>(
               static_cast<const T*>(dense), rows, cols, bm, bk, P->gr, P->gcn, P->flags.p);
@@ -974,7 +1249,6 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
       IXB_LAUNCH_CHECK("block_flags_kernel");
     }
     // group the block-level COO like coo_to_groupcoo (formats.cpp:265)
-    auto I = std::make_unique<ixb_pack>();
     I->s = P->s;
     I->dense = P->flags.p;
     I->dtype = IXB_U8;  // block flags
@@ -983,11 +1257,11 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
     I->group_dim = group_dim;
     if (group_dim == 0) {
       I->type = 1;
-      plan_dense_rows(I.get(), g, g_out);
+      plan_dense_rows(I.get(), g, g_out, fused);
     } else {
       count_rows(I.get());
       I->offs = Scratch<int32_t>(I->rows + 1, I->s);
-      I->nnz = exclusive_scan_total(I->occ.p, I->rows, I->offs.p, I->s);
+      I->nnz = groups_scan_total(I->occ.p, I->rows, 1, I->offs.p, I->s);
       I->coo_r = Scratch<int32_t>(I->nnz, I->s);
       I->coo_c = Scratch<int32_t>(I->nnz, I->s);
       launch_row_pack(static_cast<const uint8_t*>(I->dense), I->rows, I->cols, I->occ.p,
@@ -1021,6 +1295,23 @@ int ixb_blockgroupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint
     if (!m) {
       own_mask = Scratch<uint8_t>(slots + 16, P->s);
       m = own_mask.p;
+    }
+    const bool vec_rows = (P->bk * static_cast<int64_t>(dense_bytes(P->dtype))) % 16 == 0 &&
+                          (P->cols * static_cast<int64_t>(dense_bytes(P->dtype))) % 16 == 0 &&
+                          reinterpret_cast<uintptr_t>(P->dense) % 16 == 0 &&
+                          reinterpret_cast<uintptr_t>(AV) % 16 == 0;
+    if (I->type == 1 && vec_rows) {
+      // fused: AM/AK/mask and the AV blocks in one pass per block row
+      if (P->gr && slots) {
+        dispatch_dense(P->dtype, [&](auto tag) {
+          using T = decltype(tag);
+          block_row_pack_kernel<T><<<static_cast<unsigned>(P->gr), kTB, 0, P->s>>>(
+              static_cast<const T*>(P->dense), P->rows, P->cols, P->bm, P->bk, P->gcn, P->flags.p,
+              I->occ.p, I->offs.p, P->g, AM, AK, static_cast<T*>(AV), m);
+        });
+        IXB_LAUNCH_CHECK("block_row_pack_kernel");
+      }
+      return;
     }
     if (I->type == 1) {
       pack_dense_rows(I, AM, AK, nullptr, m);

@@ -44,7 +44,8 @@ def run(P, t, out, accumulate=True, flags=0):
 def test_blockgroupcoo_builder_bit_exact(P, ixo, dtype):
     rng = ixo.Rng(8)
     cases = [(4, 4, 2, 2, 2, 0.5), (5, 6, 4, 4, 2, 0.5), (64, 48, 16, 16, 3, 0.3),
-             (37, 53, 8, 4, 1, 0.2), (128, 128, 16, 16, 8, 0.1), (16, 16, 16, 16, 1, 1.0)]
+             (37, 53, 8, 4, 1, 0.2), (128, 128, 16, 16, 8, 0.1), (16, 16, 16, 16, 1, 1.0),
+             (13, 33600, 8, 8, 3, 0.3)]  # > 4096 block columns: several pack tiles per block row
     for rows, cols, bm, bk, g, d in cases:
         a = ixo.synth_block_sparse_matrix(rng, rows, cols, bm, bk, d)
         a = bf16_round(a) if dtype == torch.bfloat16 else a.astype(np.float32).astype(np.float64)

@@ -97,6 +97,21 @@ def test_coo_to_groupcoo_canonical_fast_path(P, ixo):
     np.testing.assert_array_equal(got.AM.cpu().numpy(), want["AM"])
 
 
+@pytest.mark.parametrize("rows", [9000, 70000])
+def test_dense_groupcoo_tall_profiles(P, ixo, rows):
+    """Row profiles longer than one scan tile (8192 rows) and longer than the
+    single-CTA scan (65536 rows, cub path): group offsets and AM bit-exact."""
+    rng = ixo.Rng(rows)
+    a = f32(ixo.synth_sparse_matrix(rng, rows, 12, 0.3))
+    r, c, v = ixo.dense_to_coo(a)
+    for g in (3, 0):
+        got = P.dense_to_groupcoo(dev(a, torch.float32), g=g)
+        want = ixo.coo_to_groupcoo(rows, 12, r, c, v, 0, got.group_size)
+        for k in ("AM", "AK", "AV", "mask"):
+            np.testing.assert_array_equal(getattr(got, k).cpu().numpy().astype(want[k].dtype),
+                                          want[k], err_msg=f"{k} rows={rows} g={g}")
+
+
 def test_tuner_matches_oracle(P, ixo):
     g_np = np.random.default_rng(2)
     for it in range(20):

@@ -64,6 +64,17 @@ def main():
     out["stages_per_cta"] = {q: float(np.percentile(t[:, 12], q)) for q in (0, 50, 100)}
     dur = (t[:, 7] - t[:, 6]) / 1e3
     out["iss_active_us"] = {q: round(float(np.percentile(dur, q)), 2) for q in (10, 50, 90, 100)}
+    # end time (us) by CTA index (c and c + grid/2 usually share an SM)
+    endt = (t[:, 10] - t0) / 1e3
+    first = (t[:, 6] - t0) / 1e3
+    n = len(endt)
+    out["end_by_cta_half"] = [round(float(np.median(endt[: n // 2])), 2),
+                              round(float(np.median(endt[n // 2:])), 2)]
+    order = np.argsort(endt)
+    out["latest_ctas"] = [(int(i), round(float(endt[i]), 2), round(float(first[i]), 2))
+                          for i in order[-12:]]
+    out["earliest_ctas"] = [(int(i), round(float(endt[i]), 2), round(float(first[i]), 2))
+                            for i in order[:6]]
     print(json.dumps(out, indent=1))
 
 

@@ -14,11 +14,9 @@ subprocess.run([sys.executable, os.path.join(here, "tp_run.py"), "1"], check=Tru
 t = np.load("/tmp/tp_trace.npy").reshape(4, 4, 512).astype(np.int64)
 t0 = t[1, 0, 0]
 print("group  mma:wW  wW->  vE->  commit   cons4: wait  got  done   cons19 done   wload")
-print("pass: arrive-bar1  after-bar1  coefs-done  after-bar2 | exchange (of the pass before): "
-      "round0  round1  round1-after-wait (consumer warp 4)")
-for P in range(12):
-    print(P, " ".join(f"{t[i, j, P] - t0:8d}" for i, j in ((3, 0), (3, 1), (3, 3), (0, 3))), "|",
-          " ".join(f"{t[i, j, P] - t0:8d}" for i, j in ((3, 2), (0, 2), (0, 1))))
+print("pass end (consumer warp 4): start  after-read-wait  after-barA  after-barB  after-barC  coefs-done  after-bar")
+for P in range(1, 13):
+    print(P, " ".join(f"{t[i, j, P] - t0:8d}" for i, j in ((3, 0), (3, 1), (3, 2), (0, 1), (0, 2), (3, 3), (0, 3))))
 for g in range(0, 130):
     r = [t[1, 0, g], t[1, 1, g], t[1, 2, g], t[1, 3, g], t[2, 0, g], t[2, 1, g], t[2, 2, g],
          0, t[0, 0, g]]
