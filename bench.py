@@ -668,6 +668,22 @@ def cpu_reference_time(wl, steps=1, warmup=0, budget_rows=None):
             "ms_per_step": ms, "mode": mode}
 
 
+def host_info():
+    """CPU model and the reference build's compiler flags (BASELINE.md §5 asks
+    for both next to every CPU number)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(),
+            "compiler": "g++ -std=c++20 -O2 (oracle/Makefile, unmodified reference sources)"}
+
+
 def run_reference_arm(args, wl):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -680,7 +696,7 @@ def run_reference_arm(args, wl):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference synth, seed 1)", "config": wl.config(),
             "cpu_baseline": {"value": r["value"], "unit": r["unit"], "cores": r["cores"],
-                             "kind": r["kind"], "sample": r["sample"]},
+                             "kind": r["kind"], "sample": r["sample"], **host_info()},
             "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -1097,7 +1113,7 @@ def sharded_records(torch, P, S, dev, rank, ws, dist, flush, stream, steps, name
 def cpu_line(wl, budget=None, steps=1):
     try:
         r = cpu_reference_time(wl, steps=steps, budget_rows=budget)
-        return {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        return dict({k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}, **host_info())
     except Exception as e:  # reported, never fatal
         return {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "reference",
                 "sample": f"unavailable: {e}"}
