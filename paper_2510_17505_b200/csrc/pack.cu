@@ -92,15 +92,39 @@ __global__ void occ_stats_kernel(const int32_t* occ, int64_t n, OccStats* out) {
 
 // select() of tuner.cpp:100-118 from the occupancy statistics (host or
 // device: IEEE double sqrt/division, the same result either side).
+// g_star (tuner.cpp:60-65) and candidate_group_sizes (tuner.cpp:67-84): the
+// power-of-two candidates lo <= hi around g_star, capped by the largest
+// occupancy; S == 0 gives {1}.
+__host__ __device__ void tuner_candidates(unsigned long long S, unsigned long long nonzero,
+                                          unsigned long long maxocc, int64_t extent,
+                                          int count_empty_rows, double* gs_out, int64_t* lo_out,
+                                          int64_t* hi_out) {
+  double gs = 1.0;
+  if (S > 0) {
+    double nn = count_empty_rows ? static_cast<double>(extent) : static_cast<double>(nonzero);
+    gs = nn <= 0 ? 1.0 : sqrt(static_cast<double>(S) / nn);
+  }
+  *gs_out = gs;
+  if (S == 0) {
+    *lo_out = *hi_out = 1;
+    return;
+  }
+  int64_t lo = 1;
+  while (lo * 2 <= static_cast<int64_t>(gs)) lo *= 2;
+  int64_t hi = lo;
+  while (static_cast<double>(hi) < gs) hi *= 2;
+  int64_t cap = 1;
+  while (cap * 2 <= static_cast<int64_t>(maxocc)) cap *= 2;
+  *lo_out = lo < 1 ? 1 : (lo > cap ? cap : lo);
+  *hi_out = hi < 1 ? 1 : (hi > cap ? cap : hi);
+}
+
 __host__ __device__ int64_t choose_group_size(const OccStats& h, int64_t extent,
                                               int count_empty_rows, double* gstar_out,
                                               int64_t* cand_g, double* cand_score, int* ncand) {
-  // g_star (tuner.cpp:60-65)
-  double gs = 1.0;
-  if (h.S > 0) {
-    double nn = count_empty_rows ? static_cast<double>(extent) : static_cast<double>(h.nonzero);
-    gs = nn <= 0 ? 1.0 : sqrt(static_cast<double>(h.S) / nn);
-  }
+  double gs;
+  int64_t lo, hi;
+  tuner_candidates(h.S, h.nonzero, h.maxocc, extent, count_empty_rows, &gs, &lo, &hi);
   if (gstar_out) *gstar_out = gs;
   if (h.S == 0) {  // candidate_group_sizes: {1}
     if (ncand) {
@@ -110,15 +134,6 @@ __host__ __device__ int64_t choose_group_size(const OccStats& h, int64_t extent,
     }
     return 1;
   }
-  // candidate_group_sizes (tuner.cpp:67-84)
-  int64_t lo = 1;
-  while (lo * 2 <= static_cast<int64_t>(gs)) lo *= 2;
-  int64_t hi = lo;
-  while (static_cast<double>(hi) < gs) hi *= 2;
-  int64_t cap = 1;
-  while (cap * 2 <= static_cast<int64_t>(h.maxocc)) cap *= 2;
-  lo = lo < 1 ? 1 : (lo > cap ? cap : lo);
-  hi = hi < 1 ? 1 : (hi > cap ? cap : hi);
   auto cost = [&](int64_t g) {  // cost_exact (tuner.cpp:31-36), g a power of two
     int sh = 0;
     while ((1ll << sh) < g) ++sh;
@@ -199,21 +214,27 @@ int dense_bytes(int dtype) {
 }
 
 template <typename T>
-struct Vec16 {
+struct alignas(16) Vec16 {
   static constexpr int V = 16 / sizeof(T);
   T x[V];
 };
 
 // occ[row] = number of nonzeros of row `row` (formats.cpp:33-41 scan order).
+// Long rows are cut into nseg segments of seg columns, one warp each: the
+// segment's count goes to occ_seg[row * nseg + seg] and is added to occ[row]
+// (zeroed by the caller); nseg == 1 stores occ[row] directly.
 template <typename T, int V>
 __global__ void row_count_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
-                                 int32_t* occ) {
-  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (row >= rows) return;
+                                 int64_t nseg, int64_t seg, int32_t* occ, int32_t* occ_seg) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w >= rows * nseg) return;
+  const int64_t row = w / nseg, c0 = (w % nseg) * seg;
+  const int64_t c1 = c0 + seg < cols ? c0 + seg : cols;
   const int lane = lane_id();
   const T* p = dense + row * cols;
   int cnt = 0;
-  for (int64_t c = static_cast<int64_t>(lane) * V; c < cols; c += 32 * V) {
+#pragma unroll 4
+  for (int64_t c = c0 + static_cast<int64_t>(lane) * V; c < c1; c += 32 * V) {
     if (V > 1) {
       Vec16<T> v = *reinterpret_cast<const Vec16<T>*>(p + c);
 #pragma unroll
@@ -222,75 +243,136 @@ __global__ void row_count_kernel(const T* __restrict__ dense, int64_t rows, int6
       cnt += nz<T>(p[c]);
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) occ[row] = cnt;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) {
+    if (nseg == 1) {
+      occ[row] = cnt;
+    } else {
+      occ_seg[w] = cnt;
+      if (cnt) atomicAdd(&occ[row], cnt);
+    }
+  }
 }
 
 // Dense-row pack. mode 0: GroupCOO slots (gofs, g); mode 1: plain COO at rowptr.
+// One warp per (row, segment) as in row_count_kernel: the segment's first
+// entry index in the row is the sum of the earlier segments' counts; the
+// warp of the row's last non-empty segment also writes AM and the padding.
 template <typename T, int V>
-__global__ void row_pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
-                                const int32_t* __restrict__ occ,
+__global__ void __launch_bounds__(256, 4) row_pack_kernel(const T* __restrict__ dense, int64_t rows, int64_t cols,
+                                int64_t nseg, int64_t seg, const int32_t* __restrict__ occ,
+                                const int32_t* __restrict__ occ_seg,
                                 const int32_t* __restrict__ offs,  // gofs (mode 0) / rowptr (1)
                                 int64_t g, int mode, int32_t* AM, int32_t* AK, T* AV,
                                 uint8_t* mask) {
-  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (row >= rows) return;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w >= rows * nseg) return;
+  const int64_t row = w / nseg;
+  const int sg = static_cast<int>(w % nseg);
   const int lane = lane_id();
-  const int n = occ[row];
-  if (n == 0) return;
+  const int64_t c_lo = static_cast<int64_t>(sg) * seg;
+  const int64_t c_hi = c_lo + seg < cols ? c_lo + seg : cols;
   const T* p = dense + row * cols;
-  const int64_t base = offs[row];
-  int64_t k0 = 0;
-  int last_col = 0;
-  for (int64_t c = static_cast<int64_t>(lane) * V; c - lane * V < cols; c += 32 * V) {
-    T vals[V];
-    if (V > 1) {
-      if (c < cols) {
-        Vec16<T> v = *reinterpret_cast<const Vec16<T>*>(p + c);
+  // batches of kB chunks of 32 * V columns: the kB 16-byte loads of a lane
+  // are in flight together; the first batch is issued before the row's
+  // metadata arrives
+  constexpr int kB = 4;
+  static_assert(32 * V < 65536, "16-bit count fields");
+  auto load_batch = [&](T (&vals)[kB][V], int64_t cb) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) vals[j] = v.x[j];
+    for (int u = 0; u < kB; ++u) {
+      const int64_t c = cb + u * 32 * V;
+      if (V > 1) {
+        if (c < c_hi) {
+          Vec16<T> v = *reinterpret_cast<const Vec16<T>*>(p + c);
+#pragma unroll
+          for (int j = 0; j < V; ++j) vals[u][j] = v.x[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; ++j) vals[u][j] = T(0);
+        }
       } else {
-#pragma unroll
-        for (int j = 0; j < V; ++j) vals[j] = T(0);
+        vals[u][0] = c < c_hi ? p[c] : T(0);
       }
-    } else {
-      vals[0] = c < cols ? p[c] : T(0);
     }
-    int mine = 0;
+  };
+  T vals[kB][V];
+  int64_t cb = c_lo + static_cast<int64_t>(lane) * V;
+  load_batch(vals, cb);
+  const int n = occ[row];
+  const int cs = nseg > 1 && lane < nseg ? occ_seg[row * nseg + lane] : 0;
+  const int64_t base = offs[row];
+  if (n == 0) return;
+  int64_t k0 = 0;
+  bool last_seg = true;
+  if (nseg > 1) {  // nseg <= 32: one count per lane
+    if (__shfl_sync(0xffffffffu, cs, sg) == 0) return;
+    k0 = __reduce_add_sync(0xffffffffu, lane < sg ? cs : 0);
+    last_seg = __ballot_sync(0xffffffffu, lane > sg && cs > 0) == 0;
+  }
+  int last_col = 0;
+  for (bool first = true; cb - lane * V < c_hi; cb += kB * 32 * V, first = false) {
+    if (!first) load_batch(vals, cb);
+    // one warp scan for the kB chunks: their per-lane counts packed as
+    // 16-bit fields (chunks 0, 1 in lo; 2, 3 in hi)
+    int cnt[kB];
 #pragma unroll
-    for (int j = 0; j < V; ++j) mine += nz<T>(vals[j]);
-    int incl = mine;
+    for (int u = 0; u < kB; ++u) {
+      cnt[u] = 0;
+#pragma unroll
+      for (int j = 0; j < V; ++j) cnt[u] += nz<T>(vals[u][j]);
+    }
+    const uint32_t plo = static_cast<uint32_t>(cnt[0]) | (static_cast<uint32_t>(cnt[1]) << 16);
+    const uint32_t phi = static_cast<uint32_t>(cnt[2]) | (static_cast<uint32_t>(cnt[3]) << 16);
+    const bool any = __any_sync(0xffffffffu, (plo | phi) != 0);  // else an all-zero batch
+    if (any) {
+    uint32_t ilo = plo, ihi = phi;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    int64_t k = k0 + incl - mine;
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (!nz<T>(vals[j])) continue;
-      const int col = static_cast<int>(c + j);
-      if (mode == 0) {
-        const int64_t slot = (base + k / g) * g + k % g;
-        AK[slot] = col;
-        if (AV) AV[slot] = vals[j];
-        if (mask) mask[slot] = 1;
-      } else {
-        AM[base + k] = static_cast<int32_t>(row);
-        AK[base + k] = col;
-        if (AV) AV[base + k] = vals[j];
+      const uint32_t tl = __shfl_up_sync(0xffffffffu, ilo, o);
+      const uint32_t th = __shfl_up_sync(0xffffffffu, ihi, o);
+      if (lane >= o) {
+        ilo += tl;
+        ihi += th;
       }
-      last_col = col;
-      ++k;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    // the lane holding the row's last nonzero so far
-    const unsigned has = __ballot_sync(0xffffffffu, mine > 0);
-    if (has) last_col = __shfl_sync(0xffffffffu, last_col, 31 - __clz(has));
-    k0 += total;
+    const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
+    const uint32_t elo = ilo - plo, ehi = ihi - phi;  // exclusive
+    int my_last = -1;
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const uint32_t tot_f = u < 2 ? tlo : thi, ex_f = u < 2 ? elo : ehi;
+      const int sh = 16 * (u & 1);
+      const int total = static_cast<int>((tot_f >> sh) & 0xFFFFu);
+      if (total == 0) continue;  // warp-uniform
+      int64_t k = k0 + static_cast<int>((ex_f >> sh) & 0xFFFFu);
+      const int64_t c = cb + u * 32 * V;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (!nz<T>(vals[u][j])) continue;
+        const int col = static_cast<int>(c + j);
+        if (mode == 0) {  // k < 2^31 (checked at plan time): 32-bit division
+          const int k32 = static_cast<int>(k), g32 = static_cast<int>(g);
+          const int64_t slot = (base + k32 / g32) * g + k32 % g32;
+          AK[slot] = col;
+          if (AV) AV[slot] = vals[u][j];
+          if (mask) mask[slot] = 1;
+        } else {
+          AM[base + k] = static_cast<int32_t>(row);
+          AK[base + k] = col;
+          if (AV) AV[base + k] = vals[u][j];
+        }
+        my_last = col;
+        ++k;
+      }
+      k0 += total;
+    }
+    // the row's last nonzero so far: the largest column any lane wrote
+    const int bl = __reduce_max_sync(0xffffffffu, my_last);
+    if (bl >= 0) last_col = bl;
+    }
   }
-  if (mode == 0) {
+  if (mode == 0 && last_seg) {
     const int64_t ng = (n + g - 1) / g;
     for (int64_t j = lane; j < ng; j += 32) AM[base + j] = static_cast<int32_t>(row);
     const int64_t real_last = n - (ng - 1) * g;  // real entries in the last group
@@ -688,6 +770,8 @@ struct ixb_pack {
   const void* dense = nullptr;
   int64_t rows = 0, cols = 0;
   ixb::Scratch<int32_t> occ, offs;  // per row: occupancy, group/row offsets
+  ixb::Scratch<int32_t> occ_seg;    // per (row, column segment) counts when nseg > 1
+  int64_t nseg = 1, seg = 0;
   // sorted-run engine
   std::vector<const int32_t*> coords;  // rank source coordinate arrays
   ixb::Scratch<int32_t> perm, run_incl, start, len, gofs;
@@ -703,31 +787,54 @@ struct ixb_pack {
 namespace ixb {
 namespace {
 
-template <typename T>
-void launch_row_count(const T* d, int64_t rows, int64_t cols, int32_t* occ, cudaStream_t s) {
-  constexpr int V = 16 / sizeof(T);
-  const int64_t grid = ceil_div(rows * 32, kTB);
-  if (rows == 0) return;
-  if (cols % V == 0 && reinterpret_cast<uintptr_t>(d) % 16 == 0) {
-    row_count_kernel<T, V><<<grid, kTB, 0, s>>>(d, rows, cols, occ);
-  } else {
-    row_count_kernel<T, 1><<<grid, kTB, 0, s>>>(d, rows, cols, occ);
-  }
-  IXB_LAUNCH_CHECK("row_count_kernel");
+// Segment width of the count/pack warps: whole chunks of 32 * V columns,
+// at least 8 of them, and at most 32 segments per row.
+void row_segments(int64_t cols, int V, int64_t* nseg, int64_t* seg) {
+  const int64_t chunk = 32 * static_cast<int64_t>(V);
+  int64_t sc = 8 * chunk;
+  const int64_t need = ceil_div(ceil_div(cols, 32), chunk) * chunk;
+  if (need > sc) sc = need;
+  *seg = sc;
+  *nseg = cols > 0 ? ceil_div(cols, sc) : 1;
 }
 
 template <typename T>
-void launch_row_pack(const T* d, int64_t rows, int64_t cols, const int32_t* occ,
-                     const int32_t* offs, int64_t g, int mode, int32_t* AM, int32_t* AK, T* AV,
-                     uint8_t* mask, cudaStream_t s) {
+void launch_row_count(const T* d, ixb_pack* P) {
   constexpr int V = 16 / sizeof(T);
-  const int64_t grid = ceil_div(rows * 32, kTB);
-  if (rows == 0) return;
-  if (cols % V == 0 && reinterpret_cast<uintptr_t>(d) % 16 == 0) {
-    row_pack_kernel<T, V><<<grid, kTB, 0, s>>>(d, rows, cols, occ, offs, g, mode, AM, AK, AV, mask);
-  } else {
-    row_pack_kernel<T, 1><<<grid, kTB, 0, s>>>(d, rows, cols, occ, offs, g, mode, AM, AK, AV, mask);
+  const bool vec = P->cols % V == 0 && reinterpret_cast<uintptr_t>(d) % 16 == 0;
+  row_segments(P->cols, vec ? V : 1, &P->nseg, &P->seg);
+  if (P->rows == 0) return;
+  if (P->nseg > 1) {
+    P->occ_seg = Scratch<int32_t>(P->rows * P->nseg, P->s);
+    IXB_CUDA_CHECK(cudaMemsetAsync(P->occ.p, 0, P->rows * sizeof(int32_t), P->s));
   }
+  const int64_t grid = ceil_div(P->rows * P->nseg * 32, kTB);
+  if (vec)
+    row_count_kernel<T, V><<<grid, kTB, 0, P->s>>>(d, P->rows, P->cols, P->nseg, P->seg, P->occ.p,
+                                                   P->occ_seg.p);
+  else
+    row_count_kernel<T, 1><<<grid, kTB, 0, P->s>>>(d, P->rows, P->cols, P->nseg, P->seg, P->occ.p,
+                                                   P->occ_seg.p);
+  IXB_LAUNCH_CHECK("row_count_kernel");
+}
+
+// P's occupancy (and segments, when count_rows made them) over rows x cols of d.
+template <typename T>
+void launch_row_pack(const T* d, const ixb_pack* P, const int32_t* offs, int64_t g, int mode,
+                     int32_t* AM, int32_t* AK, T* AV, uint8_t* mask, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  if (P->rows == 0) return;
+  const bool vec = P->cols % V == 0 && reinterpret_cast<uintptr_t>(d) % 16 == 0;
+  // a plan whose occupancy came from elsewhere (block flags) has one segment
+  int64_t nseg = P->occ_seg.p ? P->nseg : 1, seg = P->occ_seg.p ? P->seg : P->cols;
+  if (seg < 1) seg = 1;
+  const int64_t grid = ceil_div(P->rows * nseg * 32, kTB);
+  if (vec)
+    row_pack_kernel<T, V><<<grid, kTB, 0, s>>>(d, P->rows, P->cols, nseg, seg, P->occ.p,
+                                               P->occ_seg.p, offs, g, mode, AM, AK, AV, mask);
+  else
+    row_pack_kernel<T, 1><<<grid, kTB, 0, s>>>(d, P->rows, P->cols, nseg, seg, P->occ.p,
+                                               P->occ_seg.p, offs, g, mode, AM, AK, AV, mask);
   IXB_LAUNCH_CHECK("row_pack_kernel");
 }
 
@@ -757,6 +864,13 @@ struct GroupsOf {
 // ceil(in / g) (g = 1: the counts themselves) in tiles of 8 per thread and
 // writes the total to out[n] — one launch instead of cub's init + scan.
 constexpr int kSmallScan = 1 << 16;
+__device__ __forceinline__ int groups_of(int occ, int64_t g) {
+  // ceil(occ / g), 32-bit: occ < 2^31
+  if (g > INT32_MAX) return occ > 0;
+  return static_cast<int>((static_cast<uint32_t>(occ) + static_cast<uint32_t>(g) - 1u) /
+                          static_cast<uint32_t>(g));
+}
+
 __device__ void block_scan_groups(const int32_t* in, int64_t n, int64_t g, int32_t* out,
                                   int* wsum /* smem [32] */) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -767,7 +881,7 @@ __device__ void block_scan_groups(const int32_t* in, int64_t n, int64_t g, int32
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t i = t0 + tid * 8 + q;
-      v[q] = i < n ? static_cast<int>((static_cast<int64_t>(in[i]) + g - 1) / g) : 0;
+      v[q] = i < n ? groups_of(in[i], g) : 0;
       mine += v[q];
     }
     int incl = mine;
@@ -803,67 +917,83 @@ __global__ void __launch_bounds__(1024) small_scan_kernel(const int32_t* in, int
   block_scan_groups(in, n, g, out, wsum);
 }
 
-// Short profiles, one launch and one host read for the whole plan step: the
-// occupancy statistics (S, and with g_req = 0 the tuner's as in
-// occ_stats_kernel), select() on the device (choose_group_size), then the
-// group offsets ceil(occ / g) scanned into out[0..n]. res = {g, S}.
-__global__ void __launch_bounds__(512) tune_scan_kernel(const int32_t* occ, int64_t n,
+// Sum over the CTA of a per-thread unsigned partial (REDUX per warp, then
+// warp 0 over the warps' sums in 64 bits); the result is valid in thread 0.
+__device__ unsigned long long block_sum(unsigned v, unsigned long long* part /* smem [32] */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = __reduce_add_sync(0xffffffffu, v);
+  if (lane == 0) part[w] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (w == 0) {
+    t = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  __syncthreads();
+  return t;
+}
+
+// Short profiles, one launch and one host read for the whole plan step:
+// S, the non-empty count and the maximum occupancy; with g_req = 0 the
+// tuner's candidates (tuner_candidates, the host's function) and, when they
+// differ, F(lo) and F(hi) = sum ceil(occ / g) for just those two (select():
+// cost (g + 1) F(g), the smaller wins, lo on a tie — tuner.cpp:100-118);
+// then the group offsets ceil(occ / g) scanned into out[0..n]. res = {g, S}.
+__global__ void __launch_bounds__(1024) tune_scan_kernel(const int32_t* occ, int64_t n,
                                                          int64_t extent, int count_empty_rows,
                                                          int64_t g_req, int32_t* out,
                                                          int64_t* res) {
-  __shared__ unsigned long long part[32][35];
-  __shared__ OccStats st;
+  __shared__ unsigned long long part[32];
   __shared__ int wsum[32];
+  __shared__ int64_t cand[2];
   __shared__ int64_t g_s;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  unsigned S = 0, nz = 0, mx = 0, grp[32] = {};
-  const bool tune = g_req == 0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  unsigned S = 0, nz = 0, mx = 0;
   for (int64_t r = tid; r < n; r += blockDim.x) {
     const unsigned o = static_cast<unsigned>(occ[r]);
     S += o;
     nz += o > 0;
     mx = o > mx ? o : mx;
-    if (tune) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) grp[i] += static_cast<unsigned>(
-          (static_cast<unsigned long long>(o) + (1ull << i) - 1) >> i);
-    }
   }
-  S = __reduce_add_sync(0xffffffffu, S);
-  nz = __reduce_add_sync(0xffffffffu, nz);
+  const unsigned long long tS = block_sum(S, part);
+  const unsigned long long tnz = block_sum(nz, part);
   mx = __reduce_max_sync(0xffffffffu, mx);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) grp[i] = __reduce_add_sync(0xffffffffu, grp[i]);
-  if (lane == 0) {
-    part[w][0] = S;
-    part[w][1] = nz;
-    part[w][2] = mx;
-  }
-#pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if (lane == i) part[w][3 + i] = grp[i];
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  if (tid < 35) {
-    unsigned long long v = 0;
-    for (int k = 0; k < nw; ++k) {
-      const unsigned long long x = part[k][tid];
-      v = tid == 2 ? (x > v ? x : v) : v + x;
-    }
-    if (tid == 0) st.S = v;
-    else if (tid == 1) st.nonzero = v;
-    else if (tid == 2) st.maxocc = v;
-    else st.groups_pow2[tid - 3] = v;
-  }
+  if (lane == 0) part[tid >> 5] = mx;
   __syncthreads();
   if (tid == 0) {
-    g_s = tune ? choose_group_size(st, extent, count_empty_rows, nullptr, nullptr, nullptr,
-                                   nullptr)
-               : g_req;
-    res[0] = g_s;
-    res[1] = static_cast<int64_t>(st.S);
+    unsigned long long m = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = part[w] > m ? part[w] : m;
+    int64_t lo = g_req, hi = g_req;
+    if (g_req == 0) {
+      double gs;
+      tuner_candidates(tS, tnz, m, extent, count_empty_rows, &gs, &lo, &hi);
+    }
+    cand[0] = lo;
+    cand[1] = hi;
+    g_s = lo;
+    res[1] = static_cast<int64_t>(tS);
   }
   __syncthreads();
+  const int64_t lo = cand[0], hi = cand[1];
+  if (lo != hi) {  // the tuner's two candidates (powers of two)
+    const int sl = __ffsll(lo) - 1, shh = __ffsll(hi) - 1;
+    unsigned fl = 0, fh = 0;
+    for (int64_t r = tid; r < n; r += blockDim.x) {
+      const unsigned long long o = static_cast<unsigned>(occ[r]);
+      fl += static_cast<unsigned>((o + static_cast<unsigned long long>(lo) - 1) >> sl);
+      fh += static_cast<unsigned>((o + static_cast<unsigned long long>(hi) - 1) >> shh);
+    }
+    const unsigned long long Fl = block_sum(fl, part);
+    const unsigned long long Fh = block_sum(fh, part);
+    if (tid == 0) {
+      const double cl = static_cast<double>((lo + 1) * static_cast<int64_t>(Fl));
+      const double ch = static_cast<double>((hi + 1) * static_cast<int64_t>(Fh));
+      g_s = ch < cl ? hi : lo;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) res[0] = g_s;
   block_scan_groups(occ, n, g_s, out, wsum);
 }
 
@@ -883,7 +1013,7 @@ bool tune_and_scan(const int32_t* counts, int64_t n, int64_t extent, int count_e
                    int64_t* G) {
   if (n == 0 || n > kSmallScan) return false;
   Scratch<int64_t> res(2, s);
-  tune_scan_kernel<<<1, 512, 0, s>>>(counts, n, extent, count_empty_rows, g_req, out, res.p);
+  tune_scan_kernel<<<1, 1024, 0, s>>>(counts, n, extent, count_empty_rows, g_req, out, res.p);
   IXB_LAUNCH_CHECK("tune_scan_kernel");
   int64_t h[2];
   int32_t total = 0;
@@ -914,7 +1044,7 @@ void count_rows(ixb_pack* P) {
   P->occ = Scratch<int32_t>(P->rows + 1, P->s);
   dispatch_dense(P->dtype, [&](auto tag) {
     using T = decltype(tag);
-    launch_row_count(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->s);
+    launch_row_count(static_cast<const T*>(P->dense), P);
   });
 }
 
@@ -944,8 +1074,8 @@ void plan_dense_rows(ixb_pack* P, int64_t g_req, int64_t* g_out, bool have_occ =
 
 template <typename T>
 void pack_dense_rows_t(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask) {
-  launch_row_pack(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p, P->g, 0,
-                  AM, AK, static_cast<T*>(AV), mask, P->s);
+  launch_row_pack(static_cast<const T*>(P->dense), P, P->offs.p, P->g, 0, AM, AK,
+                  static_cast<T*>(AV), mask, P->s);
 }
 
 void pack_dense_rows(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uint8_t* mask) {
@@ -1099,8 +1229,8 @@ int ixb_dense_to_coo_pack(ixb_pack* P, int32_t* row_coord, int32_t* col_coord, v
     P->s = reinterpret_cast<cudaStream_t>(stream);
     dispatch_dense(P->dtype, [&](auto tag) {
       using T = decltype(tag);
-      launch_row_pack(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p, 1,
-                      1, row_coord, col_coord, static_cast<T*>(values), nullptr, P->s);
+      launch_row_pack(static_cast<const T*>(P->dense), P, P->offs.p, 1, 1, row_coord, col_coord,
+                      static_cast<T*>(values), nullptr, P->s);
     });
   });
 }
@@ -1162,8 +1292,8 @@ int ixb_dense_groupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t 
       P->coo_c = Scratch<int32_t>(P->nnz, P->s);
       dispatch_dense(dtype, [&](auto tag) {
         using T = decltype(tag);
-        launch_row_pack(static_cast<const T*>(dense), rows, cols, P->occ.p, P->offs.p, 1, 1,
-                        P->coo_r.p, P->coo_c.p, static_cast<T*>(nullptr), nullptr, P->s);
+        launch_row_pack(static_cast<const T*>(dense), P.get(), P->offs.p, 1, 1, P->coo_r.p,
+                        P->coo_c.p, static_cast<T*>(nullptr), nullptr, P->s);
       });
       P->type = 3;
       P->rank = 2;
@@ -1188,9 +1318,8 @@ int ixb_dense_groupcoo_pack(ixb_pack* P, int32_t* AM, int32_t* AK, void* AV, uin
       Scratch<char> vals(P->nnz * dense_bytes(P->dtype), P->s);
       dispatch_dense(P->dtype, [&](auto tag) {
         using T = decltype(tag);
-        launch_row_pack(static_cast<const T*>(P->dense), P->rows, P->cols, P->occ.p, P->offs.p,
-                        1, 1, P->coo_r.p, P->coo_c.p, reinterpret_cast<T*>(vals.p), nullptr,
-                        P->s);
+        launch_row_pack(static_cast<const T*>(P->dense), P, P->offs.p, 1, 1, P->coo_r.p,
+                        P->coo_c.p, reinterpret_cast<T*>(vals.p), nullptr, P->s);
       });
       int32_t* mo[1] = {AK};
       pack_sorted_runs(P, vals.p, P->dtype, AM, mo, AV, mask);
@@ -1264,9 +1393,8 @@ int ixb_blockgroupcoo_plan(const void* dense, int dtype, int64_t rows, int64_t c
       I->nnz = groups_scan_total(I->occ.p, I->rows, 1, I->offs.p, I->s);
       I->coo_r = Scratch<int32_t>(I->nnz, I->s);
       I->coo_c = Scratch<int32_t>(I->nnz, I->s);
-      launch_row_pack(static_cast<const uint8_t*>(I->dense), I->rows, I->cols, I->occ.p,
-                      I->offs.p, 1, 1, I->coo_r.p, I->coo_c.p, static_cast<uint8_t*>(nullptr),
-                      nullptr, I->s);
+      launch_row_pack(static_cast<const uint8_t*>(I->dense), I.get(), I->offs.p, 1, 1,
+                      I->coo_r.p, I->coo_c.p, static_cast<uint8_t*>(nullptr), nullptr, I->s);
       I->type = 3;
       I->rank = 2;
       I->coords = {I->coo_r.p, I->coo_c.p};

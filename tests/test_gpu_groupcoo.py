@@ -39,7 +39,8 @@ def f32(x):
 @pytest.mark.parametrize("kind", [0, 1])
 def test_dense_to_coo_bit_exact(P, ixo, kind):
     rng = ixo.Rng(11)
-    for rows, cols, d in ((1, 1, 1.0), (9, 7, 0.3), (33, 130, 0.1), (64, 64, 0.0), (5, 1000, 0.01)):
+    for rows, cols, d in ((1, 1, 1.0), (9, 7, 0.3), (33, 130, 0.1), (64, 64, 0.0), (5, 1000, 0.01),
+                          (6, 5000, 0.002), (3, 40001, 0.0003)):  # multi-segment rows
         a = ixo.synth_sparse_matrix(rng, rows, cols, d, kind)
         r, c, v = P.dense_to_coo(dev(a, torch.float32))
         wr, wc, wv = ixo.dense_to_coo(a)
@@ -51,7 +52,8 @@ def test_dense_to_coo_bit_exact(P, ixo, kind):
 @pytest.mark.parametrize("group_dim", [0, 1])
 def test_dense_groupcoo_bit_exact(P, ixo, group_dim):
     rng = ixo.Rng(5)
-    for rows, cols, d in ((4, 4, 0.5), (17, 29, 0.2), (100, 64, 0.05), (3, 3, 0.0), (40, 1, 0.7)):
+    for rows, cols, d in ((4, 4, 0.5), (17, 29, 0.2), (100, 64, 0.05), (3, 3, 0.0), (40, 1, 0.7),
+                          (7, 5000, 0.001), (2, 40000, 0.0002)):  # rows of several segments
         a = ixo.synth_sparse_matrix(rng, rows, cols, d)
         a32 = f32(a)
         r, c, v = ixo.dense_to_coo(a32)
