@@ -311,6 +311,36 @@ __global__ void __launch_bounds__(256, 4) row_pack_kernel(const T* __restrict__ 
     last_seg = __ballot_sync(0xffffffffu, lane > sg && cs > 0) == 0;
   }
   int last_col = 0;
+  // The compacted entries go through a per-warp shared staging buffer and
+  // leave as contiguous runs (each lane-level store a whole sector's worth
+  // per warp): scattered per-lane stores made the pack L2-store-bound.
+  constexpr int kPerBatch = kB * 32 * V;
+  constexpr bool kChunkFlush = kPerBatch > 512;
+  constexpr int kStage = kChunkFlush ? 32 * V : kPerBatch;
+  __shared__ int32_t s_col[kTB / 32][kStage];
+  __shared__ T s_val[kTB / 32][kStage];
+  const int wib = threadIdx.x >> 5;
+  int32_t* st_col = s_col[wib];
+  T* st_val = s_val[wib];
+  auto flush = [&](int& staged) {
+    __syncwarp();
+    for (int r = lane; r < staged; r += 32) {
+      const int64_t k = k0 + r;
+      if (mode == 0) {  // slot (base + k / g) * g + k % g = base * g + k
+        const int64_t slot = base * g + k;
+        AK[slot] = st_col[r];
+        if (AV) AV[slot] = st_val[r];
+        if (mask) mask[slot] = 1;
+      } else {
+        AM[base + k] = static_cast<int32_t>(row);
+        AK[base + k] = st_col[r];
+        if (AV) AV[base + k] = st_val[r];
+      }
+    }
+    __syncwarp();
+    k0 += staged;
+    staged = 0;
+  };
   for (bool first = true; cb - lane * V < c_hi; cb += kB * 32 * V, first = false) {
     if (!first) load_batch(vals, cb);
     // one warp scan for the kB chunks: their per-lane counts packed as
@@ -324,8 +354,7 @@ __global__ void __launch_bounds__(256, 4) row_pack_kernel(const T* __restrict__ 
     }
     const uint32_t plo = static_cast<uint32_t>(cnt[0]) | (static_cast<uint32_t>(cnt[1]) << 16);
     const uint32_t phi = static_cast<uint32_t>(cnt[2]) | (static_cast<uint32_t>(cnt[3]) << 16);
-    const bool any = __any_sync(0xffffffffu, (plo | phi) != 0);  // else an all-zero batch
-    if (any) {
+    if (!__any_sync(0xffffffffu, (plo | phi) != 0)) continue;  // an all-zero batch
     uint32_t ilo = plo, ihi = phi;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -339,38 +368,31 @@ __global__ void __launch_bounds__(256, 4) row_pack_kernel(const T* __restrict__ 
     const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
     const uint32_t elo = ilo - plo, ehi = ihi - phi;  // exclusive
     int my_last = -1;
+    int staged = 0;  // entries staged since the last flush (warp-uniform)
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
       const uint32_t tot_f = u < 2 ? tlo : thi, ex_f = u < 2 ? elo : ehi;
       const int sh = 16 * (u & 1);
       const int total = static_cast<int>((tot_f >> sh) & 0xFFFFu);
       if (total == 0) continue;  // warp-uniform
-      int64_t k = k0 + static_cast<int>((ex_f >> sh) & 0xFFFFu);
+      int r = staged + static_cast<int>((ex_f >> sh) & 0xFFFFu);
       const int64_t c = cb + u * 32 * V;
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         if (!nz<T>(vals[u][j])) continue;
         const int col = static_cast<int>(c + j);
-        if (mode == 0) {  // k < 2^31 (checked at plan time): 32-bit division
-          const int k32 = static_cast<int>(k), g32 = static_cast<int>(g);
-          const int64_t slot = (base + k32 / g32) * g + k32 % g32;
-          AK[slot] = col;
-          if (AV) AV[slot] = vals[u][j];
-          if (mask) mask[slot] = 1;
-        } else {
-          AM[base + k] = static_cast<int32_t>(row);
-          AK[base + k] = col;
-          if (AV) AV[base + k] = vals[u][j];
-        }
+        st_col[r] = col;
+        st_val[r] = vals[u][j];
         my_last = col;
-        ++k;
+        ++r;
       }
-      k0 += total;
+      staged += total;
+      if (kChunkFlush || u == kB - 1) flush(staged);
     }
+    if (!kChunkFlush && staged) flush(staged);
     // the row's last nonzero so far: the largest column any lane wrote
     const int bl = __reduce_max_sync(0xffffffffu, my_last);
     if (bl >= 0) last_col = bl;
-    }
   }
   if (mode == 0 && last_seg) {
     const int64_t ng = (n + g - 1) / g;
@@ -660,7 +682,7 @@ __global__ void __launch_bounds__(kTB) block_row_pack_kernel(
     __syncthreads();
     for (int i = tid; i < tot; i += kTB) {
       const int64_t kk = k0 + i;
-      const int64_t slot = (base + kk / g) * g + kk % g;
+      const int64_t slot = base * g + kk;  // = (base + kk / g) * g + kk % g
       AK[slot] = list[i];
       if (mask) mask[slot] = 1;
     }
@@ -668,7 +690,6 @@ __global__ void __launch_bounds__(kTB) block_row_pack_kernel(
     if (AV) {
       // 4 independent 16-byte loads in flight per thread before their stores
       const int nchunks = tot * cpb;
-      const int g32 = static_cast<int>(g);
       for (int e0 = tid; e0 < nchunks; e0 += 4 * kTB) {
         uint4 v[4];
         T* dst[4];
@@ -681,7 +702,7 @@ __global__ void __launch_bounds__(kTB) block_row_pack_kernel(
             const int i = e / cpb, c = e - i * cpb;
             const int r = c / cpr, j = (c - r * cpr) * V;
             const int kk = static_cast<int>(k0) + i;
-            const int64_t slot = (base + kk / g32) * g + kk % g32;
+            const int64_t slot = base * g + kk;  // = (base + kk / g) * g + kk % g
             const int64_t si = br * bm + r, sj = static_cast<int64_t>(list[i]) * bk + j;
             if (si < rows && sj < cols)
               v[u] = __ldg(reinterpret_cast<const uint4*>(dense + si * cols + sj));

@@ -20,6 +20,12 @@ if which in ("all", "k1"):
     A = S.synth_sparse_matrix(rng, 4096, 4096, 0.01, S.REAL, torch.float32).to(dev)
     for _ in range(2):
         P.dense_to_groupcoo(A, g=0)
+if which == "k1big":  # cfg3 d = 0.30: 16384^2 fp32
+    rng = S.Rng(1)
+    S.synth_dense(rng, (16384, 256), S.REAL, torch.float32)
+    A = S.synth_sparse_matrix(rng, 16384, 16384, 0.30, S.REAL, torch.float32).to(dev)
+    for _ in range(2):
+        P.dense_to_groupcoo(A, g=0)
 if which in ("all", "k2"):
     rng = S.Rng(1)
     S.synth_dense(rng, (512, 16, 512), S.REAL, torch.bfloat16)
