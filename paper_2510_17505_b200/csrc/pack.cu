@@ -17,6 +17,7 @@
 // (formats.cpp:155-160, 454-468).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
 #include <cmath>
@@ -421,14 +422,41 @@ __global__ void occupancy_kernel(const int32_t* c, int64_t n, int64_t ext, int32
     for (int64_t b = threadIdx.x; b < ext; b += blockDim.x) h[b] = 0;
     __syncthreads();
   }
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t v = c[i];
-    if (v >= 0 && v < ext) {
-      if (small) atomicAdd(h + v, 1);
-      else atomicAdd(o + v, 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  auto add = [&](int32_t v, int cnt) {
+    if (v < 0 || v >= ext) return;
+    if (small) atomicAdd(h + v, cnt);
+    else atomicAdd(o + v, cnt);
+  };
+  int64_t done = 0;
+  if (small && (reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+    // 16-byte loads, whole warps (the lanes stay converged): a warp whose
+    // 128 values are all equal (sorted input: nearly every warp) adds once,
+    // a lane whose 4 values are equal adds once
+    const int64_t n4 = n / 4;
+    for (int64_t base = (tid >> 5) * 32; base < n4; base += (nthreads >> 5) * 32) {
+      const int64_t q = base + lane;
+      const int4 x = q < n4 ? reinterpret_cast<const int4*>(c)[q] : make_int4(-1, -1, -1, -1);
+      const int32_t v0 = __shfl_sync(0xffffffffu, x.x, 0);
+      const bool eq = x.x == x.y && x.y == x.z && x.z == x.w;  // the lane's four values
+      if (__all_sync(0xffffffffu, eq && x.x == v0 && q < n4)) {
+        if (lane == 0) add(v0, 128);
+      } else if (q < n4) {
+        if (eq) {
+          add(x.x, 4);
+        } else {
+          add(x.x, 1);
+          add(x.y, 1);
+          add(x.z, 1);
+          add(x.w, 1);
+        }
+      }
     }
+    done = n4 * 4;
   }
+  for (int64_t i = done + tid; i < n; i += nthreads) add(c[i], 1);
   if (small) {
     __syncthreads();
     for (int64_t b = threadIdx.x; b < ext; b += blockDim.x)
@@ -460,7 +488,7 @@ __global__ void brute_cost_kernel(const int32_t* occ, int64_t n, int64_t maxocc,
 void launch_occupancy(const int32_t* coord, int64_t nnz, int64_t extent, int32_t* occ,
                       cudaStream_t s) {
   int64_t grid = ceil_div(nnz, kTB);
-  if (extent <= kOccSmemBins && grid > 2 * sm_count()) grid = 2 * sm_count();
+  if (extent <= kOccSmemBins && grid > 6 * sm_count()) grid = 6 * sm_count();
   occupancy_kernel<<<static_cast<unsigned>(grid), kTB, 0, s>>>(coord, nnz, extent, occ);
   IXB_LAUNCH_CHECK("occupancy_kernel");
 }
@@ -476,17 +504,21 @@ __global__ void gather_key(const int32_t* coord, const int32_t* perm, int64_t n,
   if (i < n) key[i] = coord[perm[i]];
 }
 
-__global__ void head_flags(const int32_t* gcoord, const int32_t* perm, int64_t n, int32_t* flag) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t a = gcoord[perm ? perm[i] : i];
-  flag[i] = (i == 0 || a != gcoord[perm ? perm[i - 1] : i - 1]) ? 1 : 0;
-}
+// Head flag of sorted position i (a run of equal group coordinate starts
+// there), computed inside the scan's input iterator: no flag array.
+struct HeadFlag {
+  const int32_t* gcoord;
+  const int32_t* perm;
+  __host__ __device__ int operator()(int64_t i) const {
+    if (i == 0) return 1;
+    return gcoord[perm ? perm[i] : i] != gcoord[perm ? perm[i - 1] : i - 1] ? 1 : 0;
+  }
+};
 
-__global__ void run_starts(const int32_t* flag, const int32_t* run_incl, int64_t n,
-                           int32_t* start) {
+__global__ void run_starts(const int32_t* run_incl, int64_t n, int32_t* start) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n && flag[i]) start[run_incl[i] - 1] = static_cast<int32_t>(i);
+  if (i < n && (i == 0 || run_incl[i] != run_incl[i - 1]))
+    start[run_incl[i] - 1] = static_cast<int32_t>(i);
 }
 
 __global__ void run_lengths(const int32_t* start, int64_t R, int64_t n, int32_t* len) {
@@ -496,7 +528,8 @@ __global__ void run_lengths(const int32_t* start, int64_t R, int64_t n, int32_t*
 
 struct RunPackArgs {
   const int32_t* perm;      // sorted pos -> source (null = identity)
-  const int32_t* run_incl;  // inclusive run count per sorted pos (run id + 1)
+  const int32_t* run_incl;  // inclusive run count per sorted pos (run id + 1); null:
+                            // runs indexed by group coordinate value
   const int32_t* start;     // [R]
   const int32_t* len;       // [R]
   const int32_t* gofs;      // [R] exclusive group offsets
@@ -512,23 +545,31 @@ struct RunPackArgs {
   int32_t* gout;  // group coordinate output [G]
 };
 
-__global__ void run_pack_elems(RunPackArgs a) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  const int64_t r = a.run_incl[i] - 1;
-  const int64_t k = i - a.start[r];
-  const int64_t slot = (a.gofs[r] + k / a.g) * a.g + k % a.g;
-  const int64_t src = a.perm ? a.perm[i] : i;
-  for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][src];
-  if (a.vbytes == 8) {
-    static_cast<unsigned long long*>(a.vout)[slot] =
-        static_cast<const unsigned long long*>(a.vals)[src];
-  } else if (a.vbytes == 4) {
-    static_cast<float*>(a.vout)[slot] = static_cast<const float*>(a.vals)[src];
-  } else if (a.vbytes == 2) {
-    static_cast<__nv_bfloat16*>(a.vout)[slot] = static_cast<const __nv_bfloat16*>(a.vals)[src];
+// kPackElems consecutive-by-stride entries per thread: their independent
+// loads are in flight together.
+constexpr int kPackElems = 4;
+__global__ void __launch_bounds__(kTB) run_pack_elems(RunPackArgs a) {
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTB * kPackElems + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kPackElems; ++u) {
+    const int64_t i = i0 + u * kTB;
+    if (i >= a.n) break;
+    // runs by rank (run_incl) or, for canonical small-extent input, by value
+    const int64_t r = a.run_incl ? a.run_incl[i] - 1 : a.gcoord[i];
+    const int64_t k = i - a.start[r];
+    const int64_t slot = static_cast<int64_t>(a.gofs[r]) * a.g + k;  // = (gofs + k / g) * g + k % g
+    const int64_t src = a.perm ? a.perm[i] : i;
+    for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][src];
+    if (a.vbytes == 8) {
+      static_cast<unsigned long long*>(a.vout)[slot] =
+          static_cast<const unsigned long long*>(a.vals)[src];
+    } else if (a.vbytes == 4) {
+      static_cast<float*>(a.vout)[slot] = static_cast<const float*>(a.vals)[src];
+    } else if (a.vbytes == 2) {
+      static_cast<__nv_bfloat16*>(a.vout)[slot] = static_cast<const __nv_bfloat16*>(a.vals)[src];
+    }
+    if (a.mask) a.mask[slot] = 1;
   }
-  if (a.mask) a.mask[slot] = 1;
 }
 
 // Per run: its group coordinates and the pad slots of its last group.
@@ -540,6 +581,7 @@ __global__ void run_pack_runs(RunPackArgs a, int cta) {
   if (r >= a.R) return;
   const int64_t t0 = cta ? threadIdx.x : 0, dt = cta ? blockDim.x : 1;
   const int64_t len = a.len[r];
+  if (len == 0) return;  // a value with no entries (value-indexed runs)
   const int64_t ng = (len + a.g - 1) / a.g;
   const int64_t g0 = a.gofs[r];
   const int64_t first = a.start[r], last = first + len - 1;
@@ -1134,16 +1176,41 @@ void plan_sorted_runs(ixb_pack* P, bool identity_order, int64_t g_req, int64_t e
     }
   }
   const int32_t* gcoord = P->coords[P->group_dim];
-  Scratch<int32_t> flag(n + 1, s);
+  if (identity_order && n > 0 && extent > 0 && extent <= kOccSmemBins) {
+    // Canonical input over a small extent (the 27 offsets of a kernel map,
+    // the paths of a CG table): the runs are the values in order, so their
+    // lengths are the value histogram and their starts its exclusive scan —
+    // no pass over the entries beyond the histogram. Runs are indexed by
+    // value (empty values give no groups); tune_scan's S = the in-range
+    // count proves every coordinate was in [0, extent).
+    P->len = Scratch<int32_t>(extent + 1, s);
+    IXB_CUDA_CHECK(cudaMemsetAsync(P->len.p, 0, (extent + 1) * sizeof(int32_t), s));
+    launch_occupancy(gcoord, n, extent, P->len.p, s);
+    P->start = Scratch<int32_t>(extent + 1, s);
+    small_scan_kernel<<<1, 1024, 0, s>>>(P->len.p, extent, 1, P->start.p);
+    IXB_LAUNCH_CHECK("small_scan_kernel");
+    P->gofs = Scratch<int32_t>(extent + 1, s);
+    int64_t S = 0;
+    if (tune_and_scan(P->len.p, extent, extent, count_empty_rows, g_req, P->gofs.p, s, &P->g, &S,
+                      &P->G) &&
+        S == n) {
+      P->R = extent;
+      if (g_out) *g_out = P->g;
+      return;
+    }
+    P->len = Scratch<int32_t>();  // out-of-range coordinates: the general path
+    P->start = Scratch<int32_t>();
+    P->gofs = Scratch<int32_t>();
+  }
   P->run_incl = Scratch<int32_t>(n + 1, s);
   if (n > 0) {
-    head_flags<<<ceil_div(n, kTB), kTB, 0, s>>>(gcoord, P->perm.p, n, flag.p);
-    IXB_LAUNCH_CHECK("head_flags");
+    auto flags = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                 HeadFlag{gcoord, P->perm.p});
     size_t tb = 0;
-    IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.p, P->run_incl.p,
+    IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, flags, P->run_incl.p,
                                                  static_cast<int>(n), s));
     Scratch<char> tmp(tb, s);
-    IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.p, tb, flag.p, P->run_incl.p,
+    IXB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.p, tb, flags, P->run_incl.p,
                                                  static_cast<int>(n), s));
     note_launch();
     int32_t R = 0;
@@ -1155,7 +1222,7 @@ void plan_sorted_runs(ixb_pack* P, bool identity_order, int64_t g_req, int64_t e
   P->start = Scratch<int32_t>(R + 1, s);
   P->len = Scratch<int32_t>(R + 1, s);
   if (n > 0) {
-    run_starts<<<ceil_div(n, kTB), kTB, 0, s>>>(flag.p, P->run_incl.p, n, P->start.p);
+    run_starts<<<ceil_div(n, kTB), kTB, 0, s>>>(P->run_incl.p, n, P->start.p);
     IXB_LAUNCH_CHECK("run_starts");
     run_lengths<<<ceil_div(R, kTB), kTB, 0, s>>>(P->start.p, R, n, P->len.p);
     IXB_LAUNCH_CHECK("run_lengths");
@@ -1200,7 +1267,7 @@ void pack_sorted_runs(ixb_pack* P, const void* vals, int dtype, int32_t* gout,
   a.mask = mask;
   a.gout = gout;
   if (a.n > 0) {
-    run_pack_elems<<<ceil_div(a.n, kTB), kTB, 0, P->s>>>(a);
+    run_pack_elems<<<ceil_div(a.n, kTB * kPackElems), kTB, 0, P->s>>>(a);
     IXB_LAUNCH_CHECK("run_pack_elems");
     if (a.R <= 4 * sm_count()) run_pack_runs<<<a.R, 128, 0, P->s>>>(a, 1);
     else run_pack_runs<<<ceil_div(a.R, kTB), kTB, 0, P->s>>>(a, 0);

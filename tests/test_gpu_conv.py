@@ -78,6 +78,43 @@ def test_group_coo_tensor_bit_exact(P, ixo):
                 np.testing.assert_array_equal(got.mask.cpu().numpy(), want["mask"])
 
 
+def test_group_coo_tensor_canonical_small_extent(P, ixo):
+    """canonical=True over small group extents: runs indexed by value (the
+    histogram fast path), values absent from the input, and a coordinate
+    out of range (falls back to the general run finder)."""
+    g_np = np.random.default_rng(4)
+    for it in range(12):
+        rank = int(g_np.integers(2, 4))
+        shape = [int(x) for x in g_np.integers(2, 12, rank)]
+        nnz = int(g_np.integers(1, 300))
+        gd = int(g_np.integers(0, rank))
+        coords = np.stack([g_np.integers(0, s, nnz) for s in shape]).astype(np.int64)
+        coords[gd] = np.where(coords[gd] % 3 == 1, 0, coords[gd])  # gaps in the group values
+        # canonical order: group dim, then the other dims ascending
+        keys = [coords[d] for d in reversed([d for d in range(rank) if d != gd])] + [coords[gd]]
+        coords = coords[:, np.lexsort(keys)]
+        vals = g_np.integers(-4, 5, nnz).astype(np.float64)
+        for g in (1, 4):
+            got = P.group_coo_tensor(shape, [cuda(c, torch.int32) for c in coords],
+                                     cuda(vals, torch.float32), gd, g, canonical=True)
+            want = ixo.group_coo_tensor(shape, coords, vals, gd, g)
+            np.testing.assert_array_equal(got.group_coord.cpu().numpy(), want["group_coord"])
+            for m in range(rank - 1):
+                np.testing.assert_array_equal(got.member_coords[m].cpu().numpy(),
+                                              want["member_coords"][m])
+            np.testing.assert_array_equal(got.values.double().cpu().numpy(), want["values"])
+            np.testing.assert_array_equal(got.mask.cpu().numpy(), want["mask"])
+    # a group coordinate beyond the declared extent: same result as canonical=False
+    coords = np.array([[0, 0, 2, 5], [1, 2, 0, 1]], np.int64)
+    vals = np.array([1.0, 2.0, 3.0, 4.0])
+    a = P.group_coo_tensor([3, 3], [cuda(c, torch.int32) for c in coords],
+                           cuda(vals, torch.float32), 0, 2, canonical=True)
+    b = P.group_coo_tensor([3, 3], [cuda(c, torch.int32) for c in coords],
+                           cuda(vals, torch.float32), 0, 2)
+    np.testing.assert_array_equal(a.group_coord.cpu().numpy(), b.group_coord.cpu().numpy())
+    np.testing.assert_array_equal(a.values.cpu().numpy(), b.values.cpu().numpy())
+
+
 def build_grouped_map(P, ixo, pts, g):
     """Device kernel map -> device group_coo_tensor(·, 2, g); checked vs oracle."""
     n = len(pts)
