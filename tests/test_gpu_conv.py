@@ -42,7 +42,11 @@ def test_kernel_map_bit_exact(P, ixo):
     from paper_2510_17505_b200 import synth as S
     cases = [random_voxels(0, 400, 6), random_voxels(1, 3000, 12), random_voxels(2, 50, 100),
              S.synth_voxel_shells(5000).numpy(), np.zeros((0, 3), np.int32),
-             np.array([[5, -7, 3]], np.int32)]
+             np.array([[5, -7, 3]], np.int32),
+             # flat and thin boxes (the occupancy-bitmap count pass's column edges)
+             np.array([[x, y, 0] for x in range(-3, 20) for y in range(9)], np.int32),
+             np.array([[2, 1, z] for z in range(-40, 40, 1)], np.int32),
+             random_voxels(3, 2000, 9)[:, [2, 0, 1]]]
     for pts in cases:
         mo, mi, mz = P.kernel_map(cuda(pts, torch.int32))
         wo, wi, wz = ixo.kernel_map(pts)
