@@ -232,7 +232,7 @@ class GroupCooWorkload:
     def e2e_step(self, P):
         # host buffers in, host C out: row-boundary chunks pipeline H2D / kernel / D2H
         AM, AK, AV, B = self.h_in
-        P.spmm_groupcoo_host(AM, AK, AV, B, self.h_out, accumulate=False, nchunks=2)
+        P.spmm_groupcoo_host(AM, AK, AV, B, self.h_out, accumulate=False, nchunks=0)
 
     def e2e_bytes(self):
         return sum(x.numel() * x.element_size() for x in self.h_in), \
@@ -346,7 +346,7 @@ class BlockGroupCooWorkload:
     def e2e_step(self, P):
         # host buffers in, host C out: row-boundary chunks pipeline H2D / kernel / D2H
         AM, AK, AV, B = self.h_in
-        P.spmm_blockgroupcoo_host(AM, AK, AV, B, self.h_out, accumulate=False, nchunks=2)
+        P.spmm_blockgroupcoo_host(AM, AK, AV, B, self.h_out, accumulate=False, nchunks=0)
 
     def e2e_bytes(self):
         return sum(x.numel() * x.element_size() for x in self.h_in), \

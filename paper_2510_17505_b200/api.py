@@ -409,7 +409,7 @@ def _host(t, dtype=None):
     return t.contiguous()
 
 
-def spmm_groupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=2, stream=None):
+def spmm_groupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=0, stream=None):
     """K3 with HOST buffers in and out (execute_mode's shape, driver.cpp:235-265):
     row-boundary chunks pipeline H2D, kernel and D2H on three streams; returns
     with C_out written. Bit-identical to spmm_groupcoo."""
@@ -422,7 +422,7 @@ def spmm_groupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=2
     return C_out
 
 
-def spmm_blockgroupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=2,
+def spmm_blockgroupcoo_host(AM, AK, AV, B, C_out, accumulate=True, flags=0, nchunks=0,
                             stream=None):
     """K4 with HOST buffers in and out (see spmm_groupcoo_host)."""
     AM, AK, AV, B = _host(AM, torch.int32), _host(AK, torch.int32), _host(AV), _host(B)

@@ -1,7 +1,8 @@
 // Host-buffer entry points of the SpMM evaluators (the shape the reference's
 // execute_mode has: host Tensors in, host result out — driver.cpp:235-265),
 // pipelined so the PCIe transfers overlap each other and the kernels:
-//   stream h2d : dense operand B, then the format of chunk 0, 1, ...
+//   stream h2d : dense operand B and the index arrays, then the values of
+//                chunk 0, 1, ...
 //   stream comp: (zero C) then the evaluator on chunk i once it has landed
 //   stream d2h : C rows of chunk i once its kernel is done
 // Chunks are contiguous group ranges cut at output-row boundaries
@@ -59,7 +60,14 @@ void run_pipelined(const int32_t* AM, const int32_t* AK, const void* AV, int64_t
                    int64_t slotbytes, const void* B, int64_t bbytes, float* C, int64_t MB,
                    int64_t rowbytes, int accumulate, int nchunks, bool check, int64_t K,
                    cudaStream_t s, Eval&& eval) {
-  if (nchunks < 1) nchunks = 1;
+  if (nchunks < 1) {
+    // auto: ~2 MB of transfers (values in + C rows out) per chunk, 2..8 chunks
+    // (tools/e2e_chunks.py: cfg1 best at 2, cfg2 at 8; each chunk costs a
+    // kernel launch and two copies)
+    const double mb = (static_cast<double>(G) * g * slotbytes + static_cast<double>(MB) * rowbytes) /
+                      (2.0 * 1024 * 1024);
+    nchunks = mb < 2 ? 2 : mb > 8 ? 8 : static_cast<int>(mb + 0.5);
+  }
   if (nchunks > G) nchunks = static_cast<int>(G < 1 ? 1 : G);
   std::vector<int64_t> bounds(nchunks + 1);
   if (ixb_shard_groups(AM, G, nchunks, bounds.data()) != IXB_OK)
@@ -73,6 +81,9 @@ void run_pipelined(const int32_t* AM, const int32_t* AK, const void* AV, int64_t
   IXB_CUDA_CHECK(cudaEventRecord(ready, s));
   IXB_CUDA_CHECK(cudaStreamWaitEvent(st.h2d, ready, 0));
   IXB_CUDA_CHECK(cudaMemcpyAsync(dB.p, B, bbytes, cudaMemcpyHostToDevice, st.h2d));
+  // the small index arrays whole (one copy each); only AV is cut per chunk
+  IXB_CUDA_CHECK(cudaMemcpyAsync(dAM.p, AM, G * 4, cudaMemcpyHostToDevice, st.h2d));
+  IXB_CUDA_CHECK(cudaMemcpyAsync(dAK.p, AK, G * g * 4, cudaMemcpyHostToDevice, st.h2d));
   if (accumulate)  // `+=` needs the caller's C; `=` starts from zeros
     IXB_CUDA_CHECK(cudaMemcpyAsync(dC.p, C, MB * rowbytes, cudaMemcpyHostToDevice, st.h2d));
   else
@@ -88,10 +99,6 @@ void run_pipelined(const int32_t* AM, const int32_t* AK, const void* AV, int64_t
     const int64_t g0 = bounds[i], g1 = bounds[i + 1];
     cudaEvent_t in = st.ev[2 + 2 * i], out = st.ev[3 + 2 * i];
     if (g1 > g0) {
-      IXB_CUDA_CHECK(cudaMemcpyAsync(dAM.p + g0, AM + g0, (g1 - g0) * 4, cudaMemcpyHostToDevice,
-                                     st.h2d));
-      IXB_CUDA_CHECK(cudaMemcpyAsync(dAK.p + g0 * g, AK + g0 * g, (g1 - g0) * g * 4,
-                                     cudaMemcpyHostToDevice, st.h2d));
       IXB_CUDA_CHECK(cudaMemcpyAsync(dAV.p + g0 * g * slotbytes,
                                      static_cast<const char*>(AV) + g0 * g * slotbytes,
                                      (g1 - g0) * g * slotbytes, cudaMemcpyHostToDevice, st.h2d));
@@ -135,10 +142,12 @@ int ixb_spmm_blockgroupcoo_host(const int32_t* AM, const int32_t* AK, const void
     auto s = reinterpret_cast<cudaStream_t>(stream);
     if (G < 0 || g < 1 || bm < 1 || bk < 1 || KB < 0 || N < 0 || MB < 0)
       fail(IXB_SHAPE, "ixb_spmm_blockgroupcoo: bad extents");
-    if (!sorted_host(AM, G)) nchunks = 1;  // one chunk: the evaluator sorts on the device
+    const bool sorted = sorted_host(AM, G);
+    if (!sorted) nchunks = 1;  // one chunk: the evaluator sorts on the device
     const int64_t slotbytes = bm * bk * 2, rowbytes = bm * N * 4;
     int rc_err = IXB_OK;
-    const int cflags = IXB_UNCHECKED | IXB_ASYNC | (nchunks > 1 ? IXB_GROUPS_SORTED : 0);
+    // sortedness was checked here on the host: the evaluator need not
+    const int cflags = IXB_UNCHECKED | IXB_ASYNC | (sorted ? IXB_GROUPS_SORTED : 0);
     run_pipelined(AM, AK, AV, G, g, slotbytes, B, KB * bk * N * 2, C, MB, rowbytes, accumulate,
                   nchunks, !(flags & IXB_UNCHECKED), KB, s,
                   [&](const int32_t* am, const int32_t* ak, const char* av, int64_t Gc,
@@ -158,9 +167,11 @@ int ixb_spmm_groupcoo_host(const int32_t* AM, const int32_t* AK, const float* AV
   return ixb_guard([&] {
     auto s = reinterpret_cast<cudaStream_t>(stream);
     if (G < 0 || g < 1 || K < 0 || N < 0 || M < 0) fail(IXB_SHAPE, "ixb_spmm_groupcoo: bad extents");
-    if (!sorted_host(AM, G)) nchunks = 1;
+    const bool sorted = sorted_host(AM, G);
+    if (!sorted) nchunks = 1;
     int rc_err = IXB_OK;
-    const int cflags = IXB_UNCHECKED | IXB_ASYNC | (nchunks > 1 ? IXB_GROUPS_SORTED : 0);
+    // sortedness was checked here on the host: the evaluator need not
+    const int cflags = IXB_UNCHECKED | IXB_ASYNC | (sorted ? IXB_GROUPS_SORTED : 0);
     run_pipelined(AM, AK, AV, G, g, 4, B, K * N * 4, C, M, N * 4, accumulate, nchunks,
                   !(flags & IXB_UNCHECKED), K, s,
                   [&](const int32_t* am, const int32_t* ak, const char* av, int64_t Gc,
