@@ -285,9 +285,10 @@ int ixb_tp_plan_run_host(ixb_tp_plan* plan, const void* X, const void* Y, const 
  * groups are cut into `nchunks` ranges at output-row boundaries: B is copied
  * first, then chunk i's format H2D, its kernel and its C rows D2H run on
  * three streams, so transfers overlap each other and the kernels (the small
- * index arrays go whole, right after B). nchunks <= 0 picks one chunk per
- * ~2 MB of values in + C rows out, 2..8 chunks. Results and errors are
- * bit-identical to the device-buffer calls. */
+ * index arrays go whole, right after B, when small next to the values).
+ * nchunks <= 0 picks 2 chunks for GroupCOO and one per ~2 MB of values in +
+ * C rows out (2..8) for BlockGroupCOO. Results and errors are bit-identical
+ * to the device-buffer calls. */
 int ixb_spmm_blockgroupcoo_host(const int32_t* AM, const int32_t* AK, const void* AV, int64_t G,
                                 int64_t g, int64_t bm, int64_t bk, const void* B, int64_t KB,
                                 int64_t N, float* C, int64_t MB, int accumulate, int flags,

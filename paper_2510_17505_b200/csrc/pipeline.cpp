@@ -61,12 +61,13 @@ void run_pipelined(const int32_t* AM, const int32_t* AK, const void* AV, int64_t
                    int64_t rowbytes, int accumulate, int nchunks, bool check, int64_t K,
                    cudaStream_t s, Eval&& eval) {
   if (nchunks < 1) {
-    // auto: ~2 MB of transfers (values in + C rows out) per chunk, 2..8 chunks
-    // (tools/e2e_chunks.py: cfg1 best at 2, cfg2 at 8; each chunk costs a
-    // kernel launch and two copies)
-    const double mb = (static_cast<double>(G) * g * slotbytes + static_cast<double>(MB) * rowbytes) /
-                      (2.0 * 1024 * 1024);
-    nchunks = mb < 2 ? 2 : mb > 8 ? 8 : static_cast<int>(mb + 0.5);
+    // auto (tools/e2e_chunks.py, bench e2e): BlockGroupCOO ~2 MB of values
+    // in + C rows out per chunk, 2..8 chunks (cfg2: 0.73 ms at 2, 0.65 at
+    // 8); GroupCOO 2 chunks (cfg1 and cfg3: more chunks measured slower —
+    // each costs a latency-bound K3 launch and its copies)
+    const double mb = (static_cast<double>(G) * g * (slotbytes + 4) +
+                       static_cast<double>(MB) * rowbytes) / (2.0 * 1024 * 1024);
+    nchunks = slotbytes < 64 || mb < 2 ? 2 : mb > 8 ? 8 : static_cast<int>(mb + 0.5);
   }
   if (nchunks > G) nchunks = static_cast<int>(G < 1 ? 1 : G);
   std::vector<int64_t> bounds(nchunks + 1);
@@ -81,9 +82,13 @@ void run_pipelined(const int32_t* AM, const int32_t* AK, const void* AV, int64_t
   IXB_CUDA_CHECK(cudaEventRecord(ready, s));
   IXB_CUDA_CHECK(cudaStreamWaitEvent(st.h2d, ready, 0));
   IXB_CUDA_CHECK(cudaMemcpyAsync(dB.p, B, bbytes, cudaMemcpyHostToDevice, st.h2d));
-  // the small index arrays whole (one copy each); only AV is cut per chunk
+  // AM whole (one small copy); AK whole too when it is small next to the
+  // values (BlockGroupCOO: 4 B per 512-B block), else per chunk with them
+  // (GroupCOO: as large as AV — uploading it first delays chunk 0)
+  const bool ak_whole = slotbytes >= 64;
   IXB_CUDA_CHECK(cudaMemcpyAsync(dAM.p, AM, G * 4, cudaMemcpyHostToDevice, st.h2d));
-  IXB_CUDA_CHECK(cudaMemcpyAsync(dAK.p, AK, G * g * 4, cudaMemcpyHostToDevice, st.h2d));
+  if (ak_whole)
+    IXB_CUDA_CHECK(cudaMemcpyAsync(dAK.p, AK, G * g * 4, cudaMemcpyHostToDevice, st.h2d));
   if (accumulate)  // `+=` needs the caller's C; `=` starts from zeros
     IXB_CUDA_CHECK(cudaMemcpyAsync(dC.p, C, MB * rowbytes, cudaMemcpyHostToDevice, st.h2d));
   else
@@ -99,6 +104,9 @@ void run_pipelined(const int32_t* AM, const int32_t* AK, const void* AV, int64_t
     const int64_t g0 = bounds[i], g1 = bounds[i + 1];
     cudaEvent_t in = st.ev[2 + 2 * i], out = st.ev[3 + 2 * i];
     if (g1 > g0) {
+      if (!ak_whole)
+        IXB_CUDA_CHECK(cudaMemcpyAsync(dAK.p + g0 * g, AK + g0 * g, (g1 - g0) * g * 4,
+                                       cudaMemcpyHostToDevice, st.h2d));
       IXB_CUDA_CHECK(cudaMemcpyAsync(dAV.p + g0 * g * slotbytes,
                                      static_cast<const char*>(AV) + g0 * g * slotbytes,
                                      (g1 - g0) * g * slotbytes, cudaMemcpyHostToDevice, st.h2d));
