@@ -344,9 +344,24 @@ __global__ void __launch_bounds__(kConvThreads, IXB_CONV_MINB)
   auto issue = [&](int k) {
     const int z = __fns(tmask, 0, k + 1);  // k-th used offset (warp-uniform)
     const int st = k % kUnitStages;
+    // yr[z] for the warp-uniform z: a uniform jump table, not a 28-way
+    // compare/select chain per offset (yr stays in registers)
     int y1 = 0;
-#pragma unroll
-    for (int j = 0; j < kOffPad; ++j) y1 = (j == z) ? yr[j] : y1;
+    switch (z) {
+#define IXB_YR_CASE(j) \
+  case j:              \
+    y1 = yr[j];        \
+    break;
+      IXB_YR_CASE(0) IXB_YR_CASE(1) IXB_YR_CASE(2) IXB_YR_CASE(3) IXB_YR_CASE(4)
+      IXB_YR_CASE(5) IXB_YR_CASE(6) IXB_YR_CASE(7) IXB_YR_CASE(8) IXB_YR_CASE(9)
+      IXB_YR_CASE(10) IXB_YR_CASE(11) IXB_YR_CASE(12) IXB_YR_CASE(13) IXB_YR_CASE(14)
+      IXB_YR_CASE(15) IXB_YR_CASE(16) IXB_YR_CASE(17) IXB_YR_CASE(18) IXB_YR_CASE(19)
+      IXB_YR_CASE(20) IXB_YR_CASE(21) IXB_YR_CASE(22) IXB_YR_CASE(23) IXB_YR_CASE(24)
+      IXB_YR_CASE(25) IXB_YR_CASE(26)
+#undef IXB_YR_CASE
+      default:
+        break;
+    }
     const uint32_t awarp = smem_u32(A + st * kATile + warp * 32 * 128);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
