@@ -257,7 +257,7 @@ def test_cfg2_full_size_slab_vs_oracle(P, ixo):
     assert rel <= 1e-3
 
 
-@pytest.mark.parametrize("nchunks", [1, 3, 8])
+@pytest.mark.parametrize("nchunks", [0, 1, 3, 8])  # 0: automatic
 def test_host_buffer_pipeline_bit_identical(P, ixo, nchunks):
     """ixb_spmm_blockgroupcoo_host (host buffers, chunked H2D/kernel/D2H on
     three streams) equals the device-buffer call bit for bit on integer
@@ -304,7 +304,7 @@ def test_host_buffer_pipeline_groupcoo_and_unsorted(P, ixo):
     AM, AK = torch.from_numpy(f["AM"]).int(), torch.from_numpy(f["AK"]).int()
     AV, B = torch.from_numpy(f["AV"]).float(), torch.from_numpy(Bn).float()
     want = torch.from_numpy(A.astype(np.float32) @ Bn.astype(np.float32))
-    for nch in (1, 5):
+    for nch in (0, 1, 5):  # 0: automatic
         out = torch.empty(300, 64)
         P.spmm_groupcoo_host(AM, AK, AV, B, out, accumulate=False, nchunks=nch)
         assert torch.equal(out, want)
