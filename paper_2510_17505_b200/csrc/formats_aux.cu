@@ -104,8 +104,11 @@ extern "C" int ixb_mask_real_count(const uint8_t* mask, int64_t slots, ixb_strea
     mask_count_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(mask, slots, acc.p);
     IXB_LAUNCH_CHECK("mask_count_kernel");
     unsigned long long h = 0;
-    IXB_CUDA_CHECK(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
-    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    {
+      HostReads rd(s);
+      rd.add(&h, acc.p, 8);
+      rd.wait();
+    }
     *real = static_cast<int64_t>(h);
   });
 }
@@ -122,8 +125,11 @@ extern "C" int ixb_is_ell(const int32_t* group_coord, int64_t G, ixb_stream stre
         group_coord, G, flag.p);
     IXB_LAUNCH_CHECK("adjacent_equal_kernel");
     int h = 0;
-    IXB_CUDA_CHECK(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, s));
-    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    {
+      HostReads rd(s);
+      rd.add(&h, flag.p, 4);
+      rd.wait();
+    }
     *is_ell = h ? 0 : 1;
   });
 }
@@ -146,8 +152,11 @@ extern "C" int ixb_max_occupancy(const int32_t* coord, int64_t nnz, int64_t exte
     max_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(occ.p, extent, res.p);
     IXB_LAUNCH_CHECK("max_kernel");
     int h[2] = {0, 0};
-    IXB_CUDA_CHECK(cudaMemcpyAsync(h, res.p, 8, cudaMemcpyDeviceToHost, s));
-    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    {
+      HostReads rd(s);
+      rd.add(h, res.p, 8);
+      rd.wait();
+    }
     if (h[1]) fail(IXB_SHAPE, "occupancy: coordinate out of range");
     *max_occ = h[0];
   });

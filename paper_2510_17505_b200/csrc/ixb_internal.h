@@ -69,6 +69,25 @@ struct OperandInfo {
 };
 void check_error_record(cudaStream_t stream, const OperandInfo* ops, int nops);
 
+// Small device->host reads of a plan phase through one pinned staging
+// buffer per host thread: every add() is queued on `stream`, wait() syncs
+// once and copies the values out (a pageable destination would make each
+// read its own staged, host-blocking round trip). Reads past the buffer's
+// 4 KB go straight to their destination.
+class HostReads {
+ public:
+  explicit HostReads(cudaStream_t stream) : s_(stream) {}
+  void add(void* dst, const void* src, size_t bytes);
+  void wait();
+
+ private:
+  cudaStream_t s_;
+  size_t used_ = 0;
+  struct Item { void* dst; size_t off, bytes; };
+  Item items_[16];
+  int n_ = 0;
+};
+
 // Stream-ordered scratch allocation (cudaMallocAsync pool).
 void* scratch_alloc(size_t bytes, cudaStream_t stream);
 void scratch_free(void* p, cudaStream_t stream);

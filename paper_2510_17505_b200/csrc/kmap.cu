@@ -380,8 +380,9 @@ int ixb_kernel_map_plan(const int32_t* coords, int64_t n, ixb_stream stream, ixb
                     256, 0, s>>>(coords, n, bbd.p);
       IXB_LAUNCH_CHECK("bbox_kernel");
       int bb[7];
-      IXB_CUDA_CHECK(cudaMemcpyAsync(bb, bbd.p, sizeof bb, cudaMemcpyDeviceToHost, s));
-      IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+      HostReads rd(s);
+      rd.add(bb, bbd.p, sizeof bb);
+      rd.wait();
       for (int d = 0; d < 3; ++d)  // the hash key's range (hash_insert checks the same)
         if (bb[d] < -kBias + 1 || bb[3 + d] >= kBias - 1)
           fail(IXB_SHAPE, "kernel map: voxel coordinate outside [-2^20, 2^20)");
@@ -437,12 +438,13 @@ int ixb_kernel_map_plan(const int32_t* coords, int64_t n, ixb_stream stream, ixb
     }
     int hflags[2] = {0, 0};
     int32_t last_base = 0, last_cnt = 0;
-    IXB_CUDA_CHECK(cudaMemcpyAsync(hflags, flags.p, sizeof hflags, cudaMemcpyDeviceToHost, s));
+    HostReads rd(s);
+    rd.add(hflags, flags.p, sizeof hflags);
     if (n > 0) {
-      IXB_CUDA_CHECK(cudaMemcpyAsync(&last_base, P.base.p + T - 1, 4, cudaMemcpyDeviceToHost, s));
-      IXB_CUDA_CHECK(cudaMemcpyAsync(&last_cnt, cnt.p + T - 1, 4, cudaMemcpyDeviceToHost, s));
+      rd.add(&last_base, P.base.p + T - 1, 4);
+      rd.add(&last_cnt, cnt.p + T - 1, 4);
     }
-    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    rd.wait();
     if (hflags[1]) fail(IXB_SHAPE, "kernel map: voxel coordinate outside [-2^20, 2^20)");
     if (hflags[0]) fail(IXB_SHAPE, "kernel map: duplicate voxel coordinates");
     P.pairs = static_cast<int64_t>(last_base) + last_cnt;

@@ -172,8 +172,9 @@ int64_t tune_from_occ(const int32_t* occ, int64_t n, int64_t extent, int count_e
     IXB_LAUNCH_CHECK("occ_stats_kernel");
   }
   OccStats h;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
-  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  HostReads rd(s);
+  rd.add(&h, d.p, sizeof h);
+  rd.wait();
   if (total_out) *total_out = static_cast<int64_t>(h.S);
   if (maxocc_out) *maxocc_out = static_cast<int64_t>(h.maxocc);
   return choose_group_size(h, extent, count_empty_rows, gstar_out, cand_g, cand_score, ncand);
@@ -1062,8 +1063,9 @@ __global__ void __launch_bounds__(1024) tune_scan_kernel(const int32_t* occ, int
 
 int64_t read_scan_total(const int32_t* out, int64_t n, cudaStream_t s) {
   int32_t total = 0;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&total, out + n, 4, cudaMemcpyDeviceToHost, s));
-  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  HostReads rd(s);
+  rd.add(&total, out + n, 4);
+  rd.wait();
   // counts are non-negative, so a negative int32 total means it wrapped past 2^31
   if (total < 0) fail(IXB_SHAPE, "format exceeds 2^31 entries");
   return total;
@@ -1080,9 +1082,10 @@ bool tune_and_scan(const int32_t* counts, int64_t n, int64_t extent, int count_e
   IXB_LAUNCH_CHECK("tune_scan_kernel");
   int64_t h[2];
   int32_t total = 0;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(h, res.p, sizeof h, cudaMemcpyDeviceToHost, s));
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&total, out + n, 4, cudaMemcpyDeviceToHost, s));
-  IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+  HostReads rd(s);
+  rd.add(h, res.p, sizeof h);
+  rd.add(&total, out + n, 4);
+  rd.wait();
   if (total < 0 || h[1] > INT32_MAX) fail(IXB_SHAPE, "format exceeds 2^31 entries");
   *g = h[0];
   if (S) *S = h[1];
@@ -1214,8 +1217,9 @@ void plan_sorted_runs(ixb_pack* P, bool identity_order, int64_t g_req, int64_t e
                                                  static_cast<int>(n), s));
     note_launch();
     int32_t R = 0;
-    IXB_CUDA_CHECK(cudaMemcpyAsync(&R, P->run_incl.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    IXB_CUDA_CHECK(cudaStreamSynchronize(s));
+    HostReads rd(s);
+    rd.add(&R, P->run_incl.p + n - 1, 4);
+    rd.wait();
     P->R = R;
   }
   const int64_t R = P->R;

@@ -124,15 +124,46 @@ void* stream_buffer(cudaStream_t stream, size_t bytes, int tag) {
   return b.first;
 }
 
+namespace {
+constexpr size_t kPinnedBytes = 4096;
+thread_local char* t_pinned = nullptr;
+char* pinned_staging() {
+  if (!t_pinned) {
+    void* p = nullptr;
+    cuda_check(cudaMallocHost(&p, kPinnedBytes), "cudaMallocHost(staging)");
+    t_pinned = static_cast<char*>(p);
+  }
+  return t_pinned;
+}
+}  // namespace
+
+void HostReads::add(void* dst, const void* src, size_t bytes) {
+  const size_t off = (used_ + 15) & ~size_t(15);
+  if (off + bytes > kPinnedBytes || n_ == 16) {
+    IXB_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s_));
+    return;
+  }
+  IXB_CUDA_CHECK(cudaMemcpyAsync(pinned_staging() + off, src, bytes, cudaMemcpyDeviceToHost, s_));
+  items_[n_++] = {dst, off, bytes};
+  used_ = off + bytes;
+}
+
+void HostReads::wait() {
+  IXB_CUDA_CHECK(cudaStreamSynchronize(s_));
+  for (int i = 0; i < n_; ++i) std::memcpy(items_[i].dst, t_pinned + items_[i].off, items_[i].bytes);
+  n_ = 0;
+  used_ = 0;
+}
+
 void reset_error_record(cudaStream_t stream) {
   IXB_CUDA_CHECK(cudaMemsetAsync(&ctx().rec->key, 0xff, sizeof(unsigned long long), stream));
 }
 
 void check_error_record(cudaStream_t stream, const OperandInfo* ops, int nops) {
   unsigned long long key = kNoError;
-  IXB_CUDA_CHECK(cudaMemcpyAsync(&key, &ctx().rec->key, sizeof key, cudaMemcpyDeviceToHost,
-                                 stream));
-  IXB_CUDA_CHECK(cudaStreamSynchronize(stream));
+  HostReads rd(stream);
+  rd.add(&key, &ctx().rec->key, sizeof key);
+  rd.wait();
   if (key == kNoError) return;
   int op = static_cast<int>(key >> 56);
   int64_t pos = static_cast<int64_t>(key & ((1ull << 56) - 1));
