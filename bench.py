@@ -155,21 +155,20 @@ def dist_env():
 
 
 # ------------------------------------------------------------- workloads
-def time_builder(torch, fn, reps=2):
+def time_builder(torch, fn, reps=10):
     """Wall time of a format-builder call (its plan phase syncs the host for
     the output sizes, so CUDA events would miss nothing but the host part):
-    one warm call, then the best of `reps` synchronised calls. Returns
-    (result, ms)."""
+    one warm call, then `reps` synchronised calls. Returns (result, ms) with
+    ms = {"best": min, "median": median} over the reps."""
     out = fn()
-    best = None
+    ts = []
     for _ in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = fn()
         torch.cuda.synchronize()
-        ms = (time.perf_counter() - t0) * 1e3
-        best = ms if best is None else min(best, ms)
-    return out, best
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return out, {"best": min(ts), "median": statistics.median(ts)}
 
 
 class GroupCooWorkload:
@@ -203,7 +202,8 @@ class GroupCooWorkload:
         slots = self.G * self.g
         # builder: dense read (compulsory once; the kernels read it twice: count + pack)
         # + format written (AM, AK, AV, mask)
-        self.builder = {"name": "K1 dense_to_groupcoo (+tuner)", "ms": build_ms,
+        self.builder = {"name": "K1 dense_to_groupcoo (+tuner)", "ms": build_ms["best"],
+                        "ms_median": build_ms["median"],
                         "compulsory_bytes": self.M * self.K * 4 + self.G * 4 + slots * 9,
                         "passes_over_dense": 2}
         del Ad
@@ -327,7 +327,8 @@ class BlockGroupCooWorkload:
             self.M * self.N * 4
         self.tc_flops = 2.0 * self.nblk * b * b * self.N
         # builder: dense read once + present blocks re-read + format written
-        self.builder = {"name": "K2 dense_to_blockgroupcoo (+tuner)", "ms": build_ms,
+        self.builder = {"name": "K2 dense_to_blockgroupcoo (+tuner)", "ms": build_ms["best"],
+                        "ms_median": build_ms["median"],
                         "compulsory_bytes": self.M * self.K * 2 + self.nblk * b * b * 2 +
                         slots * (b * b * 2 + 4 + 1) + self.G * 4, "passes_over_dense": 1}
         self.mma_count = slots * (self.N // 128)  # one M=128 (n) x N=16 (bm) UMMA per slot per n tile
@@ -549,13 +550,14 @@ class SparseConvWorkload:
         tile_off = int(torch.unique((mo // 128).long() * 27 + mz.long()).numel())
         self.l2_bytes = pairs * 128 + tile_off * 64 * 64 * 2 + n * 28 * 4 + n * 64 * 4
         self.tc_flops = self.flops
-        self.builder = {"name": "K5 kernel_map + tuner + group_coo_tensor", "ms": build_ms,
+        self.builder = {"name": "K5 kernel_map + tuner + group_coo_tensor", "ms": build_ms["best"],
+                        "ms_median": build_ms["median"],
                         # coords read + hash table (2 x 8 B per slot) + pairs written (3 x 4 B)
                         # + grouped map written (MAPZ, MAPX, MAPY, MAPV)
                         "compulsory_bytes": n * 12 + 2 * n * 8 + pairs * 12 + G * 4 +
                         G * g * 12, "passes_over_dense": None}
         self.info = {"voxels": n, "pairs": pairs, "kappa": pairs / n, "G": G, "g": g,
-                     "kernel_map_and_group_ms": build_ms, "plan_ms": plan_ms}
+                     "kernel_map_and_group_ms": build_ms["best"], "plan_ms": plan_ms}
         self.h_in = [self.In.cpu().pin_memory()]
         self.h_out = torch.empty_like(self.Out, device="cpu").pin_memory()
         self.d_in = [torch.empty_like(self.In)]
@@ -866,8 +868,8 @@ def builder_record(wl):
     b = dict(wl.builder)
     gbps = b["compulsory_bytes"] / (b["ms"] * 1e-3) / 1e9
     b.update({"workload": wl.name, "achieved_GBps": gbps, "hbm_frac": gbps / hbm,
-              "timing": "wall time of the API call (warm, best of 2; its plan phase syncs "
-                        "the host for the output sizes)"})
+              "timing": "wall time of the API call (warm, best of 10, median beside it; its plan "
+                        "phase syncs the host for the output sizes)"})
     return b
 
 
