@@ -546,30 +546,48 @@ struct RunPackArgs {
   int32_t* gout;  // group coordinate output [G]
 };
 
-// kPackElems consecutive-by-stride entries per thread: their independent
-// loads are in flight together.
+// kPackElems consecutive-by-stride entries per thread, in two phases: every
+// load of the thread's entries is issued before any store (the outputs may
+// alias the inputs as far as the compiler knows, so interleaved load/store
+// pairs would serialise each entry's loads behind the previous stores).
 constexpr int kPackElems = 4;
+constexpr int kMaxMembers = 8;
 __global__ void __launch_bounds__(kTB) run_pack_elems(RunPackArgs a) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTB * kPackElems + threadIdx.x;
+  int64_t slot[kPackElems];
+  int32_t mc[kPackElems][kMaxMembers];
+  unsigned long long v[kPackElems];
 #pragma unroll
   for (int u = 0; u < kPackElems; ++u) {
     const int64_t i = i0 + u * kTB;
-    if (i >= a.n) break;
-    // runs by rank (run_incl) or, for canonical small-extent input, by value
-    const int64_t r = a.run_incl ? a.run_incl[i] - 1 : a.gcoord[i];
-    const int64_t k = i - a.start[r];
-    const int64_t slot = static_cast<int64_t>(a.gofs[r]) * a.g + k;  // = (gofs + k / g) * g + k % g
-    const int64_t src = a.perm ? a.perm[i] : i;
-    for (int m = 0; m < a.nm; ++m) a.mout[m][slot] = a.mcoord[m][src];
-    if (a.vbytes == 8) {
-      static_cast<unsigned long long*>(a.vout)[slot] =
-          static_cast<const unsigned long long*>(a.vals)[src];
-    } else if (a.vbytes == 4) {
-      static_cast<float*>(a.vout)[slot] = static_cast<const float*>(a.vals)[src];
-    } else if (a.vbytes == 2) {
-      static_cast<__nv_bfloat16*>(a.vout)[slot] = static_cast<const __nv_bfloat16*>(a.vals)[src];
+    slot[u] = -1;
+    if (i < a.n) {
+      // runs by rank (run_incl) or, for canonical small-extent input, by value
+      const int64_t r = a.run_incl ? a.run_incl[i] - 1 : a.gcoord[i];
+      const int64_t k = i - a.start[r];
+      slot[u] = static_cast<int64_t>(a.gofs[r]) * a.g + k;  // = (gofs + k / g) * g + k % g
+      const int64_t src = a.perm ? a.perm[i] : i;
+#pragma unroll
+      for (int m = 0; m < kMaxMembers; ++m)
+        if (m < a.nm) mc[u][m] = a.mcoord[m][src];
+      if (a.vbytes == 8) v[u] = static_cast<const unsigned long long*>(a.vals)[src];
+      else if (a.vbytes == 4) v[u] = __float_as_uint(static_cast<const float*>(a.vals)[src]);
+      else if (a.vbytes == 2)
+        v[u] = static_cast<const unsigned short*>(a.vals)[src];  // bf16 bits
     }
-    if (a.mask) a.mask[slot] = 1;
+  }
+#pragma unroll
+  for (int u = 0; u < kPackElems; ++u) {
+    if (slot[u] < 0) continue;
+    const int64_t sl = slot[u];
+#pragma unroll
+    for (int m = 0; m < kMaxMembers; ++m)
+      if (m < a.nm) a.mout[m][sl] = mc[u][m];
+    if (a.vbytes == 8) static_cast<unsigned long long*>(a.vout)[sl] = v[u];
+    else if (a.vbytes == 4) static_cast<unsigned*>(a.vout)[sl] = static_cast<unsigned>(v[u]);
+    else if (a.vbytes == 2)
+      static_cast<unsigned short*>(a.vout)[sl] = static_cast<unsigned short>(v[u]);
+    if (a.mask) a.mask[sl] = 1;
   }
 }
 
